@@ -1,0 +1,34 @@
+# Build the sm_100a traversal library and the CPU oracle.
+#   make            -> paper_2103_02309_b200/libtetb200.so + oracle/libtetoracle.so
+#   make ref        -> oracle/_ref/_kernels*.so (reference compiled kernels; needs /root/reference)
+NVCC ?= nvcc
+CC ?= gcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+# Exactness flags: no FMA contraction, IEEE division/sqrt, no denormal flush
+# (the reference is built with -ffp-contract=off, pkg/setup.py:17-20).
+NVFLAGS := $(ARCH) -O3 -std=c++17 -lineinfo -fmad=false -ftz=false -prec-div=true -prec-sqrt=true \
+           -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+PKG := paper_2103_02309_b200
+LIB := $(PKG)/libtetb200.so
+ORACLE := oracle/libtetoracle.so
+CSRC := $(PKG)/csrc/tetb200.cu
+CHDR := $(PKG)/csrc/traverse.cuh $(PKG)/csrc/sctp.cuh include/tetb200.h
+
+all: $(LIB) $(ORACLE)
+
+$(LIB): $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)
+
+$(ORACLE): oracle/tetoracle.c oracle/tetoracle.h
+	$(CC) -O3 -ffp-contract=off -fno-fast-math -fPIC -shared -pthread -Wall -o $@ oracle/tetoracle.c -lm
+
+ptxas: $(CSRC) $(CHDR)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o /tmp/tetb200.o $(CSRC)
+
+ref:
+	./oracle/build_ref.sh
+
+clean:
+	rm -f $(LIB) $(ORACLE)
+
+.PHONY: all ref clean ptxas

@@ -1,0 +1,163 @@
+/*
+ * tetb200.h -- C ABI of the B200-native tetrahedral-mesh ray traversal engine.
+ *
+ * This is the drop-in boundary for the reference package's "kernel module"
+ * protocol (BACKEND_NAME / cast_rays / locate_points / shadow_rays,
+ * /root/reference/pkg/src/tetray/_kernels.pyx:15,271,416,527, selected by
+ * backend.get_kernels, backend.py:35-45, and passed as `kernels=` by every
+ * batch entry point, batch.py:45,84,140,152).  Plain pointers and sizes only:
+ * no torch or numpy types cross this boundary.
+ *
+ * Pointer conventions
+ *   - tb_mesh_create / tb_mesh_create_tet80: HOST pointers (the mesh is copied
+ *     into HBM once and is immutable afterwards).
+ *   - tb_cast_rays, tb_cast_rays_visits, tb_locate_points, tb_shadow_rays,
+ *     tb_sctp_cast_rays: DEVICE pointers on the mesh's device, enqueued on
+ *     `stream` (a cudaStream_t; NULL = legacy default stream).  Nothing is
+ *     synchronised; the caller owns ordering.
+ *   - *_host variants: HOST pointers (pageable or pinned); the call stages
+ *     the inputs to HBM, launches, copies the outputs back and synchronises.
+ *
+ * Errors: every function returns 0 on success and a negative TB_E* code on
+ * failure; tb_last_error() returns a thread-local message for the last
+ * failure on the calling thread.  Per-ray problems are not errors: they are
+ * reported through the per-ray status (TB_STATUS_ERROR = the reference's
+ * cycle guard, _kernels.pyx:365-368).
+ *
+ * Thread safety: a tb_mesh is immutable after creation; concurrent calls on
+ * the same mesh from several host threads are allowed (the reference's tile
+ * pool calls cast_rays concurrently, render.py:538-541).
+ */
+#ifndef TETB200_H
+#define TETB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TB_ABI_VERSION 1
+
+/* Record layouts (tetmesh.py:34-46); 80 = TetMesh-80 (4 ids + 4 refs + 4
+ * inline float3 vertices, no separate point fetch; not in the reference). */
+#define TB_LAYOUT_TET32 32
+#define TB_LAYOUT_TET20 20
+#define TB_LAYOUT_TET16 16
+#define TB_LAYOUT_TET80 80
+
+/* Per-ray status codes (_kernels.pyx:17-19). */
+#define TB_STATUS_MISS 0
+#define TB_STATUS_HIT 1
+#define TB_STATUS_ERROR 2
+
+/* Neighbour-reference encoding (tetmesh.py:29-32). */
+#define TB_CONSTRAINED_BIT 0x80000000u
+#define TB_PAYLOAD_MASK 0x7FFFFFFFu
+#define TB_BOUNDARY_REF 0x7FFFFFFFu
+
+/* Error codes. */
+#define TB_OK 0
+#define TB_E_ARG -1
+#define TB_E_CUDA -2
+#define TB_E_OOM -3
+#define TB_E_LAYOUT -4
+
+typedef struct tb_mesh tb_mesh;
+
+/* Upload a CompactMesh (tetmesh.py:147-195) to HBM on `device`.
+ * Replaces: the arrays _kernels.cast_rays reads per call
+ *   (_kernels.pyx:276-282: mesh.points, records_u32(), side_verts,
+ *   side_neighbors) plus what batch.cast_rays' epilogue reads
+ *   (batch.py:63-71: cf_triangle, cf_tets, triangle_coords()).
+ *   points_xyz      (n_points, 3) float32
+ *   records         (n_tets, layout/4) uint32 = CompactMesh.records_u32()
+ *   side_verts      (n_tets, 4) int32, ascending per row
+ *   side_neighbors  (n_tets, 4) uint32, sorted-slot references
+ *   cf_triangle     (n_cf,) int32      scene triangle per constrained face
+ *   cf_tets         (n_cf, 2) int32    [front, back], back = -1 on the hull
+ *   tri_coords      (n_tri, 3, 3) float64 = triangle_coords()
+ * layout is TB_LAYOUT_TET32/20/16 (records must match it) or TB_LAYOUT_TET80,
+ * for which `records` is ignored and the 80-byte records are built from the
+ * side tables and the points on the device. */
+int tb_mesh_create(int device, int layout, int64_t n_points, const float* points_xyz,
+                   int64_t n_tets, const uint32_t* records, const int32_t* side_verts,
+                   const uint32_t* side_neighbors, int64_t n_cf, const int32_t* cf_triangle,
+                   const int32_t* cf_tets, int64_t n_tri, const double* tri_coords,
+                   tb_mesh** out);
+int tb_mesh_destroy(tb_mesh* mesh);
+/* Bytes of HBM the mesh occupies, and the hot "accelerator" bytes
+ * (records + points, CompactMesh.accelerator_bytes, tetmesh.py:182-185). */
+int tb_mesh_info(const tb_mesh* mesh, int* device, int* layout, int64_t* n_points,
+                 int64_t* n_tets, int64_t* n_cf, int64_t* hbm_bytes, int64_t* hot_bytes);
+
+/* Batch traversal with the batch-layer epilogue fused.
+ * Replaces: _kernels.cast_rays (_kernels.pyx:271-370) -> (status, cf, tet,
+ *   visited), plus batch.cast_rays' host epilogue (batch.py:57-71 and
+ *   _kernels_py._mt_t, _kernels_py.py:435-454) -> (triangle, t, tet_back).
+ *   o, d     (n, 3) float32; start (n,) int32
+ *   status   (n,) uint8; cf, tet, visited (n,) int32
+ *   triangle (n,) int32, t (n,) float64, tet_back (n,) int32 -- each may be
+ *   NULL to skip that part of the epilogue.  Misses: triangle -1, t +inf,
+ *   tet_back -1.  Start tets are NOT range-checked on the device: the caller
+ *   validates them (the reference does not either). */
+int tb_cast_rays(tb_mesh* mesh, int64_t n, const float* o, const float* d, const int32_t* start,
+                 uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle,
+                 double* t, int32_t* tet_back, void* stream);
+int tb_cast_rays_host(tb_mesh* mesh, int64_t n, const float* o, const float* d,
+                      const int32_t* start, uint8_t* status, int32_t* cf, int32_t* tet,
+                      int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back);
+
+/* Visit-sequence recording (the visits_sink path of _kernels.pyx:307-341,
+ * consumed by batch.cast_rays_visits, batch.py:83-137).  Second pass of a
+ * two-pass scheme: `offsets` (n+1,) int64 is the exclusive scan of the
+ * `visited` output of a prior tb_cast_rays on the same rays; ray i's visited
+ * tets are written to seq[offsets[i] : offsets[i+1]] (start tet first). */
+int tb_cast_rays_visits(tb_mesh* mesh, int64_t n, const float* o, const float* d,
+                        const int32_t* start, const int64_t* offsets, int32_t* seq, void* stream);
+
+/* Batch point location.
+ * Replaces: _kernels.locate_points (_kernels.pyx:416-492).
+ *   q (n, 3) float64; hints (n,) int32; tet (n,) int32 (-1 = outside);
+ *   visited (n,) int32. */
+int tb_locate_points(tb_mesh* mesh, int64_t n, const double* q, const int32_t* hints,
+                     int32_t* tet, int32_t* visited, void* stream);
+int tb_locate_points_host(tb_mesh* mesh, int64_t n, const double* q, const int32_t* hints,
+                          int32_t* tet, int32_t* visited);
+
+/* Batch occlusion (shadow) walks.
+ * Replaces: _kernels.shadow_rays (_kernels.pyx:527-614).
+ *   p (n, 3) float64; light (n,3) float64 when light_stride == 3, or a single
+ *   (3,) point when light_stride == 0; p_tet (n,) int32; light_tet (n,) int32
+ *   when light_tet_stride == 1 or a single value when 0; occluded (n,) uint8;
+ *   visited (n,) int32. */
+int tb_shadow_rays(tb_mesh* mesh, int64_t n, const double* p, const double* light,
+                   int light_stride, const int32_t* p_tet, const int32_t* light_tet,
+                   int light_tet_stride, double eps, uint8_t* occluded, int32_t* visited,
+                   void* stream);
+int tb_shadow_rays_host(tb_mesh* mesh, int64_t n, const double* p, const double* light,
+                        int light_stride, const int32_t* p_tet, const int32_t* light_tet,
+                        int light_tet_stride, double eps, uint8_t* occluded, int32_t* visited);
+
+/* Fallback traversal with the fp64 scalar-triple-product exit test (ScTP).
+ * Replaces: traversal.sctp_exit_face (traversal.py:484-511) applied per tet
+ * (the reference has the predicate only, no walk).  Same
+ * outputs and epilogue as tb_cast_rays. */
+int tb_sctp_cast_rays(tb_mesh* mesh, int64_t n, const float* o, const float* d,
+                      const int32_t* start, uint8_t* status, int32_t* cf, int32_t* tet,
+                      int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back,
+                      void* stream);
+
+/* Pinned host memory helpers for end-to-end callers. */
+int tb_host_alloc(size_t bytes, void** out);
+int tb_host_free(void* ptr);
+
+const char* tb_last_error(void);
+int tb_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TETB200_H */

@@ -1,0 +1,79 @@
+"""ctypes binding of libtetb200.so (the C ABI in include/tetb200.h).
+
+The library is built in-tree (``make`` or ``__graft_entry__.build()``) and
+loaded from this package directory.  There is deliberately no fallback: if
+the library is missing the import fails loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_size_t, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("TETB200_LIB", os.path.join(_HERE, "libtetb200.so"))
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libtetb200.so not found at {LIB_PATH}: build it with `make` or "
+        "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)"
+    )
+
+lib = ctypes.CDLL(LIB_PATH)
+
+P = c_void_p  # every array argument is passed as a raw address
+
+_SIGS = {
+    "tb_abi_version": (c_int, []),
+    "tb_last_error": (c_char_p, []),
+    "tb_mesh_create": (
+        c_int,
+        [c_int, c_int, c_int64, P, c_int64, P, P, P, c_int64, P, P, c_int64, P, POINTER(c_void_p)],
+    ),
+    "tb_mesh_destroy": (c_int, [c_void_p]),
+    "tb_mesh_info": (
+        c_int,
+        [c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
+         POINTER(c_int64), POINTER(c_int64)],
+    ),
+    "tb_cast_rays": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),
+    "tb_cast_rays_host": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P]),
+    "tb_sctp_cast_rays": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),
+    "tb_cast_rays_visits": (c_int, [c_void_p, c_int64, P, P, P, P, P, c_void_p]),
+    "tb_locate_points": (c_int, [c_void_p, c_int64, P, P, P, P, c_void_p]),
+    "tb_locate_points_host": (c_int, [c_void_p, c_int64, P, P, P, P]),
+    "tb_shadow_rays": (c_int, [c_void_p, c_int64, P, P, c_int, P, P, c_int, c_double, P, P, c_void_p]),
+    "tb_shadow_rays_host": (c_int, [c_void_p, c_int64, P, P, c_int, P, P, c_int, c_double, P, P]),
+    "tb_host_alloc": (c_int, [c_size_t, POINTER(c_void_p)]),
+    "tb_host_free": (c_int, [c_void_p]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+if lib.tb_abi_version() != 1:
+    raise ImportError(f"libtetb200.so ABI {lib.tb_abi_version()} != 1; rebuild")
+
+
+class TetB200Error(RuntimeError):
+    """A C-ABI call failed (bad argument, CUDA error, out of memory)."""
+
+
+def check(code: int, what: str) -> None:
+    if code != 0:
+        msg = lib.tb_last_error()
+        raise TetB200Error(f"{what} failed ({code}): {msg.decode() if msg else 'unknown error'}")
+
+
+def addr(a) -> int | None:
+    """Raw address of a numpy array or torch tensor (None stays NULL)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data

@@ -1,0 +1,807 @@
+// tetb200.cu -- sm_100a kernels and the C ABI declared in include/tetb200.h.
+//
+// Hot path: batch.cast_rays -> _kernels.cast_rays
+// (/root/reference/pkg/src/tetray/batch.py:39-80, _kernels.pyx:271-370).
+// One lane per ray walks the compact xor-linked records of an HBM-resident
+// mesh; the host epilogue of batch.cast_rays (triangle id, fp64 t, back tet;
+// batch.py:57-71) is fused into the termination path.  See DESIGN.md.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/tetb200.h"
+#include "sctp.cuh"
+#include "traverse.cuh"
+
+using namespace tb;
+
+// ----------------------------------------------------------------------------
+// Error plumbing
+static thread_local std::string g_last_error;
+
+static int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define TB_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      return set_error(e_ == cudaErrorMemoryAllocation ? TB_E_OOM : TB_E_CUDA,         \
+                       "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                       __LINE__);                                                      \
+    }                                                                                  \
+  } while (0)
+
+struct tb_mesh {
+  int device = 0;
+  int layout = 0;
+  int64_t n_points = 0, n_tets = 0, n_cf = 0, n_tri = 0;
+  float4* pts = nullptr;
+  uint4* rec4 = nullptr;
+  uint32_t* vx = nullptr;
+  int4* sv = nullptr;
+  uint4* sn = nullptr;
+  int32_t* cf_tri = nullptr;
+  int2* cf_tets = nullptr;
+  double* tri = nullptr;
+  int64_t hbm_bytes = 0;
+  int64_t hot_bytes = 0;
+
+  MeshView view() const {
+    MeshView v;
+    v.pts = pts; v.rec4 = rec4; v.vx = vx; v.sv = sv; v.sn = sn;
+    v.cf_tri = cf_tri; v.cf_tets = cf_tets; v.tri = tri;
+    v.n_points = n_points; v.n_tets = n_tets;
+    return v;
+  }
+};
+
+namespace {
+
+constexpr int kBlock = 128;
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
+
+// ----------------------------------------------------------------------------
+// Mesh build kernels (run once per upload).
+__global__ void pad_points_kernel(const float* __restrict__ xyz, float4* __restrict__ out, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_float4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], 0.0f);
+}
+
+__global__ void split_tet20_kernel(const uint32_t* __restrict__ rec, uint32_t* __restrict__ vx,
+                                   uint4* __restrict__ nb, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    const uint32_t* r = rec + 5 * i;
+    vx[i] = r[0];
+    nb[i] = make_uint4(r[1], r[2], r[3], r[4]);
+  }
+}
+
+__global__ void build_tet80_kernel(const int4* __restrict__ sv, const uint4* __restrict__ sn,
+                                   const float4* __restrict__ pts, uint4* __restrict__ out, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int4 v = sv[i];
+  const float4 a = pts[v.x], b = pts[v.y], c = pts[v.z], d = pts[v.w];
+  uint4* o = out + 5 * i;
+  o[0] = make_uint4((uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w);
+  o[1] = sn[i];
+  o[2] = make_uint4(__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(a.z), __float_as_uint(b.x));
+  o[3] = make_uint4(__float_as_uint(b.y), __float_as_uint(b.z), __float_as_uint(c.x), __float_as_uint(c.y));
+  o[4] = make_uint4(__float_as_uint(c.z), __float_as_uint(d.x), __float_as_uint(d.y), __float_as_uint(d.z));
+}
+
+// ----------------------------------------------------------------------------
+// Shared termination + fused epilogue (batch.py:57-71).
+__device__ __forceinline__ void write_result(const MeshView& m, int64_t r, uint8_t st, uint32_t ref,
+                                             uint32_t cur, int vis, float o0, float o1, float o2,
+                                             float d0, float d1, float d2, uint8_t* status, int32_t* cf,
+                                             int32_t* tet, int32_t* visited, int32_t* triangle,
+                                             double* t, int32_t* tet_back) {
+  status[r] = st;
+  const int32_t cfi = (st == kHit) ? (int32_t)(ref & kPayload) : -1;
+  cf[r] = cfi;
+  tet[r] = (int32_t)cur;
+  visited[r] = vis;
+  if (triangle != nullptr || t != nullptr || tet_back != nullptr) {
+    int32_t tri = -1, back = -1;
+    double tt = INFINITY;
+    if (cfi >= 0) {
+      tri = __ldg(&m.cf_tri[cfi]);
+      if (t != nullptr)
+        tt = mt_t((double)o0, (double)o1, (double)o2, (double)d0, (double)d1, (double)d2,
+                  m.tri + 9 * (int64_t)tri);
+      const int2 ct = __ldg(&m.cf_tets[cfi]);
+      back = (ct.x == (int32_t)cur) ? ct.y : ct.x;
+    }
+    if (triangle != nullptr) triangle[r] = tri;
+    if (t != nullptr) t[r] = tt;
+    if (tet_back != nullptr) tet_back[r] = back;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Primary traversal kernel: one lane per ray, _kernels.pyx:343-369.
+template <int L>
+__global__ void __launch_bounds__(kBlock) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
+                                                      const float* __restrict__ d,
+                                                      const int32_t* __restrict__ start,
+                                                      uint8_t* __restrict__ status, int32_t* __restrict__ cf,
+                                                      int32_t* __restrict__ tet, int32_t* __restrict__ visited,
+                                                      int32_t* __restrict__ triangle, double* __restrict__ t,
+                                                      int32_t* __restrict__ tet_back) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const float o0 = __ldg(o + 3 * r), o1 = __ldg(o + 3 * r + 1), o2 = __ldg(o + 3 * r + 2);
+  const float d0 = __ldg(d + 3 * r), d1 = __ldg(d + 3 * r + 1), d2 = __ldg(d + 3 * r + 2);
+  uint32_t cur = (uint32_t)__ldg(start + r);
+  Basis b;
+  uint32_t idx[3];
+  float p[6];
+  const int j = init_ray(m, o0, o1, o2, d0, d1, d2, (int)cur, b, idx, p);
+  uint32_t ref = pick4u(__ldg(&m.sn[cur]), j);
+  uint32_t prev = cur;
+  int vis = 1;
+  uint8_t st;
+  const uint32_t n_tets = (uint32_t)m.n_tets;
+  while (true) {
+    if (ref == kBoundary) { st = kMiss; break; }
+    if (ref & kConstrained) { st = kHit; break; }
+    const uint32_t nxt = ref & kPayload;
+    if (nxt >= n_tets) { st = kError; break; }  // corrupt reference: fail the ray, never fault
+    ref = advance<L>(m, b, idx, p, nxt, prev);
+    prev = nxt;
+    cur = nxt;
+    ++vis;
+    if ((uint32_t)vis > n_tets) { st = kError; break; }  // cycle guard, _kernels.pyx:365-368
+  }
+  write_result(m, r, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
+               tet_back);
+}
+
+// Visit-sequence recorder (second pass; offsets from a prior cast), _kernels.pyx:307-341.
+template <int L>
+__global__ void __launch_bounds__(kBlock) visits_kernel(MeshView m, int64_t n, const float* __restrict__ o,
+                                                        const float* __restrict__ d,
+                                                        const int32_t* __restrict__ start,
+                                                        const int64_t* __restrict__ offsets,
+                                                        int32_t* __restrict__ seq) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const float o0 = o[3 * r], o1 = o[3 * r + 1], o2 = o[3 * r + 2];
+  const float d0 = d[3 * r], d1 = d[3 * r + 1], d2 = d[3 * r + 2];
+  uint32_t cur = (uint32_t)start[r];
+  int64_t pos = offsets[r];
+  const int64_t end = offsets[r + 1];
+  Basis b;
+  uint32_t idx[3];
+  float p[6];
+  const int j = init_ray(m, o0, o1, o2, d0, d1, d2, (int)cur, b, idx, p);
+  uint32_t ref = pick4u(__ldg(&m.sn[cur]), j);
+  uint32_t prev = cur;
+  if (pos < end) seq[pos++] = (int32_t)cur;
+  int vis = 1;
+  const uint32_t n_tets = (uint32_t)m.n_tets;
+  while (pos < end) {
+    if (ref == kBoundary || (ref & kConstrained)) break;
+    const uint32_t nxt = ref & kPayload;
+    if (nxt >= n_tets) break;
+    ref = advance<L>(m, b, idx, p, nxt, prev);
+    prev = nxt;
+    cur = nxt;
+    ++vis;
+    seq[pos++] = (int32_t)cur;
+    if ((uint32_t)vis > n_tets) break;
+  }
+}
+
+// Point location, _kernels.pyx:416-492.
+template <int L>
+__global__ void __launch_bounds__(kBlock) locate_kernel(MeshView m, int64_t n, const double* __restrict__ q,
+                                                        const int32_t* __restrict__ hints,
+                                                        int32_t* __restrict__ out, int32_t* __restrict__ visited) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const double qq[3] = {q[3 * r], q[3 * r + 1], q[3 * r + 2]};
+  uint32_t cur = (uint32_t)hints[r];
+  int32_t res = -1;
+  int vis = 1;
+  const uint32_t n_tets = (uint32_t)m.n_tets;
+  if (contains(m, cur, qq)) {
+    out[r] = (int32_t)cur;
+    visited[r] = 1;
+    return;
+  }
+  const int4 sv = __ldg(&m.sv[cur]);
+  const int vid[4] = {sv.x, sv.y, sv.z, sv.w};
+  double c[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float4 P = ldg_f4(&m.pts[vid[i]]);
+    c[0] = __dadd_rn(c[0], (double)P.x);
+    c[1] = __dadd_rn(c[1], (double)P.y);
+    c[2] = __dadd_rn(c[2], (double)P.z);
+  }
+  c[0] = __ddiv_rn(c[0], 4.0); c[1] = __ddiv_rn(c[1], 4.0); c[2] = __ddiv_rn(c[2], 4.0);
+  const float d0 = __double2float_rn(__dsub_rn(qq[0], c[0]));
+  const float d1 = __double2float_rn(__dsub_rn(qq[1], c[1]));
+  const float d2 = __double2float_rn(__dsub_rn(qq[2], c[2]));
+  if (d0 == 0.0f && d1 == 0.0f && d2 == 0.0f) {
+    out[r] = -1;
+    visited[r] = 1;
+    return;
+  }
+  const float o0 = __double2float_rn(c[0]), o1 = __double2float_rn(c[1]), o2 = __double2float_rn(c[2]);
+  Basis b;
+  uint32_t idx[3];
+  float p[6];
+  const int j = init_ray(m, o0, o1, o2, d0, d1, d2, (int)cur, b, idx, p);
+  uint32_t ref = pick4u(__ldg(&m.sn[cur]), j);
+  while (true) {
+    uint32_t nxt, entry;
+    if (ref == kBoundary) break;
+    if (ref & kConstrained) {
+      const int2 ct = __ldg(&m.cf_tets[ref & kPayload]);
+      const int32_t other = (ct.x == (int32_t)cur) ? ct.y : ct.x;
+      if (other < 0) break;
+      nxt = (uint32_t)other;
+      entry = ref;  // Tet16 xor partner is the tagged face ref
+    } else {
+      nxt = ref & kPayload;
+      entry = cur;
+    }
+    if (nxt >= n_tets) break;
+    ref = advance<L>(m, b, idx, p, nxt, entry);
+    cur = nxt;
+    ++vis;
+    if (contains(m, nxt, qq)) { res = (int32_t)nxt; break; }
+    if ((uint32_t)vis > n_tets) break;
+  }
+  out[r] = res;
+  visited[r] = vis;
+}
+
+// Occlusion walks, _kernels.pyx:527-614.
+template <int L>
+__global__ void __launch_bounds__(kBlock) shadow_kernel(MeshView m, int64_t n, const double* __restrict__ p,
+                                                        const double* __restrict__ light, int light_stride,
+                                                        const int32_t* __restrict__ p_tet,
+                                                        const int32_t* __restrict__ light_tet, int lt_stride,
+                                                        double eps, uint8_t* __restrict__ occ,
+                                                        int32_t* __restrict__ visited) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  uint32_t cur = (uint32_t)p_tet[r];
+  const int32_t ltet = light_tet[lt_stride * r];
+  int vis = 1;
+  uint8_t oc = 0;
+  if ((int32_t)cur == ltet) {
+    occ[r] = 0;
+    visited[r] = 1;
+    return;
+  }
+  const double* L3 = light + (int64_t)light_stride * r;
+  float o32[3], d32[3];
+  double o64[3], d64[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    d32[k] = __double2float_rn(__dsub_rn(L3[k], p[3 * r + k]));
+    o32[k] = __double2float_rn(p[3 * r + k]);
+    o64[k] = o32[k];
+    d64[k] = d32[k];
+  }
+  Basis b;
+  uint32_t idx[3];
+  float pw[6];
+  const int j = init_ray(m, o32[0], o32[1], o32[2], d32[0], d32[1], d32[2], (int)cur, b, idx, pw);
+  uint32_t ref = pick4u(__ldg(&m.sn[cur]), j);
+  const uint32_t n_tets = (uint32_t)m.n_tets;
+  const double one_m_eps = __dsub_rn(1.0, eps);
+  while (true) {
+    uint32_t nxt, entry;
+    if (ref == kBoundary) break;
+    if (ref & kConstrained) {
+      const uint32_t cfi = ref & kPayload;
+      const int32_t tri = __ldg(&m.cf_tri[cfi]);
+      const double tt = seg_tri_t(o64, d64, m.tri + 9 * (int64_t)tri);
+      if (tt >= one_m_eps) break;
+      if (tt > eps) { oc = 1; break; }
+      const int2 ct = __ldg(&m.cf_tets[cfi]);
+      const int32_t other = (ct.x == (int32_t)cur) ? ct.y : ct.x;
+      if (other < 0) break;
+      nxt = (uint32_t)other;
+      entry = ref;
+    } else {
+      nxt = ref & kPayload;
+      entry = cur;
+    }
+    if ((int32_t)nxt == ltet) break;
+    if (nxt >= n_tets) break;
+    ref = advance<L>(m, b, idx, pw, nxt, entry);
+    cur = nxt;
+    ++vis;
+    if ((uint32_t)vis > n_tets) break;
+  }
+  occ[r] = oc;
+  visited[r] = vis;
+}
+
+// ScTP fallback walk: fp64 scalar-triple-product exit test per tet
+// (traversal.sctp_exit_face, traversal.py:484-511) over the same xor-linked
+// records; the entry face is the one opposite the recovered vertex i3.
+template <int L>
+__global__ void __launch_bounds__(kBlock) sctp_kernel(MeshView m, int64_t n, const float* __restrict__ o,
+                                                      const float* __restrict__ d,
+                                                      const int32_t* __restrict__ start,
+                                                      uint8_t* __restrict__ status, int32_t* __restrict__ cf,
+                                                      int32_t* __restrict__ tet, int32_t* __restrict__ visited,
+                                                      int32_t* __restrict__ triangle, double* __restrict__ t,
+                                                      int32_t* __restrict__ tet_back) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const float o0 = o[3 * r], o1 = o[3 * r + 1], o2 = o[3 * r + 2];
+  const float d0 = d[3 * r], d1 = d[3 * r + 1], d2 = d[3 * r + 2];
+  const double O[3] = {o0, o1, o2};
+  const double D[3] = {d0, d1, d2};
+  uint32_t cur = (uint32_t)start[r];
+  SctpWindow w;
+  const int4 qd = __ldg(&m.sv[cur]);
+  const uint32_t ids[4] = {(uint32_t)qd.x, (uint32_t)qd.y, (uint32_t)qd.z, (uint32_t)qd.w};
+  float4 P[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) P[i] = ldg_f4(&m.pts[ids[i]]);
+  const int j = sctp_exit(P, ids, O, D, -1);
+  w.drop(P, ids, j);
+  uint32_t ref = pick4u(__ldg(&m.sn[cur]), j);
+  uint32_t prev = cur;
+  int vis = 1;
+  uint8_t st;
+  const uint32_t n_tets = (uint32_t)m.n_tets;
+  while (true) {
+    if (ref == kBoundary) { st = kMiss; break; }
+    if (ref & kConstrained) { st = kHit; break; }
+    const uint32_t nxt = ref & kPayload;
+    if (nxt >= n_tets) { st = kError; break; }
+    ref = sctp_advance<L>(m, w, O, D, nxt, prev);
+    prev = nxt;
+    cur = nxt;
+    ++vis;
+    if ((uint32_t)vis > n_tets) { st = kError; break; }
+  }
+  write_result(m, r, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
+               tet_back);
+}
+
+// Layout dispatch helper.
+template <template <int> class K, typename... Args>
+int launch_layout(int layout, unsigned grid, cudaStream_t s, Args... args) {
+  switch (layout) {
+    case 16: K<16>::launch(grid, s, args...); break;
+    case 20: K<20>::launch(grid, s, args...); break;
+    case 32: K<32>::launch(grid, s, args...); break;
+    case 80: K<80>::launch(grid, s, args...); break;
+    default: return set_error(TB_E_LAYOUT, "unsupported layout %d", layout);
+  }
+  return TB_OK;
+}
+
+template <int L>
+struct CastL {
+  template <typename... A>
+  static void launch(unsigned g, cudaStream_t s, A... a) { cast_kernel<L><<<g, kBlock, 0, s>>>(a...); }
+};
+template <int L>
+struct VisitsL {
+  template <typename... A>
+  static void launch(unsigned g, cudaStream_t s, A... a) { visits_kernel<L><<<g, kBlock, 0, s>>>(a...); }
+};
+template <int L>
+struct LocateL {
+  template <typename... A>
+  static void launch(unsigned g, cudaStream_t s, A... a) { locate_kernel<L><<<g, kBlock, 0, s>>>(a...); }
+};
+template <int L>
+struct ShadowL {
+  template <typename... A>
+  static void launch(unsigned g, cudaStream_t s, A... a) { shadow_kernel<L><<<g, kBlock, 0, s>>>(a...); }
+};
+template <int L>
+struct SctpL {
+  template <typename... A>
+  static void launch(unsigned g, cudaStream_t s, A... a) { sctp_kernel<L><<<g, kBlock, 0, s>>>(a...); }
+};
+
+int check_mesh(const tb_mesh* m) {
+  if (m == nullptr) return set_error(TB_E_ARG, "mesh handle is NULL");
+  return TB_OK;
+}
+
+// Stream-ordered scratch for the *_host entry points.
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+extern "C" {
+
+int tb_abi_version(void) { return TB_ABI_VERSION; }
+
+const char* tb_last_error(void) { return g_last_error.c_str(); }
+
+int tb_mesh_create(int device, int layout, int64_t n_points, const float* points_xyz, int64_t n_tets,
+                   const uint32_t* records, const int32_t* side_verts, const uint32_t* side_neighbors,
+                   int64_t n_cf, const int32_t* cf_triangle, const int32_t* cf_tets, int64_t n_tri,
+                   const double* tri_coords, tb_mesh** out) {
+  if (out == nullptr) return set_error(TB_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (layout != 16 && layout != 20 && layout != 32 && layout != 80)
+    return set_error(TB_E_LAYOUT, "unknown layout %d (expected 16, 20, 32 or 80)", layout);
+  if (n_points <= 0 || n_tets <= 0 || n_cf < 0 || n_tri < 0)
+    return set_error(TB_E_ARG, "bad sizes n_points=%lld n_tets=%lld n_cf=%lld n_tri=%lld",
+                     (long long)n_points, (long long)n_tets, (long long)n_cf, (long long)n_tri);
+  if (n_tets >= (int64_t)0x7FFFFFFF || n_points >= (int64_t)0x7FFFFFFF)
+    return set_error(TB_E_ARG, "mesh too large for 31-bit references");
+  if (!points_xyz || !side_verts || !side_neighbors || (layout != 80 && !records))
+    return set_error(TB_E_ARG, "NULL mesh array");
+  if (n_cf > 0 && (!cf_triangle || !cf_tets)) return set_error(TB_E_ARG, "NULL constrained-face array");
+  if (n_tri > 0 && !tri_coords) return set_error(TB_E_ARG, "NULL triangle coordinates");
+  int ndev = 0;
+  TB_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return set_error(TB_E_ARG, "device %d out of range (%d)", device, ndev);
+  DeviceGuard g(device);
+
+  tb_mesh* m = new tb_mesh();
+  m->device = device;
+  m->layout = layout;
+  m->n_points = n_points;
+  m->n_tets = n_tets;
+  m->n_cf = n_cf;
+  m->n_tri = n_tri;
+  auto fail = [&](int code) {
+    tb_mesh_destroy(m);
+    return code;
+  };
+#define TB_MC(call)                                                                      \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(set_error(e_ == cudaErrorMemoryAllocation ? TB_E_OOM : TB_E_CUDA,      \
+                            "%s failed: %s", #call, cudaGetErrorString(e_)));            \
+  } while (0)
+
+  float* tmp_xyz = nullptr;
+  TB_MC(cudaMalloc(&m->pts, n_points * sizeof(float4)));
+  TB_MC(cudaMalloc(&tmp_xyz, n_points * 3 * sizeof(float)));
+  TB_MC(cudaMemcpy(tmp_xyz, points_xyz, n_points * 3 * sizeof(float), cudaMemcpyHostToDevice));
+  pad_points_kernel<<<grid_for(n_points, 256), 256>>>(tmp_xyz, m->pts, n_points);
+  TB_MC(cudaGetLastError());
+  TB_MC(cudaDeviceSynchronize());
+  cudaFree(tmp_xyz);
+
+  TB_MC(cudaMalloc(&m->sv, n_tets * sizeof(int4)));
+  TB_MC(cudaMemcpy(m->sv, side_verts, n_tets * sizeof(int4), cudaMemcpyHostToDevice));
+  TB_MC(cudaMalloc(&m->sn, n_tets * sizeof(uint4)));
+  TB_MC(cudaMemcpy(m->sn, side_neighbors, n_tets * sizeof(uint4), cudaMemcpyHostToDevice));
+
+  int64_t rec_bytes = 0;
+  if (layout == 16) {
+    rec_bytes = n_tets * 16;
+    TB_MC(cudaMalloc(&m->rec4, rec_bytes));
+    TB_MC(cudaMemcpy(m->rec4, records, rec_bytes, cudaMemcpyHostToDevice));
+  } else if (layout == 32) {
+    rec_bytes = n_tets * 32;
+    TB_MC(cudaMalloc(&m->rec4, rec_bytes));
+    TB_MC(cudaMemcpy(m->rec4, records, rec_bytes, cudaMemcpyHostToDevice));
+  } else if (layout == 20) {
+    rec_bytes = n_tets * 20;
+    uint32_t* tmp = nullptr;
+    TB_MC(cudaMalloc(&m->vx, n_tets * sizeof(uint32_t)));
+    TB_MC(cudaMalloc(&m->rec4, n_tets * sizeof(uint4)));
+    TB_MC(cudaMalloc(&tmp, rec_bytes));
+    TB_MC(cudaMemcpy(tmp, records, rec_bytes, cudaMemcpyHostToDevice));
+    split_tet20_kernel<<<grid_for(n_tets, 256), 256>>>(tmp, m->vx, m->rec4, n_tets);
+    TB_MC(cudaGetLastError());
+    TB_MC(cudaDeviceSynchronize());
+    cudaFree(tmp);
+  } else {  // 80
+    rec_bytes = n_tets * 80;
+    TB_MC(cudaMalloc(&m->rec4, rec_bytes));
+    build_tet80_kernel<<<grid_for(n_tets, 256), 256>>>(m->sv, m->sn, m->pts, m->rec4, n_tets);
+    TB_MC(cudaGetLastError());
+    TB_MC(cudaDeviceSynchronize());
+  }
+
+  if (n_cf > 0) {
+    TB_MC(cudaMalloc(&m->cf_tri, n_cf * sizeof(int32_t)));
+    TB_MC(cudaMemcpy(m->cf_tri, cf_triangle, n_cf * sizeof(int32_t), cudaMemcpyHostToDevice));
+    TB_MC(cudaMalloc(&m->cf_tets, n_cf * sizeof(int2)));
+    TB_MC(cudaMemcpy(m->cf_tets, cf_tets, n_cf * sizeof(int2), cudaMemcpyHostToDevice));
+  }
+  if (n_tri > 0) {
+    TB_MC(cudaMalloc(&m->tri, n_tri * 9 * sizeof(double)));
+    TB_MC(cudaMemcpy(m->tri, tri_coords, n_tri * 9 * sizeof(double), cudaMemcpyHostToDevice));
+  }
+#undef TB_MC
+  m->hbm_bytes = n_points * 16 + n_tets * 32 + rec_bytes + n_cf * 12 + n_tri * 72;
+  // Hot accelerator bytes as the reference counts them (records + f32 xyz points).
+  m->hot_bytes = (layout == 80) ? rec_bytes : rec_bytes + n_points * 12;
+  *out = m;
+  return TB_OK;
+}
+
+int tb_mesh_destroy(tb_mesh* m) {
+  if (m == nullptr) return TB_OK;
+  DeviceGuard g(m->device);
+  cudaFree(m->pts);
+  cudaFree(m->rec4);
+  cudaFree(m->vx);
+  cudaFree(m->sv);
+  cudaFree(m->sn);
+  cudaFree(m->cf_tri);
+  cudaFree(m->cf_tets);
+  cudaFree(m->tri);
+  delete m;
+  return TB_OK;
+}
+
+int tb_mesh_info(const tb_mesh* m, int* device, int* layout, int64_t* n_points, int64_t* n_tets,
+                 int64_t* n_cf, int64_t* hbm_bytes, int64_t* hot_bytes) {
+  if (int e = check_mesh(m)) return e;
+  if (device) *device = m->device;
+  if (layout) *layout = m->layout;
+  if (n_points) *n_points = m->n_points;
+  if (n_tets) *n_tets = m->n_tets;
+  if (n_cf) *n_cf = m->n_cf;
+  if (hbm_bytes) *hbm_bytes = m->hbm_bytes;
+  if (hot_bytes) *hot_bytes = m->hot_bytes;
+  return TB_OK;
+}
+
+int tb_cast_rays(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
+                 uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t,
+                 int32_t* tet_back, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  if (n == 0) return TB_OK;
+  if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
+  DeviceGuard g(m->device);
+  const cudaStream_t s = (cudaStream_t)stream;
+  if (int e = launch_layout<CastL>(m->layout, grid_for(n, kBlock), s, m->view(), n, o, d, start, status, cf,
+                                   tet, visited, triangle, t, tet_back))
+    return e;
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_sctp_cast_rays(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
+                      uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle,
+                      double* t, int32_t* tet_back, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  if (n == 0) return TB_OK;
+  if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
+  DeviceGuard g(m->device);
+  const cudaStream_t s = (cudaStream_t)stream;
+  if (int e = launch_layout<SctpL>(m->layout, grid_for(n, kBlock), s, m->view(), n, o, d, start, status, cf,
+                                   tet, visited, triangle, t, tet_back))
+    return e;
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_cast_rays_visits(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
+                        const int64_t* offsets, int32_t* seq, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  if (n == 0) return TB_OK;
+  if (!o || !d || !start || !offsets || !seq) return set_error(TB_E_ARG, "NULL buffer");
+  DeviceGuard g(m->device);
+  const cudaStream_t s = (cudaStream_t)stream;
+  if (int e = launch_layout<VisitsL>(m->layout, grid_for(n, kBlock), s, m->view(), n, o, d, start, offsets, seq))
+    return e;
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_locate_points(tb_mesh* m, int64_t n, const double* q, const int32_t* hints, int32_t* tet,
+                     int32_t* visited, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative point count");
+  if (n == 0) return TB_OK;
+  if (!q || !hints || !tet || !visited) return set_error(TB_E_ARG, "NULL buffer");
+  DeviceGuard g(m->device);
+  const cudaStream_t s = (cudaStream_t)stream;
+  if (int e = launch_layout<LocateL>(m->layout, grid_for(n, kBlock), s, m->view(), n, q, hints, tet, visited))
+    return e;
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_shadow_rays(tb_mesh* m, int64_t n, const double* p, const double* light, int light_stride,
+                   const int32_t* p_tet, const int32_t* light_tet, int light_tet_stride, double eps,
+                   uint8_t* occluded, int32_t* visited, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  if (n == 0) return TB_OK;
+  if (!p || !light || !p_tet || !light_tet || !occluded || !visited) return set_error(TB_E_ARG, "NULL buffer");
+  if ((light_stride != 0 && light_stride != 3) || (light_tet_stride != 0 && light_tet_stride != 1))
+    return set_error(TB_E_ARG, "bad light strides %d/%d", light_stride, light_tet_stride);
+  DeviceGuard g(m->device);
+  const cudaStream_t s = (cudaStream_t)stream;
+  if (int e = launch_layout<ShadowL>(m->layout, grid_for(n, kBlock), s, m->view(), n, p, light, light_stride,
+                                     p_tet, light_tet, light_tet_stride, eps, occluded, visited))
+    return e;
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+// ----------------------------------------------------------------------------
+// Host-buffer entry points: stage -> launch -> copy back -> synchronise, on a
+// private stream with stream-ordered scratch (reentrant per host thread).
+}  // extern "C"
+namespace {
+struct HostCall {
+  cudaStream_t s = nullptr;
+  char* base = nullptr;
+  size_t off = 0;
+  ~HostCall() {
+    if (base) cudaFreeAsync(base, s);
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+  static size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
+  template <typename T>
+  T* take(size_t count) {
+    T* p = reinterpret_cast<T*>(base + off);
+    off += al(count * sizeof(T));
+    return p;
+  }
+};
+}  // namespace
+
+extern "C" {
+
+int tb_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
+                      uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle,
+                      double* t, int32_t* tet_back) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  if (n == 0) return TB_OK;
+  DeviceGuard g(m->device);
+  HostCall hc;
+  TB_CUDA(cudaStreamCreateWithFlags(&hc.s, cudaStreamNonBlocking));
+  const size_t un = (size_t)n;
+  const size_t total = HostCall::al(un * 12) * 2 + HostCall::al(un * 4) * 6 + HostCall::al(un) + HostCall::al(un * 8);
+  TB_CUDA(cudaMallocAsync((void**)&hc.base, total, hc.s));
+  float* dO = hc.take<float>(un * 3);
+  float* dD = hc.take<float>(un * 3);
+  int32_t* dS = hc.take<int32_t>(un);
+  uint8_t* dSt = hc.take<uint8_t>(un);
+  int32_t* dCf = hc.take<int32_t>(un);
+  int32_t* dTet = hc.take<int32_t>(un);
+  int32_t* dVis = hc.take<int32_t>(un);
+  int32_t* dTri = hc.take<int32_t>(un);
+  double* dT = hc.take<double>(un);
+  int32_t* dBack = hc.take<int32_t>(un);
+  TB_CUDA(cudaMemcpyAsync(dO, o, un * 12, cudaMemcpyHostToDevice, hc.s));
+  TB_CUDA(cudaMemcpyAsync(dD, d, un * 12, cudaMemcpyHostToDevice, hc.s));
+  TB_CUDA(cudaMemcpyAsync(dS, start, un * 4, cudaMemcpyHostToDevice, hc.s));
+  if (int e = tb_cast_rays(m, n, dO, dD, dS, dSt, dCf, dTet, dVis, triangle ? dTri : nullptr, t ? dT : nullptr,
+                           tet_back ? dBack : nullptr, hc.s))
+    return e;
+  TB_CUDA(cudaMemcpyAsync(status, dSt, un, cudaMemcpyDeviceToHost, hc.s));
+  TB_CUDA(cudaMemcpyAsync(cf, dCf, un * 4, cudaMemcpyDeviceToHost, hc.s));
+  TB_CUDA(cudaMemcpyAsync(tet, dTet, un * 4, cudaMemcpyDeviceToHost, hc.s));
+  TB_CUDA(cudaMemcpyAsync(visited, dVis, un * 4, cudaMemcpyDeviceToHost, hc.s));
+  if (triangle) TB_CUDA(cudaMemcpyAsync(triangle, dTri, un * 4, cudaMemcpyDeviceToHost, hc.s));
+  if (t) TB_CUDA(cudaMemcpyAsync(t, dT, un * 8, cudaMemcpyDeviceToHost, hc.s));
+  if (tet_back) TB_CUDA(cudaMemcpyAsync(tet_back, dBack, un * 4, cudaMemcpyDeviceToHost, hc.s));
+  TB_CUDA(cudaStreamSynchronize(hc.s));
+  return TB_OK;
+}
+
+int tb_locate_points_host(tb_mesh* m, int64_t n, const double* q, const int32_t* hints, int32_t* tet,
+                          int32_t* visited) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative point count");
+  if (n == 0) return TB_OK;
+  DeviceGuard g(m->device);
+  HostCall hc;
+  TB_CUDA(cudaStreamCreateWithFlags(&hc.s, cudaStreamNonBlocking));
+  const size_t un = (size_t)n;
+  TB_CUDA(cudaMallocAsync((void**)&hc.base, HostCall::al(un * 24) + HostCall::al(un * 4) * 3, hc.s));
+  double* dQ = hc.take<double>(un * 3);
+  int32_t* dH = hc.take<int32_t>(un);
+  int32_t* dT = hc.take<int32_t>(un);
+  int32_t* dV = hc.take<int32_t>(un);
+  TB_CUDA(cudaMemcpyAsync(dQ, q, un * 24, cudaMemcpyHostToDevice, hc.s));
+  TB_CUDA(cudaMemcpyAsync(dH, hints, un * 4, cudaMemcpyHostToDevice, hc.s));
+  if (int e = tb_locate_points(m, n, dQ, dH, dT, dV, hc.s)) return e;
+  TB_CUDA(cudaMemcpyAsync(tet, dT, un * 4, cudaMemcpyDeviceToHost, hc.s));
+  TB_CUDA(cudaMemcpyAsync(visited, dV, un * 4, cudaMemcpyDeviceToHost, hc.s));
+  TB_CUDA(cudaStreamSynchronize(hc.s));
+  return TB_OK;
+}
+
+int tb_shadow_rays_host(tb_mesh* m, int64_t n, const double* p, const double* light, int light_stride,
+                        const int32_t* p_tet, const int32_t* light_tet, int light_tet_stride, double eps,
+                        uint8_t* occluded, int32_t* visited) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  if (n == 0) return TB_OK;
+  if ((light_stride != 0 && light_stride != 3) || (light_tet_stride != 0 && light_tet_stride != 1))
+    return set_error(TB_E_ARG, "bad light strides %d/%d", light_stride, light_tet_stride);
+  DeviceGuard g(m->device);
+  HostCall hc;
+  TB_CUDA(cudaStreamCreateWithFlags(&hc.s, cudaStreamNonBlocking));
+  const size_t un = (size_t)n;
+  const size_t nl = light_stride ? un : 1, nlt = light_tet_stride ? un : 1;
+  TB_CUDA(cudaMallocAsync((void**)&hc.base,
+                          HostCall::al(un * 24) + HostCall::al(nl * 24) + HostCall::al(un * 4) * 2 +
+                              HostCall::al(nlt * 4) + HostCall::al(un),
+                          hc.s));
+  double* dP = hc.take<double>(un * 3);
+  double* dL = hc.take<double>(nl * 3);
+  int32_t* dPT = hc.take<int32_t>(un);
+  int32_t* dLT = hc.take<int32_t>(nlt);
+  uint8_t* dOcc = hc.take<uint8_t>(un);
+  int32_t* dV = hc.take<int32_t>(un);
+  TB_CUDA(cudaMemcpyAsync(dP, p, un * 24, cudaMemcpyHostToDevice, hc.s));
+  TB_CUDA(cudaMemcpyAsync(dL, light, nl * 24, cudaMemcpyHostToDevice, hc.s));
+  TB_CUDA(cudaMemcpyAsync(dPT, p_tet, un * 4, cudaMemcpyHostToDevice, hc.s));
+  TB_CUDA(cudaMemcpyAsync(dLT, light_tet, nlt * 4, cudaMemcpyHostToDevice, hc.s));
+  if (int e = tb_shadow_rays(m, n, dP, dL, light_stride, dPT, dLT, light_tet_stride, eps, dOcc, dV, hc.s)) return e;
+  TB_CUDA(cudaMemcpyAsync(occluded, dOcc, un, cudaMemcpyDeviceToHost, hc.s));
+  TB_CUDA(cudaMemcpyAsync(visited, dV, un * 4, cudaMemcpyDeviceToHost, hc.s));
+  TB_CUDA(cudaStreamSynchronize(hc.s));
+  return TB_OK;
+}
+
+int tb_host_alloc(size_t bytes, void** out) {
+  if (!out) return set_error(TB_E_ARG, "out is NULL");
+  TB_CUDA(cudaMallocHost(out, bytes ? bytes : 1));
+  return TB_OK;
+}
+
+int tb_host_free(void* ptr) {
+  if (ptr) TB_CUDA(cudaFreeHost(ptr));
+  return TB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,424 @@
+// traverse.cuh -- device-side traversal arithmetic for sm_100a.
+//
+// Every floating-point operation here is written with explicit round-to-
+// nearest intrinsics (__fmul_rn/__fadd_rn/__fsub_rn/__fdiv_rn and the __d*
+// fp64 forms) in the exact expression order of the reference's compiled
+// kernels (/root/reference/pkg/src/tetray/_kernels.pyx, built with
+// -ffp-contract=off, pkg/setup.py:17-20).  The intrinsics are never
+// contracted into FFMA/DFMA, so results are bit-identical to the reference
+// for the same fp32 inputs; the library is additionally compiled with
+// -fmad=false -ftz=false -prec-div=true as a second line of defence.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tb {
+
+constexpr uint32_t kConstrained = 0x80000000u;  // tetmesh.py:29
+constexpr uint32_t kPayload = 0x7FFFFFFFu;      // tetmesh.py:30
+constexpr uint32_t kBoundary = 0x7FFFFFFFu;     // tetmesh.py:31
+
+constexpr uint8_t kMiss = 0, kHit = 1, kError = 2;  // _kernels.pyx:17-19
+
+// ----------------------------------------------------------------------------
+// Device view of an uploaded mesh.  Layout-specific record arrays:
+//   tet16: rec4[t]            = {vx, nx0, nx1, nx2}            (16 B)
+//   tet20: vx[t] (4 B) + rec4[t] = {n0, n1, n2, n3}           (4 + 16 B, SoA)
+//   tet32: rec4[2t], rec4[2t+1] = {v0, v1, v2, vx}, {n0..n3}  (32 B, one sector)
+//   tet80: rec4[5t .. 5t+4]   = {v0..v3}, {n0..n3}, 12 floats (80 B, inline xyz)
+struct MeshView {
+  const float4* __restrict__ pts;     // (p,) x,y,z,0 -- padded for one 16 B load
+  const uint4* __restrict__ rec4;     // layout records (see above)
+  const uint32_t* __restrict__ vx;    // tet20 only
+  const int4* __restrict__ sv;        // side_verts (t,) ascending
+  const uint4* __restrict__ sn;       // side_neighbors (t,) sorted-slot refs
+  const int32_t* __restrict__ cf_tri; // (c,)
+  const int2* __restrict__ cf_tets;   // (c,) front, back
+  const double* __restrict__ tri;     // (n_tri, 9)
+  int64_t n_points;
+  int64_t n_tets;
+};
+
+__device__ __forceinline__ float pick3(float x, float y, float z, int a) {
+  return a == 0 ? x : (a == 1 ? y : z);
+}
+__device__ __forceinline__ uint32_t pick4u(uint4 v, int k) {
+  return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+}
+
+__device__ __forceinline__ float4 ldg_f4(const float4* p) { return __ldg(p); }
+__device__ __forceinline__ uint4 ldg_u4(const uint4* p) { return __ldg(p); }
+
+// ----------------------------------------------------------------------------
+// Scaled basis, _kernels.pyx:42-86 (spec geometry.py:120-221, Eqs. 1-3).
+struct Basis {
+  int mn, mx, ot;
+  float umax, vmax, voth, sgn, pox, poy;
+};
+
+__device__ __forceinline__ void build_basis(float o0, float o1, float o2, float d0, float d1,
+                                            float d2, Basis& b) {
+  const float a0 = fabsf(d0), a1 = fabsf(d1), a2 = fabsf(d2);
+  int mn = 0;
+  if (a1 < a0) {
+    mn = 1;
+    if (a2 < a1) mn = 2;
+  } else if (a2 < a0) {
+    mn = 2;
+  }
+  int r0, r1;
+  if (mn == 0) {
+    r0 = 1; r1 = 2;
+  } else if (mn == 1) {
+    r0 = 0; r1 = 2;
+  } else {
+    r0 = 0; r1 = 1;
+  }
+  const float ar0 = (r0 == 1) ? a1 : a0;
+  const float ar1 = (r1 == 2) ? a2 : a1;
+  const int mx = (ar0 >= ar1) ? r0 : r1;
+  const int ot = 3 - mn - mx;
+  b.mn = mn; b.mx = mx; b.ot = ot;
+  const float umax = -__fdiv_rn(pick3(d0, d1, d2, ot), pick3(d0, d1, d2, mx));
+  b.umax = umax;
+  float u0 = 0.0f, u1 = 0.0f, u2 = 0.0f;
+  if (ot == 0) u0 = 1.0f; else if (ot == 1) u1 = 1.0f; else u2 = 1.0f;
+  if (mx == 0) u0 = umax; else if (mx == 1) u1 = umax; else u2 = umax;
+  const float t0 = __fsub_rn(__fmul_rn(d1, u2), __fmul_rn(d2, u1));
+  const float t1 = __fsub_rn(__fmul_rn(d2, u0), __fmul_rn(d0, u2));
+  const float t2 = __fsub_rn(__fmul_rn(d0, u1), __fmul_rn(d1, u0));
+  const float tmn = pick3(t0, t1, t2, mn);
+  const float sgn = (tmn > 0.0f) ? 1.0f : -1.0f;
+  const float tabs = (tmn > 0.0f) ? tmn : -tmn;
+  b.sgn = sgn;
+  b.vmax = __fdiv_rn(pick3(t0, t1, t2, mx), tabs);
+  b.voth = __fdiv_rn(pick3(t0, t1, t2, ot), tabs);
+  const float omx = pick3(o0, o1, o2, mx), oot = pick3(o0, o1, o2, ot), omn = pick3(o0, o1, o2, mn);
+  b.pox = __fadd_rn(__fmul_rn(umax, omx), oot);
+  b.poy = __fadd_rn(__fadd_rn(__fmul_rn(b.vmax, omx), __fmul_rn(b.voth, oot)), __fmul_rn(sgn, omn));
+}
+
+// project, _kernels.pyx:89-91.
+__device__ __forceinline__ void project(const Basis& b, float qx, float qy, float qz, float& x,
+                                        float& y) {
+  const float qmx = pick3(qx, qy, qz, b.mx);
+  const float qot = pick3(qx, qy, qz, b.ot);
+  const float qmn = pick3(qx, qy, qz, b.mn);
+  x = __fsub_rn(__fadd_rn(__fmul_rn(b.umax, qmx), qot), b.pox);
+  y = __fsub_rn(
+      __fadd_rn(__fadd_rn(__fmul_rn(b.vmax, qmx), __fmul_rn(b.voth, qot)), __fmul_rn(b.sgn, qmn)),
+      b.poy);
+}
+
+// Algorithm 1, _kernels.pyx:94-102: index of the window point replaced by p3.
+__device__ __forceinline__ int exit_face(float px, float py, const float (&p)[6]) {
+  const float a0 = __fmul_rn(px, p[1]), b0 = __fmul_rn(py, p[0]);
+  const float a2 = __fmul_rn(px, p[5]), b2 = __fmul_rn(py, p[4]);
+  const float a1 = __fmul_rn(px, p[3]), b1 = __fmul_rn(py, p[2]);
+  if (a0 < b0) return (a2 >= b2) ? 1 : 0;
+  return (a1 < b1) ? 2 : 0;
+}
+
+// ----------------------------------------------------------------------------
+// Ray initialisation, _kernels.pyx:114-192.  Returns the selected slot.
+__device__ __forceinline__ int init_ray(const MeshView& m, float o0, float o1, float o2, float d0,
+                                        float d1, float d2, int start, Basis& b, uint32_t (&idx)[3],
+                                        float (&p)[6]) {
+  build_basis(o0, o1, o2, d0, d1, d2, b);
+  const int4 qd = __ldg(&m.sv[start]);
+  const int quad[4] = {qd.x, qd.y, qd.z, qd.w};
+  float4 P[4];
+  float q2[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    P[i] = ldg_f4(&m.pts[quad[i]]);
+    project(b, P[i].x, P[i].y, P[i].z, q2[2 * i], q2[2 * i + 1]);
+  }
+  const double e1x = __dsub_rn((double)P[1].x, (double)P[0].x);
+  const double e1y = __dsub_rn((double)P[1].y, (double)P[0].y);
+  const double e1z = __dsub_rn((double)P[1].z, (double)P[0].z);
+  const double e2x = __dsub_rn((double)P[2].x, (double)P[0].x);
+  const double e2y = __dsub_rn((double)P[2].y, (double)P[0].y);
+  const double e2z = __dsub_rn((double)P[2].z, (double)P[0].z);
+  const double e3x = __dsub_rn((double)P[3].x, (double)P[0].x);
+  const double e3y = __dsub_rn((double)P[3].y, (double)P[0].y);
+  const double e3z = __dsub_rn((double)P[3].z, (double)P[0].z);
+  const double rho = __dadd_rn(
+      __dadd_rn(__dmul_rn(e1x, __dsub_rn(__dmul_rn(e2y, e3z), __dmul_rn(e2z, e3y))),
+                __dmul_rn(e1y, __dsub_rn(__dmul_rn(e2z, e3x), __dmul_rn(e2x, e3z)))),
+      __dmul_rn(e1z, __dsub_rn(__dmul_rn(e2x, e3y), __dmul_rn(e2y, e3x))));
+  const bool rho_pos = rho > 0.0;
+
+  int sel = -1, best_j = -1;
+  float best_m = -3.4e38f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    // SLOT_A/B/C, _kernels.pyx:105-111: the face opposite slot j.
+    const int ia = (j == 0) ? 1 : 0;
+    int ib = (j <= 1) ? 2 : 1;
+    int ic = (j == 3) ? 2 : 3;
+    if (((j & 1) == 0) != rho_pos) { const int tmp = ib; ib = ic; ic = tmp; }
+    const float ax = q2[2 * ia], ay = q2[2 * ia + 1];
+    const float bx = q2[2 * ib], by = q2[2 * ib + 1];
+    const float cx = q2[2 * ic], cy = q2[2 * ic + 1];
+    const float dd0 = __fsub_rn(__fmul_rn(ax, by), __fmul_rn(ay, bx));
+    const float dd1 = __fsub_rn(__fmul_rn(bx, cy), __fmul_rn(by, cx));
+    const float dd2 = __fsub_rn(__fmul_rn(cx, ay), __fmul_rn(cy, ax));
+    float mm = dd0;
+    if (dd1 < mm) mm = dd1;
+    if (dd2 < mm) mm = dd2;
+    if (sel < 0) {
+      if (mm >= 0.0f && (dd0 > 0.0f || dd1 > 0.0f || dd2 > 0.0f)) {
+        sel = j;
+      } else if (mm > best_m) {
+        best_m = mm;
+        best_j = j;
+      }
+    }
+  }
+  if (sel < 0) sel = best_j;
+  // All-NaN windows (degenerate rays) leave best_j = -1; the reference reads
+  // SLOT_A[-1] there (undefined behaviour).  Pin it to slot 0, the choice of
+  // the reference's pure twin (np.argmax over NaNs, _kernels_py.py:134).
+  if (sel < 0) sel = 0;
+  const int ia = (sel == 0) ? 1 : 0;
+  int ib = (sel <= 1) ? 2 : 1;
+  int ic = (sel == 3) ? 2 : 3;
+  if (((sel & 1) == 0) != rho_pos) { const int tmp = ib; ib = ic; ic = tmp; }
+  // Dynamic selects over the 4 projected points (registers, no local memory).
+  auto qsel = [&](int k, float& x, float& y, int& id) {
+    x = k == 0 ? q2[0] : (k == 1 ? q2[2] : (k == 2 ? q2[4] : q2[6]));
+    y = k == 0 ? q2[1] : (k == 1 ? q2[3] : (k == 2 ? q2[5] : q2[7]));
+    id = k == 0 ? quad[0] : (k == 1 ? quad[1] : (k == 2 ? quad[2] : quad[3]));
+  };
+  int i0, i1, i2;
+  qsel(ia, p[0], p[1], i0);
+  qsel(ib, p[2], p[3], i1);
+  qsel(ic, p[4], p[5], i2);
+  idx[0] = (uint32_t)i0; idx[1] = (uint32_t)i1; idx[2] = (uint32_t)i2;
+  return sel;
+}
+
+// ----------------------------------------------------------------------------
+// Layout-specific record access.  A step needs: the xor word vx (to recover
+// the fourth vertex i3) and, after the exit decision, the exit reference.
+template <int L>
+struct Record;
+
+template <>
+struct Record<16> {
+  uint4 r;
+  __device__ __forceinline__ void load(const MeshView& m, uint32_t t) { r = ldg_u4(&m.rec4[t]); }
+  __device__ __forceinline__ uint32_t vxw() const { return r.x; }
+  // Alg. 7, _kernels.pyx:222-235.
+  __device__ __forceinline__ uint32_t next_ref(const uint32_t (&idx)[3], uint32_t i3, uint32_t idxf,
+                                               uint32_t prev) const {
+    const int rank = (idx[0] < idxf) + (idx[1] < idxf) + (idx[2] < idxf) + (i3 < idxf);
+    const int order_a = (idx[0] < i3) + (idx[1] < i3) + (idx[2] < i3);
+    uint32_t nref = prev;
+    if (order_a != 3) nref ^= pick4u(r, 1 + order_a);
+    if (rank != 3) nref ^= pick4u(r, 1 + rank);
+    return nref;
+  }
+};
+
+template <>
+struct Record<20> {
+  uint32_t v;
+  uint4 n;
+  __device__ __forceinline__ void load(const MeshView& m, uint32_t t) {
+    v = __ldg(&m.vx[t]);
+    n = ldg_u4(&m.rec4[t]);
+  }
+  __device__ __forceinline__ uint32_t vxw() const { return v; }
+  // Alg. 5, _kernels.pyx:207-221.
+  __device__ __forceinline__ uint32_t next_ref(const uint32_t (&idx)[3], uint32_t i3, uint32_t idxf,
+                                               uint32_t) const {
+    const int rank = (idx[0] < idxf) + (idx[1] < idxf) + (idx[2] < idxf) + (i3 < idxf);
+    return pick4u(n, rank);
+  }
+};
+
+template <>
+struct Record<32> {
+  uint4 a, n;
+  __device__ __forceinline__ void load(const MeshView& m, uint32_t t) {
+    a = ldg_u4(&m.rec4[2 * (size_t)t]);
+    n = ldg_u4(&m.rec4[2 * (size_t)t + 1]);
+  }
+  __device__ __forceinline__ uint32_t vxw() const { return a.w; }
+  // Alg. 3, _kernels.pyx:204-209.
+  __device__ __forceinline__ uint32_t next_ref(const uint32_t (&)[3], uint32_t, uint32_t idxf,
+                                               uint32_t) const {
+    uint32_t nref = n.w;
+    if (a.x == idxf) nref = n.x;
+    if (a.y == idxf) nref = n.y;
+    if (a.z == idxf) nref = n.z;
+    return nref;
+  }
+};
+
+// TetMesh-80: sorted ids, sorted-slot refs and the four vertices inline.
+template <>
+struct Record<80> {
+  uint4 v, n;
+  const uint4* base;
+  __device__ __forceinline__ void load(const MeshView& m, uint32_t t) {
+    base = m.rec4 + 5 * (size_t)t;
+    v = ldg_u4(base);
+    n = ldg_u4(base + 1);
+  }
+  __device__ __forceinline__ uint32_t vxw() const { return v.x ^ v.y ^ v.z ^ v.w; }
+  __device__ __forceinline__ int slot_of(uint32_t id) const {
+    return (v.x == id) ? 0 : ((v.y == id) ? 1 : ((v.z == id) ? 2 : 3));
+  }
+  // Vertex coordinates of slot k from the inline block (floats 8..19).
+  __device__ __forceinline__ float4 vertex(int k) const {
+    const float* f = reinterpret_cast<const float*>(base + 2);
+    return make_float4(__ldg(f + 3 * k), __ldg(f + 3 * k + 1), __ldg(f + 3 * k + 2), 0.0f);
+  }
+  __device__ __forceinline__ uint32_t next_ref(const uint32_t (&)[3], uint32_t, uint32_t idxf,
+                                               uint32_t) const {
+    return pick4u(n, slot_of(idxf));
+  }
+};
+
+template <int L>
+__device__ __forceinline__ float4 fetch_vertex(const MeshView& m, const Record<L>&, uint32_t i3) {
+  return ldg_f4(&m.pts[i3]);
+}
+template <>
+__device__ __forceinline__ float4 fetch_vertex<80>(const MeshView&, const Record<80>& r,
+                                                   uint32_t i3) {
+  return r.vertex(r.slot_of(i3));
+}
+
+// One traversal step into tet `nxt`, _kernels.pyx:238-259.  Updates the
+// window (idx, p) and returns the exit reference of `nxt`.
+template <int L>
+__device__ __forceinline__ uint32_t advance(const MeshView& m, const Basis& b, uint32_t (&idx)[3],
+                                            float (&p)[6], uint32_t nxt, uint32_t prev) {
+  Record<L> rec;
+  rec.load(m, nxt);
+  uint32_t i3 = idx[0] ^ idx[1] ^ idx[2] ^ rec.vxw();
+  if (L != 80 && i3 >= (uint32_t)m.n_points) i3 = 0;  // corrupt record: stay in bounds
+  const float4 q = fetch_vertex<L>(m, rec, i3);
+  float qx, qy;
+  project(b, q.x, q.y, q.z, qx, qy);
+  const int f = exit_face(qx, qy, p);
+  const uint32_t idxf = (f == 0) ? idx[0] : ((f == 1) ? idx[1] : idx[2]);
+  const uint32_t nref = rec.next_ref(idx, i3, idxf, prev);
+  if (f == 0) { idx[0] = i3; p[0] = qx; p[1] = qy; }
+  else if (f == 1) { idx[1] = i3; p[2] = qx; p[3] = qy; }
+  else { idx[2] = i3; p[4] = qx; p[5] = qy; }
+  return nref;
+}
+
+// ----------------------------------------------------------------------------
+// fp64 epilogue: t of the ray/triangle pair, _kernels_py._mt_t
+// (_kernels_py.py:435-454) -- reciprocal-multiply form, numpy's cross and
+// einsum operation order, plane-distance fallback for det == 0.
+__device__ __forceinline__ double mt_t(double ox, double oy, double oz, double dx, double dy,
+                                       double dz, const double* __restrict__ T) {
+  const double ax = __ldg(T + 0), ay = __ldg(T + 1), az = __ldg(T + 2);
+  const double bx = __ldg(T + 3), by = __ldg(T + 4), bz = __ldg(T + 5);
+  const double cx = __ldg(T + 6), cy = __ldg(T + 7), cz = __ldg(T + 8);
+  const double e1x = __dsub_rn(bx, ax), e1y = __dsub_rn(by, ay), e1z = __dsub_rn(bz, az);
+  const double e2x = __dsub_rn(cx, ax), e2y = __dsub_rn(cy, ay), e2z = __dsub_rn(cz, az);
+  // pv = cross(d, e2)
+  const double pvx = __dsub_rn(__dmul_rn(dy, e2z), __dmul_rn(dz, e2y));
+  const double pvy = __dsub_rn(__dmul_rn(dz, e2x), __dmul_rn(dx, e2z));
+  const double pvz = __dsub_rn(__dmul_rn(dx, e2y), __dmul_rn(dy, e2x));
+  const double det = __dadd_rn(__dadd_rn(__dmul_rn(e1x, pvx), __dmul_rn(e1y, pvy)), __dmul_rn(e1z, pvz));
+  const double tvx = __dsub_rn(ox, ax), tvy = __dsub_rn(oy, ay), tvz = __dsub_rn(oz, az);
+  if (det != 0.0) {
+    const double inv = __ddiv_rn(1.0, det);
+    // cross(tv, e1)
+    const double qx = __dsub_rn(__dmul_rn(tvy, e1z), __dmul_rn(tvz, e1y));
+    const double qy = __dsub_rn(__dmul_rn(tvz, e1x), __dmul_rn(tvx, e1z));
+    const double qz = __dsub_rn(__dmul_rn(tvx, e1y), __dmul_rn(tvy, e1x));
+    const double num = __dadd_rn(__dadd_rn(__dmul_rn(e2x, qx), __dmul_rn(e2y, qy)), __dmul_rn(e2z, qz));
+    return __dmul_rn(num, inv);
+  }
+  // parallel: plane distance
+  const double nx = __dsub_rn(__dmul_rn(e1y, e2z), __dmul_rn(e1z, e2y));
+  const double ny = __dsub_rn(__dmul_rn(e1z, e2x), __dmul_rn(e1x, e2z));
+  const double nz = __dsub_rn(__dmul_rn(e1x, e2y), __dmul_rn(e1y, e2x));
+  const double denom = __dadd_rn(__dadd_rn(__dmul_rn(nx, dx), __dmul_rn(ny, dy)), __dmul_rn(nz, dz));
+  if (denom == 0.0) return 0.0;
+  const double num = __dadd_rn(__dadd_rn(__dmul_rn(nx, __dsub_rn(ax, ox)), __dmul_rn(ny, __dsub_rn(ay, oy))),
+                               __dmul_rn(nz, __dsub_rn(az, oz)));
+  return __ddiv_rn(num, denom);
+}
+
+// Segment/triangle parameter of the compiled shadow walk, _kernels.pyx:495-524
+// (division form, not the reciprocal of mt_t).
+__device__ __forceinline__ double seg_tri_t(const double (&o)[3], const double (&d)[3],
+                                            const double* __restrict__ T) {
+  const double ax = __ldg(T + 0), ay = __ldg(T + 1), az = __ldg(T + 2);
+  const double e1x = __dsub_rn(__ldg(T + 3), ax), e1y = __dsub_rn(__ldg(T + 4), ay),
+               e1z = __dsub_rn(__ldg(T + 5), az);
+  const double e2x = __dsub_rn(__ldg(T + 6), ax), e2y = __dsub_rn(__ldg(T + 7), ay),
+               e2z = __dsub_rn(__ldg(T + 8), az);
+  const double pvx = __dsub_rn(__dmul_rn(d[1], e2z), __dmul_rn(d[2], e2y));
+  const double pvy = __dsub_rn(__dmul_rn(d[2], e2x), __dmul_rn(d[0], e2z));
+  const double pvz = __dsub_rn(__dmul_rn(d[0], e2y), __dmul_rn(d[1], e2x));
+  const double det = __dadd_rn(__dadd_rn(__dmul_rn(e1x, pvx), __dmul_rn(e1y, pvy)), __dmul_rn(e1z, pvz));
+  const double tvx = __dsub_rn(o[0], ax), tvy = __dsub_rn(o[1], ay), tvz = __dsub_rn(o[2], az);
+  if (det != 0.0) {
+    const double qx = __dsub_rn(__dmul_rn(tvy, e1z), __dmul_rn(tvz, e1y));
+    const double qy = __dsub_rn(__dmul_rn(tvz, e1x), __dmul_rn(tvx, e1z));
+    const double qz = __dsub_rn(__dmul_rn(tvx, e1y), __dmul_rn(tvy, e1x));
+    return __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(e2x, qx), __dmul_rn(e2y, qy)), __dmul_rn(e2z, qz)), det);
+  }
+  const double nx = __dsub_rn(__dmul_rn(e1y, e2z), __dmul_rn(e1z, e2y));
+  const double ny = __dsub_rn(__dmul_rn(e1z, e2x), __dmul_rn(e1x, e2z));
+  const double nz = __dsub_rn(__dmul_rn(e1x, e2y), __dmul_rn(e1y, e2x));
+  const double denom = __dadd_rn(__dadd_rn(__dmul_rn(nx, d[0]), __dmul_rn(ny, d[1])), __dmul_rn(nz, d[2]));
+  if (denom == 0.0) return 0.0;
+  const double num = __dadd_rn(__dadd_rn(__dmul_rn(nx, __dsub_rn(ax, o[0])), __dmul_rn(ny, __dsub_rn(ay, o[1]))),
+                               __dmul_rn(nz, __dsub_rn(az, o[2])));
+  return __ddiv_rn(num, denom);
+}
+
+// _det3, _kernels.pyx:408-413.
+__device__ __forceinline__ double det3(double ax, double ay, double az, double bx, double by,
+                                       double bz, double cx, double cy, double cz) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(ax, __dsub_rn(__dmul_rn(by, cz), __dmul_rn(bz, cy))),
+                             __dmul_rn(ay, __dsub_rn(__dmul_rn(bz, cx), __dmul_rn(bx, cz)))),
+                   __dmul_rn(az, __dsub_rn(__dmul_rn(bx, cy), __dmul_rn(by, cx))));
+}
+
+// fp64 point-in-tet with relative epsilon, _kernels.pyx:373-405.
+__device__ __forceinline__ bool contains(const MeshView& m, uint32_t t, const double (&q)[3]) {
+  const int4 v = __ldg(&m.sv[t]);
+  const int vid[4] = {v.x, v.y, v.z, v.w};
+  double P[4][3];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float4 f = ldg_f4(&m.pts[vid[i]]);
+    P[i][0] = f.x; P[i][1] = f.y; P[i][2] = f.z;
+  }
+  const double vol = det3(__dsub_rn(P[1][0], P[0][0]), __dsub_rn(P[1][1], P[0][1]), __dsub_rn(P[1][2], P[0][2]),
+                          __dsub_rn(P[2][0], P[0][0]), __dsub_rn(P[2][1], P[0][1]), __dsub_rn(P[2][2], P[0][2]),
+                          __dsub_rn(P[3][0], P[0][0]), __dsub_rn(P[3][1], P[0][1]), __dsub_rn(P[3][2], P[0][2]));
+  const double s = vol > 0.0 ? 1.0 : -1.0;
+  const double eps = __dadd_rn(__dmul_rn(1e-10, fabs(vol)), 1e-300);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double S[4][3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) S[i][k] = (i == j) ? q[k] : P[i][k];
+    }
+    const double dd = det3(__dsub_rn(S[1][0], S[0][0]), __dsub_rn(S[1][1], S[0][1]), __dsub_rn(S[1][2], S[0][2]),
+                           __dsub_rn(S[2][0], S[0][0]), __dsub_rn(S[2][1], S[0][1]), __dsub_rn(S[2][2], S[0][2]),
+                           __dsub_rn(S[3][0], S[0][0]), __dsub_rn(S[3][1], S[0][1]), __dsub_rn(S[3][2], S[0][2]));
+    if (__dmul_rn(s, dd) < -eps) return false;
+  }
+  return true;
+}
+
+}  // namespace tb

@@ -1,0 +1,146 @@
+"""HBM-resident meshes: upload once, cache per (mesh, layout, device).
+
+The reference kernels read the mesh arrays on every call
+(_kernels.pyx:276-282); here a ``CompactMesh`` is uploaded to HBM on first
+use and the handle is cached.  The cache key is the mesh object plus the
+data pointers and shapes of every array the device copy is built from, so
+replacing an array (``relayout``, ``reorder``, ``dataclasses.replace``)
+triggers a fresh upload; in-place mutation of an array does not -- call
+``invalidate(mesh)`` after mutating (the reference tests that do so only
+exercise ``validate``, test_tetmesh.py:123-148).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+import weakref
+
+import numpy as np
+
+from . import _lib
+from ._lib import addr, check, lib
+
+LAYOUT_CODES = {"tet32": 32, "tet20": 20, "tet16": 16, "tet80": 80}
+
+
+def default_device() -> int:
+    env = os.environ.get("TETB200_DEVICE")
+    if env is not None:
+        return int(env)
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:  # torch is plumbing only; the library does not need it
+        pass
+    return 0
+
+
+class DeviceMesh:
+    """A mesh resident in one GPU's HBM (wraps a ``tb_mesh*``).
+
+    ``layout`` defaults to the mesh's own; ``"tet80"`` builds TetMesh-80
+    records (ids + refs + inline coordinates) on the device.
+    """
+
+    def __init__(self, mesh, device: int | None = None, layout: str | None = None):
+        self.device = default_device() if device is None else int(device)
+        self.layout = layout or mesh.layout
+        if self.layout not in LAYOUT_CODES:
+            raise ValueError(f"unknown layout {self.layout!r}")
+        code = LAYOUT_CODES[self.layout]
+        pts = np.ascontiguousarray(mesh.points, dtype=np.float32)
+        sv = np.ascontiguousarray(mesh.side_verts, dtype=np.int32)
+        sn = np.ascontiguousarray(mesh.side_neighbors, dtype=np.uint32)
+        if code == 80:
+            recs = None
+        else:
+            if self.layout != mesh.layout:
+                from .tetmesh import _records_from_tables
+
+                recs = _records_from_tables(self.layout, sv, sn).view("<u4").reshape(len(sv), -1)
+            else:
+                recs = np.ascontiguousarray(mesh.records_u32(), dtype=np.uint32)
+            if recs.shape != (len(sv), code // 4):
+                raise ValueError(f"records shape {recs.shape} does not match layout {self.layout}")
+        cft = np.ascontiguousarray(mesh.cf_triangle, dtype=np.int32)
+        cfk = np.ascontiguousarray(np.asarray(mesh.cf_tets, dtype=np.int32).reshape(-1, 2))
+        tri = np.ascontiguousarray(mesh.triangle_coords(), dtype=np.float64).reshape(-1, 9)
+        if pts.ndim != 2 or pts.shape[1] != 3 or sv.shape != (len(sv), 4) or sn.shape != sv.shape:
+            raise ValueError("mesh arrays have unexpected shapes")
+        h = ctypes.c_void_p()
+        check(
+            lib.tb_mesh_create(
+                self.device, code, len(pts), addr(pts), len(sv), addr(recs), addr(sv), addr(sn),
+                len(cft), addr(cft), addr(cfk), len(tri), addr(tri), ctypes.byref(h),
+            ),
+            "tb_mesh_create",
+        )
+        self.handle = h
+        self.n_tets = len(sv)
+        self.n_points = len(pts)
+        self.n_cf = len(cft)
+        hbm, hot = ctypes.c_int64(), ctypes.c_int64()
+        check(lib.tb_mesh_info(h, None, None, None, None, None, ctypes.byref(hbm), ctypes.byref(hot)), "tb_mesh_info")
+        self.hbm_bytes = hbm.value
+        self.hot_bytes = hot.value
+        self._finalizer = weakref.finalize(self, lib.tb_mesh_destroy, h)
+
+    @property
+    def layout_code(self) -> int:
+        return LAYOUT_CODES[self.layout]
+
+    def close(self) -> None:
+        self._finalizer()
+
+
+def _fingerprint(mesh):
+    arrs = [mesh.points, mesh.records, mesh.side_verts, mesh.side_neighbors, mesh.cf_triangle, mesh.cf_tets,
+            mesh.soup.vertices, mesh.soup.triangles]
+    return tuple((a.__array_interface__["data"][0], a.shape) for a in arrs) + (mesh.layout,)
+
+
+_lock = threading.Lock()
+_cache: dict = {}
+
+
+def device_mesh(mesh, device: int | None = None, layout: str | None = None) -> DeviceMesh:
+    """Cached upload of ``mesh`` (a CompactMesh or a DeviceMesh, returned as is)."""
+    if isinstance(mesh, DeviceMesh):
+        return mesh
+    dev = default_device() if device is None else int(device)
+    key = (id(mesh), layout or mesh.layout, dev)
+    fp = _fingerprint(mesh)
+    with _lock:
+        hit = _cache.get(key)
+        if hit is not None and hit[1] == fp:
+            return hit[0]
+        dm = DeviceMesh(mesh, dev, layout)
+        _cache[key] = (dm, fp)
+        try:
+            weakref.finalize(mesh, _evict, key)
+        except TypeError:
+            pass
+        return dm
+
+
+def _evict(key) -> None:
+    with _lock:
+        hit = _cache.pop(key, None)
+    if hit is not None:
+        hit[0].close()
+
+
+def invalidate(mesh) -> None:
+    """Drop every cached device copy of ``mesh`` (after in-place mutation)."""
+    with _lock:
+        keys = [k for k in _cache if k[0] == id(mesh)]
+        hits = [_cache.pop(k) for k in keys]
+    for dm, _ in hits:
+        dm.close()
+
+
+__all__ = ["DeviceMesh", "device_mesh", "invalidate", "default_device", "LAYOUT_CODES", "_lib"]

@@ -1,0 +1,423 @@
+"""Scene and mesh ingestion: Kuhn box fixtures, TetGen filesets, OBJ soups.
+
+Host-side mirror of the reference's ingestion layer (/root/reference/pkg/
+src/tetray/ingestion.py) producing byte-identical raw meshes, vectorised so
+fixture and scene construction is not the bottleneck on the GPU box.  The
+constrained-face order, front/back convention and triangle association are
+the reference's:
+  * faces are visited in ascending sorted-vertex-triple order
+    (``sorted(inc.items())``, ingestion.py:376);
+  * front = the first incident (tet, slot) in tet-major order, back = the
+    second or NO_TET on the hull (ingestion.py:399-401);
+  * triangle ids come from ``associate_constrained_faces``
+    (ingestion.py:470-529).
+"""
+
+from __future__ import annotations
+
+import itertools
+from pathlib import Path
+
+import numpy as np
+
+from .tetmesh import (
+    BOUNDARY_REF,
+    CONSTRAINED_BIT,
+    NO_TET,
+    MeshError,
+    RawTetMesh,
+    SceneTriangleSoup,
+    face_incidence_arrays,
+    signed_volumes,
+    unpack_keys,
+    validate_raw,
+)
+
+
+class ParseError(Exception):
+    def __init__(self, path, line_no, message):
+        super().__init__(f"{path}:{line_no}: {message}")
+        self.path = str(path)
+        self.line_no = line_no
+
+
+class AssociationError(Exception):
+    """A constrained mesh face could not be matched to a scene triangle."""
+
+
+# ---------------------------------------------------------------------------
+# Kuhn box fixture (ingestion.py:309-467)
+
+_PERMS = list(itertools.permutations((0, 1, 2)))
+_FREE_AXES = {0: (1, 2), 1: (0, 2), 2: (0, 1)}
+
+
+def _perm_parity(p) -> int:
+    inv = sum(1 for i in range(3) for j in range(i + 1, 3) if p[i] > p[j])
+    return -1 if inv % 2 else 1
+
+
+def kuhn_tets(n: int) -> np.ndarray:
+    """(6 n^3, 4) int32 Kuhn tets, cells in (i, j, k) C order, 6 permutations
+    per cell in itertools order, vertices 1/2 swapped for odd permutations."""
+    m = n + 1
+    ii, jj, kk = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    c0 = np.stack([ii.ravel(), jj.ravel(), kk.ravel()], axis=1).astype(np.int64)  # (n^3, 3)
+    eye = np.eye(3, dtype=np.int64)
+    stride = np.array([m * m, m, 1], dtype=np.int64)
+    out = np.empty((len(c0), 6, 4), dtype=np.int64)
+    for k, p in enumerate(_PERMS):
+        c1 = c0 + eye[p[0]]
+        c2 = c1 + eye[p[1]]
+        c3 = c0 + 1
+        q = [c0 @ stride, c1 @ stride, c2 @ stride, c3 @ stride]
+        if _perm_parity(p) < 0:
+            q[1], q[2] = q[2], q[1]
+        out[:, k, :] = np.stack(q, axis=1)
+    return out.reshape(-1, 4).astype(np.int32)
+
+
+def _check_occluders(n, occluders):
+    occs = []
+    for occ in occluders:
+        axis, k, (u0, v0), (u1, v1) = occ
+        ok = (
+            axis in (0, 1, 2)
+            and all(isinstance(x, (int, np.integer)) for x in (k, u0, v0, u1, v1))
+            and 1 <= k <= n - 1
+            and 0 <= u0 < u1 <= n
+            and 0 <= v0 < v1 <= n
+        )
+        if not ok:
+            raise ValueError(f"occluder {occ} is not on the interior cell-face lattice")
+        occs.append((int(axis), int(k), int(u0), int(v0), int(u1), int(v1)))
+    return occs
+
+
+def _box_soup(n: int, occs, walls: str) -> SceneTriangleSoup:
+    """Wall quads (2 big triangles each) then per-cell occluder squares, split
+    along the low->high diagonal; vertices de-duplicated in first-use order."""
+    verts: list = []
+    vid: dict = {}
+    tris: list = []
+    mats: list = []
+
+    def v(c):
+        key = (float(c[0]), float(c[1]), float(c[2]))
+        if key not in vid:
+            vid[key] = len(verts)
+            verts.append(key)
+        return vid[key]
+
+    def quad(axis, plane, u0, v0, u1, v1, mat):
+        a, b = _FREE_AXES[axis]
+
+        def pt(u, w):
+            c = [0.0, 0.0, 0.0]
+            c[axis] = float(plane)
+            c[a] = float(u)
+            c[b] = float(w)
+            return v(c)
+
+        p00, p10, p11, p01 = pt(u0, v0), pt(u1, v0), pt(u1, v1), pt(u0, v1)
+        tris.extend([(p00, p10, p11), (p00, p11, p01)])
+        mats.extend([mat, mat])
+
+    if walls == "constrained":
+        for axis in range(3):
+            for plane in (0, n):
+                quad(axis, plane, 0, 0, n, n, 0)
+    for axis, k, u0, v0, u1, v1 in occs:
+        for u in range(u0, u1):
+            for w in range(v0, v1):
+                quad(axis, k, u, w, u + 1, w + 1, 1)
+    return SceneTriangleSoup(
+        vertices=np.asarray(verts, dtype=np.float64).reshape(-1, 3),
+        triangles=np.asarray(tris, dtype=np.int32).reshape(-1, 3),
+        material_ids=np.asarray(mats, dtype=np.int32),
+    )
+
+
+def build_box_fixture(n: int, occluders=(), walls: str = "constrained"):
+    """n^3-cell box, 6 Kuhn tets per cell; occluder rectangles on interior
+    cell-face planes and (by default) the walls become constrained faces."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    if walls not in ("constrained", "open"):
+        raise ValueError("walls must be 'constrained' or 'open'")
+    occs = _check_occluders(n, occluders)
+    m = n + 1
+    ii, jj, kk = np.meshgrid(np.arange(m), np.arange(m), np.arange(m), indexing="ij")
+    points = np.stack([ii.ravel(), jj.ravel(), kk.ravel()], axis=1).astype(np.float64)
+    tets = kuhn_tets(n)
+    n_points = len(points)
+    keys, first, second = face_incidence_arrays(tets, n_points)
+    triples = unpack_keys(keys, n_points)
+    ipts = points.astype(np.int64)
+
+    interior = second >= 0
+    on_occ = np.zeros(len(keys), dtype=bool)
+    if occs:
+        fp = ipts[triples]  # (f, 3 pts, 3 coords)
+        for axis, k, u0, v0, u1, v1 in occs:
+            a, b = _FREE_AXES[axis]
+            on_occ |= (
+                np.all(fp[:, :, axis] == k, axis=1)
+                & (fp[:, :, a].min(axis=1) >= u0)
+                & (fp[:, :, a].max(axis=1) <= u1)
+                & (fp[:, :, b].min(axis=1) >= v0)
+                & (fp[:, :, b].max(axis=1) <= v1)
+            )
+    constrained = np.where(interior, on_occ, walls == "constrained")
+
+    neighbors = np.full((len(tets), 4), BOUNDARY_REF, dtype=np.uint32)
+    plain = interior & ~constrained
+    t0, j0 = first[plain] // 4, first[plain] % 4
+    t1, j1 = second[plain] // 4, second[plain] % 4
+    neighbors[t0, j0] = t1
+    neighbors[t1, j1] = t0
+
+    soup = _box_soup(n, occs, walls)
+    cidx = np.nonzero(constrained)[0]
+    face_verts = triples[cidx].astype(np.int32)
+    tri_ids = associate_constrained_faces(points, face_verts, soup, tolerance=0.0)
+    cf_front = (first[cidx] // 4).astype(np.int32)
+    cf_back = np.where(second[cidx] >= 0, second[cidx] // 4, NO_TET).astype(np.int32)
+    cfn = np.arange(len(cidx), dtype=np.int64)
+    neighbors[first[cidx] // 4, first[cidx] % 4] = (CONSTRAINED_BIT | cfn).astype(np.uint32)
+    has2 = second[cidx] >= 0
+    neighbors[second[cidx][has2] // 4, second[cidx][has2] % 4] = (CONSTRAINED_BIT | cfn[has2]).astype(np.uint32)
+    raw = RawTetMesh(
+        points=points,
+        tets=tets,
+        neighbors=neighbors,
+        cf_triangle=tri_ids.astype(np.int32),
+        cf_tets=np.stack([cf_front, cf_back], axis=1),
+        cf_verts=face_verts,
+    )
+    return raw, soup
+
+
+# ---------------------------------------------------------------------------
+# Face -> scene triangle association (ingestion.py:470-538), vectorised.
+
+
+def _inside_2d(t2, area, q, tol):
+    """Edge tests of ingestion._inside_2d, broadcast over leading axes."""
+    s = np.where(area > 0, 1.0, -1.0)
+    slack = tol * (np.abs(area) + 1.0)
+    ok = np.ones(np.broadcast_shapes(area.shape, q.shape[:-1]), dtype=bool)
+    for i in range(3):
+        a = t2[..., i, :]
+        b = t2[..., (i + 1) % 3, :]
+        e = ((b[..., 0] - a[..., 0]) * (q[..., 1] - a[..., 1]) - (b[..., 1] - a[..., 1]) * (q[..., 0] - a[..., 0])) * s
+        ok &= ~(e < -slack)
+    return ok
+
+
+def associate_constrained_faces(points, face_verts, soup: SceneTriangleSoup, tolerance: float = 1e-9) -> np.ndarray:
+    """Scene triangle containing each constrained face (coplanar within
+    tolerance, all three vertices inside; ties broken by strict containment
+    of the centroid)."""
+    points = np.asarray(points, dtype=np.float64)
+    face_verts = np.asarray(face_verts, dtype=np.int64).reshape(-1, 3)
+    tri = soup.triangle_coords()
+    if len(tri) == 0:
+        if len(face_verts):
+            raise AssociationError("scene has no triangles")
+        return np.zeros(0, dtype=np.int32)
+    n_t = np.cross(tri[:, 1] - tri[:, 0], tri[:, 2] - tri[:, 0])
+    n_len = np.linalg.norm(n_t, axis=1)
+    if np.any(n_len == 0):
+        raise AssociationError("degenerate scene triangle")
+    n_hat = n_t / n_len[:, None]
+    drop = np.argmax(np.abs(n_t), axis=1)
+    keep = np.array([[1, 2], [0, 2], [0, 1]])[drop]  # (T, 2)
+    tri2 = np.take_along_axis(tri, keep[:, None, :], axis=2)  # (T, 3, 2)
+    e1 = tri2[:, 1] - tri2[:, 0]
+    e2 = tri2[:, 2] - tri2[:, 0]
+    area2 = e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0]
+    T = len(tri)
+    out = np.empty(len(face_verts), dtype=np.int32)
+    chunk = max(1, 2_000_000 // (3 * T))
+    for lo in range(0, len(face_verts), chunk):
+        ids = face_verts[lo : lo + chunk]
+        pts = points[ids]  # (F, 3, 3)
+        cen = pts.mean(axis=1)  # (F, 3)
+        rel = pts[:, None, :, :] - tri[None, :, 0, None, :]  # (F, T, 3, 3)
+        dist = np.abs(np.einsum("tj,ftpj->ftp", n_hat, rel))
+        coplanar = dist.max(axis=2) <= tolerance + 1e-300  # (F, T)
+        # 2-D coordinates of the face vertices in each triangle's kept axes
+        q = np.take_along_axis(pts[:, None, :, :], keep[None, :, None, :], axis=3)  # (F, T, 3, 2)
+        inside = np.ones(coplanar.shape, dtype=bool)
+        for p in range(3):
+            inside &= _inside_2d(tri2[None], area2[None], q[:, :, p, :], tolerance)
+        match = coplanar & inside
+        cnt = match.sum(axis=1)
+        qc = np.take_along_axis(cen[:, None, :], keep[None, :, :], axis=2)  # (F, T, 2)
+        strict = match & _inside_2d(tri2[None], area2[None], qc, -tolerance)
+        scnt = strict.sum(axis=1)
+        use_strict = (cnt > 1) & (scnt == 1)
+        final = np.where(use_strict[:, None], strict, match)
+        fcnt = final.sum(axis=1)
+        if np.any(fcnt != 1):
+            f = int(np.nonzero(fcnt != 1)[0][0])
+            if cnt[f] == 0 and not coplanar[f].any():
+                raise AssociationError(f"face {pts[f].tolist()} is not coplanar with any triangle")
+            raise AssociationError(f"face {pts[f].tolist()} matched {int(fcnt[f])} scene triangles")
+        out[lo : lo + len(ids)] = np.argmax(final, axis=1)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# TetGen / OBJ (ingestion.py:87-288)
+
+
+def _read_rows(path, min_cols, what):
+    rows = []
+    header = None
+    with open(path) as fh:
+        for line_no, line in enumerate(fh, start=1):
+            s = line.split("#", 1)[0].strip()
+            if not s:
+                continue
+            toks = s.split()
+            if header is None:
+                header = (line_no, toks)
+                continue
+            if len(toks) < min_cols:
+                raise ParseError(path, line_no, f"{what}: expected >= {min_cols} fields")
+            rows.append((line_no, toks))
+    if header is None:
+        raise ParseError(path, 0, f"{what}: empty file")
+    return header, rows
+
+
+def parse_tetgen(base) -> RawTetMesh:
+    """TetGen ASCII fileset -> RawTetMesh (ingestion.py:87-177 semantics):
+    auto 0/1 index base, marked .face entries become constrained faces (in
+    file order), .neigh -1 -> boundary, negative tets reoriented by swapping
+    slots 1 and 2."""
+    base = str(base)
+    if base.endswith(".node"):
+        base = base[: -len(".node")]
+    node, ele, neigh, face = (Path(base + e) for e in (".node", ".ele", ".neigh", ".face"))
+    (hl, ht), rows = _read_rows(node, 4, "node")
+    n_points = int(ht[0])
+    if int(ht[1]) != 3:
+        raise ParseError(node, hl, f"dimension {ht[1]} != 3")
+    if len(rows) != n_points:
+        raise ParseError(node, hl, f"{len(rows)} nodes, header says {n_points}")
+    ib = int(rows[0][1][0]) if rows else 0
+    if ib not in (0, 1):
+        raise ParseError(node, rows[0][0], f"first node index {ib}, expected 0 or 1")
+    idx = np.array([int(t[0]) for _, t in rows], dtype=np.int64) - ib
+    if not np.array_equal(idx, np.arange(n_points)):
+        k = int(np.nonzero(idx != np.arange(n_points))[0][0])
+        raise ParseError(node, rows[k][0], f"non-sequential node index {rows[k][1][0]}")
+    points = np.array([[float(t[1]), float(t[2]), float(t[3])] for _, t in rows], dtype=np.float64).reshape(-1, 3)
+    (hl, ht), rows = _read_rows(ele, 5, "ele")
+    n_tets = int(ht[0])
+    if len(rows) != n_tets:
+        raise ParseError(ele, hl, f"{len(rows)} tets, header says {n_tets}")
+    tets = (np.array([[int(x) for x in t[1:5]] for _, t in rows], dtype=np.int64).reshape(-1, 4) - ib).astype(np.int32)
+    if len(tets) and (tets.min() < 0 or tets.max() >= n_points):
+        k = int(np.nonzero((tets < 0).any(1) | (tets >= n_points).any(1))[0][0])
+        raise ParseError(ele, rows[k][0], "vertex index out of range")
+    (hl, ht), rows = _read_rows(neigh, 5, "neigh")
+    if int(ht[0]) != n_tets or len(rows) != n_tets:
+        raise ParseError(neigh, hl, "neighbor count does not match .ele")
+    nb = np.array([[int(x) for x in t[1:5]] for _, t in rows], dtype=np.int64).reshape(-1, 4)
+    nb[nb >= 0] -= ib
+    if nb.max(initial=-1) >= n_tets:
+        raise ParseError(neigh, 0, "neighbor index out of range")
+    faces = []
+    if face.exists():
+        (hl, ht), rows = _read_rows(face, 4, "face")
+        if len(rows) != int(ht[0]):
+            raise ParseError(face, hl, f"{len(rows)} faces, header says {ht[0]}")
+        for line_no, t in rows:
+            corners = tuple(int(x) - ib for x in t[1:4])
+            marker = int(t[4]) if len(t) > 4 else 1
+            if min(corners) < 0 or max(corners) >= n_points:
+                raise ParseError(face, line_no, "face corner out of range")
+            if marker != 0:
+                faces.append(corners)
+    flip = np.nonzero(signed_volumes(points, tets) < 0)[0]
+    tets[flip[:, None], [1, 2]] = tets[flip[:, None], [2, 1]]
+    nb[flip[:, None], [1, 2]] = nb[flip[:, None], [2, 1]]
+    refs = np.where(nb < 0, np.int64(BOUNDARY_REF), nb).astype(np.uint32)
+    raw = RawTetMesh(points=points, tets=tets, neighbors=refs)
+    if faces:
+        mark_constrained(raw, np.asarray(faces, dtype=np.int64), face)
+    problems = validate_raw(raw)
+    if problems:
+        raise ParseError(neigh, 0, "; ".join(problems[:5]))
+    return raw
+
+
+def mark_constrained(raw: RawTetMesh, face_triples, face_path="<faces>") -> None:
+    """Tag the given faces (in order) as constrained faces 0..k-1
+    (ingestion._mark_constrained, ingestion.py:191-207)."""
+    keys_sorted = np.sort(np.asarray(face_triples, dtype=np.int64), axis=1)
+    ukeys, first, second = face_incidence_arrays(raw.tets, raw.n_points)
+    from .tetmesh import pack_keys
+
+    want = pack_keys(keys_sorted, raw.n_points)
+    pos = np.searchsorted(ukeys, want)
+    pos_c = np.minimum(pos, len(ukeys) - 1)
+    found = ukeys[pos_c] == want
+    if not found.all():
+        k = int(np.nonzero(~found)[0][0])
+        raise ParseError(face_path, 0, f"marked face {tuple(face_triples[k])} is not a mesh face")
+    f1, f2 = first[pos_c], second[pos_c]
+    c = np.arange(len(want), dtype=np.int64)
+    raw.neighbors[f1 // 4, f1 % 4] = (CONSTRAINED_BIT | c).astype(np.uint32)
+    h2 = f2 >= 0
+    raw.neighbors[f2[h2] // 4, f2[h2] % 4] = (CONSTRAINED_BIT | c[h2]).astype(np.uint32)
+    raw.cf_triangle = c.astype(np.int32)
+    raw.cf_tets = np.stack([f1 // 4, np.where(h2, f2 // 4, NO_TET)], axis=1).astype(np.int32)
+    raw.cf_verts = keys_sorted.astype(np.int32)
+
+
+def load_obj(path) -> SceneTriangleSoup:
+    """OBJ subset (v/f, fan triangulation, 1-based or negative indices)."""
+    verts, tris = [], []
+    with open(path) as fh:
+        for line_no, line in enumerate(fh, start=1):
+            t = line.split()
+            if not t or t[0].startswith("#"):
+                continue
+            if t[0] == "v":
+                if len(t) < 4:
+                    raise ParseError(path, line_no, "vertex needs 3 coordinates")
+                verts.append([float(t[1]), float(t[2]), float(t[3])])
+            elif t[0] == "f":
+                if len(t) < 4:
+                    raise ParseError(path, line_no, "face needs >= 3 vertices")
+                ids = [int(x.split("/")[0]) for x in t[1:]]
+                ids = [i - 1 if i > 0 else len(verts) + i for i in ids]
+                if min(ids) < 0 or max(ids) >= len(verts):
+                    raise ParseError(path, line_no, "face index out of range")
+                for k in range(1, len(ids) - 1):
+                    tris.append((ids[0], ids[k], ids[k + 1]))
+    vertices = np.asarray(verts, dtype=np.float64).reshape(-1, 3)
+    triangles = np.asarray(tris, dtype=np.int32).reshape(-1, 3)
+    if len(triangles):
+        c = vertices[triangles]
+        if np.any(np.linalg.norm(np.cross(c[:, 1] - c[:, 0], c[:, 2] - c[:, 0]), axis=1) == 0):
+            raise ParseError(path, 0, "degenerate (zero-area) triangle in file")
+    return SceneTriangleSoup(vertices=vertices, triangles=triangles, material_ids=np.zeros(len(triangles), dtype=np.int32))
+
+
+__all__ = [
+    "AssociationError",
+    "MeshError",
+    "ParseError",
+    "associate_constrained_faces",
+    "build_box_fixture",
+    "kuhn_tets",
+    "load_obj",
+    "mark_constrained",
+    "parse_tetgen",
+]

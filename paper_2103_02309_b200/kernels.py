@@ -1,0 +1,202 @@
+"""CUDA kernel module: the reference's backend protocol on sm_100a.
+
+Drop-in for ``tetray._kernels`` (/root/reference/pkg/src/tetray/
+_kernels.pyx:15-19,271,416,527): same module-level names, argument meaning,
+output dtypes and per-ray status semantics, so it can be handed to the
+reference's own batch layer as ``batch.cast_rays(mesh, o, d, st,
+kernels=paper_2103_02309_b200.kernels)``.  Every call runs on the GPU
+through the C ABI (include/tetb200.h); the mesh is uploaded to HBM once and
+cached (device.py).  ``cast_rays_full`` additionally returns the fused
+epilogue (triangle, fp64 t, back tet) that the reference computes on the
+host (batch.py:57-71).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from ._lib import addr, check, lib
+from .device import device_mesh
+
+BACKEND_NAME = "cuda"
+
+STATUS_MISS = 0
+STATUS_HIT = 1
+STATUS_ERROR = 2
+
+
+def _f32x3(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float32).reshape(-1, 3))
+
+
+def _f64x3(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1, 3))
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32).reshape(-1))
+
+
+def _check_tets(tets: np.ndarray, n_tets: int, what: str) -> None:
+    if tets.size and (tets.min() < 0 or tets.max() >= n_tets):
+        bad = int(np.nonzero((tets < 0) | (tets >= n_tets))[0][0])
+        raise IndexError(f"{what}[{bad}] = {int(tets[bad])} is not a tet index (n_tets={n_tets})")
+
+
+def _prep_cast(mesh, o32, d32, start):
+    o = _f32x3(o32)
+    d = _f32x3(d32)
+    st = _i32(start)
+    if not (len(o) == len(d) == len(st)):
+        raise ValueError(f"length mismatch: {len(o)} origins, {len(d)} dirs, {len(st)} starts")
+    _check_tets(st, mesh.n_tets, "start")
+    return o, d, st
+
+
+def cast_rays_full(mesh, o32, d32, start, *, layout: str | None = None, sctp: bool = False):
+    """Traversal + fused epilogue: (status, cf, tet, visited, triangle, t, tet_back)."""
+    o, d, st = _prep_cast(mesh, o32, d32, start)
+    n = len(st)
+    status = np.zeros(n, dtype=np.uint8)
+    cf = np.full(n, -1, dtype=np.int32)
+    tet = np.full(n, -1, dtype=np.int32)
+    visited = np.ones(n, dtype=np.int32)
+    triangle = np.full(n, -1, dtype=np.int32)
+    t = np.full(n, np.inf, dtype=np.float64)
+    back = np.full(n, -1, dtype=np.int32)
+    if n:
+        dm = device_mesh(mesh, layout=layout)
+        if sctp:
+            _sctp_host(dm, n, o, d, st, status, cf, tet, visited, triangle, t, back)
+        else:
+            check(
+                lib.tb_cast_rays_host(dm.handle, n, addr(o), addr(d), addr(st), addr(status), addr(cf), addr(tet),
+                                      addr(visited), addr(triangle), addr(t), addr(back)),
+                "tb_cast_rays_host",
+            )
+    return status, cf, tet, visited, triangle, t, back
+
+
+def _sctp_host(dm, n, o, d, st, status, cf, tet, visited, triangle, t, back):
+    import torch
+
+    dev = torch.device("cuda", dm.device)
+    to = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
+    go, gd, gs = to(o), to(d), to(st)
+    outs = [torch.empty(n, dtype=x, device=dev) for x in (torch.uint8, torch.int32, torch.int32, torch.int32,
+                                                          torch.int32, torch.float64, torch.int32)]
+    stream = torch.cuda.current_stream(dev)
+    check(lib.tb_sctp_cast_rays(dm.handle, n, addr(go), addr(gd), addr(gs), *[addr(x) for x in outs],
+                                stream.cuda_stream), "tb_sctp_cast_rays")
+    for host, dev_t in zip((status, cf, tet, visited, triangle, t, back), outs):
+        host[...] = dev_t.cpu().numpy()
+
+
+def cast_rays(mesh, o32, d32, start, visits_sink=None):
+    """Batch traversal -> (status u8, cf i32, tet i32, visited i32) (_kernels.pyx:271-370).
+
+    With ``visits_sink`` (a list) the visited-tet sequences are appended as
+    per-step (ray indices, tets) wavefronts, the format the reference's
+    ``batch.cast_rays_visits`` consumes (batch.py:101-114).
+    """
+    if visits_sink is None:
+        status, cf, tet, visited, *_ = _cast_plain(mesh, o32, d32, start)
+        return status, cf, tet, visited
+    status, cf, tet, visited, seq, offsets = cast_rays_csr(mesh, o32, d32, start)
+    n = len(status)
+    if n:
+        for k in range(int(visited.max())):
+            rays = np.nonzero(visited > k)[0]
+            visits_sink.append((rays.astype(np.int64), seq[offsets[rays] + k].copy()))
+    return status, cf, tet, visited
+
+
+def _cast_plain(mesh, o32, d32, start):
+    o, d, st = _prep_cast(mesh, o32, d32, start)
+    n = len(st)
+    status = np.zeros(n, dtype=np.uint8)
+    cf = np.full(n, -1, dtype=np.int32)
+    tet = np.full(n, -1, dtype=np.int32)
+    visited = np.ones(n, dtype=np.int32)
+    if n:
+        dm = device_mesh(mesh)
+        check(
+            lib.tb_cast_rays_host(dm.handle, n, addr(o), addr(d), addr(st), addr(status), addr(cf), addr(tet),
+                                  addr(visited), None, None, None),
+            "tb_cast_rays_host",
+        )
+    return status, cf, tet, visited
+
+
+def cast_rays_csr(mesh, o32, d32, start, *, layout: str | None = None):
+    """Traversal plus visit sequences as CSR: (status, cf, tet, visited, seq, offsets)."""
+    import torch
+
+    o, d, st = _prep_cast(mesh, o32, d32, start)
+    n = len(st)
+    if n == 0:
+        z = np.zeros(0, dtype=np.int32)
+        return np.zeros(0, np.uint8), z, z.copy(), z.copy(), z.copy(), np.zeros(1, np.int64)
+    dm = device_mesh(mesh, layout=layout)
+    dev = torch.device("cuda", dm.device)
+    go, gd, gs = (torch.from_numpy(a).to(dev) for a in (o, d, st))
+    status = torch.empty(n, dtype=torch.uint8, device=dev)
+    cf, tet, visited = (torch.empty(n, dtype=torch.int32, device=dev) for _ in range(3))
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    check(lib.tb_cast_rays(dm.handle, n, addr(go), addr(gd), addr(gs), addr(status), addr(cf), addr(tet),
+                           addr(visited), None, None, None, stream), "tb_cast_rays")
+    offsets = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(visited, 0, out=offsets[1:])
+    total = int(offsets[-1].item())
+    seq = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    check(lib.tb_cast_rays_visits(dm.handle, n, addr(go), addr(gd), addr(gs), addr(offsets), addr(seq), stream),
+          "tb_cast_rays_visits")
+    return (status.cpu().numpy(), cf.cpu().numpy(), tet.cpu().numpy(), visited.cpu().numpy(),
+            seq[:total].cpu().numpy(), offsets.cpu().numpy())
+
+
+def locate_points(mesh, q, hints):
+    """Batch point location -> (tet i32 (-1 outside), visited i32) (_kernels.pyx:416-492)."""
+    qq = _f64x3(q)
+    h = _i32(hints)
+    n = len(qq)
+    if len(h) != n:
+        raise ValueError("hints length mismatch")
+    out = np.full(n, -1, dtype=np.int32)
+    visited = np.ones(n, dtype=np.int32)
+    if n == 0:
+        return out, visited
+    _check_tets(h, mesh.n_tets, "hints")
+    dm = device_mesh(mesh)
+    check(lib.tb_locate_points_host(dm.handle, n, addr(qq), addr(h), addr(out), addr(visited)), "tb_locate_points_host")
+    return out, visited
+
+
+def shadow_rays(mesh, p, light, p_tet, light_tet, eps=1e-4):
+    """Batch occlusion -> (occluded bool, visited i32) (_kernels.pyx:527-614).
+
+    ``light`` is one (3,) point or (n, 3); ``light_tet`` an int or (n,).
+    """
+    pp = _f64x3(p)
+    n = len(pp)
+    ll = _f64x3(light)
+    lt = np.ascontiguousarray(np.asarray(light_tet, dtype=np.int32).reshape(-1))
+    pt = _i32(p_tet)
+    if len(pt) != n:
+        raise ValueError("p_tet length mismatch")
+    if len(ll) not in (1, n) or len(lt) not in (1, n):
+        raise ValueError("light / light_tet must be one value or one per ray")
+    occ = np.zeros(n, dtype=bool)
+    visited = np.ones(n, dtype=np.int32)
+    if n == 0:
+        return occ, visited
+    _check_tets(pt, mesh.n_tets, "p_tet")
+    lstride = 3 if (len(ll) == n and n > 1) else 0
+    ltstride = 1 if (len(lt) == n and n > 1) else 0
+    dm = device_mesh(mesh)
+    check(
+        lib.tb_shadow_rays_host(dm.handle, n, addr(pp), addr(ll), lstride, addr(pt), addr(lt), ltstride, float(eps),
+                                addr(occ.view(np.uint8)), addr(visited)),
+        "tb_shadow_rays_host",
+    )
+    return occ, visited

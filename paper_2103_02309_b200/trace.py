@@ -1,0 +1,89 @@
+"""Device-resident tracing API: ``trace(mesh, origins, dirs, start)``.
+
+PyTorch tensors are the ray and hit buffers (plumbing only): inputs are
+CUDA tensors already in HBM, outputs are allocated on the same device, and
+the launch is enqueued on the current torch stream with no host sync.  This
+is the call the benchmark's device-side number measures; ``trace_host`` is
+the end-to-end form (pinned host buffers, H2D + kernel + D2H).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from ._lib import addr, check, lib
+from .device import DeviceMesh, device_mesh
+
+
+@dataclass
+class TraceResult:
+    status: torch.Tensor  # (n,) uint8   0 miss / 1 hit / 2 cycle guard
+    cf: torch.Tensor  # (n,) int32   constrained face, -1 unless hit
+    triangle: torch.Tensor  # (n,) int32   scene triangle, -1 on miss
+    t: torch.Tensor  # (n,) float64 hit parameter, +inf on miss
+    tet: torch.Tensor  # (n,) int32   terminating (front) tet
+    tet_back: torch.Tensor  # (n,) int32   tet behind the hit face, -1 on hull
+    visited: torch.Tensor  # (n,) int32   tets visited (start counts 1)
+
+    def __len__(self) -> int:
+        return self.status.numel()
+
+
+def empty_result(n: int, device) -> TraceResult:
+    dev = torch.device(device)
+    return TraceResult(
+        status=torch.empty(n, dtype=torch.uint8, device=dev),
+        cf=torch.empty(n, dtype=torch.int32, device=dev),
+        triangle=torch.empty(n, dtype=torch.int32, device=dev),
+        t=torch.empty(n, dtype=torch.float64, device=dev),
+        tet=torch.empty(n, dtype=torch.int32, device=dev),
+        tet_back=torch.empty(n, dtype=torch.int32, device=dev),
+        visited=torch.empty(n, dtype=torch.int32, device=dev),
+    )
+
+
+def _check_inputs(dm: DeviceMesh, origins, dirs, start):
+    n = start.numel()
+    for name, x, dt, shape in (("origins", origins, torch.float32, (n, 3)), ("dirs", dirs, torch.float32, (n, 3)),
+                               ("start", start, torch.int32, (n,))):
+        if x.dtype != dt or tuple(x.shape) != shape or not x.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous {dt} tensor of shape {shape}")
+        if x.device.type != "cuda" or x.device.index != dm.device:
+            raise ValueError(f"{name} must live on cuda:{dm.device}")
+    return n
+
+
+def trace(mesh, origins: torch.Tensor, dirs: torch.Tensor, start: torch.Tensor, *, out: TraceResult | None = None,
+          stream: torch.cuda.Stream | None = None, epilogue: bool = True, sctp: bool = False,
+          layout: str | None = None) -> TraceResult:
+    """Trace rays on the GPU; returns hit triangle id, t and terminating tet.
+
+    ``sctp=True`` runs the fp64 scalar-triple-product fallback walk instead
+    of the 2-D modified-basis walk.  Start tets are not range-checked here
+    (device inputs stay on the device); ``kernels.cast_rays`` checks them.
+    """
+    dm = device_mesh(mesh, device=origins.device.index, layout=layout)
+    n = _check_inputs(dm, origins, dirs, start)
+    res = out if out is not None else empty_result(n, origins.device)
+    s = (stream or torch.cuda.current_stream(origins.device)).cuda_stream
+    fn = lib.tb_sctp_cast_rays if sctp else lib.tb_cast_rays
+    check(
+        fn(dm.handle, n, addr(origins), addr(dirs), addr(start), addr(res.status), addr(res.cf), addr(res.tet),
+           addr(res.visited), addr(res.triangle) if epilogue else None, addr(res.t) if epilogue else None,
+           addr(res.tet_back) if epilogue else None, s),
+        "tb_sctp_cast_rays" if sctp else "tb_cast_rays",
+    )
+    return res
+
+
+def locate(mesh, q: torch.Tensor, hints: torch.Tensor, *, stream=None):
+    """Device point location: (tet, visited) int32 tensors."""
+    dm = device_mesh(mesh, device=q.device.index)
+    n = hints.numel()
+    tet = torch.empty(n, dtype=torch.int32, device=q.device)
+    vis = torch.empty(n, dtype=torch.int32, device=q.device)
+    s = (stream or torch.cuda.current_stream(q.device)).cuda_stream
+    check(lib.tb_locate_points(dm.handle, n, addr(q), addr(hints), addr(tet), addr(vis), s), "tb_locate_points")
+    return tet, vis

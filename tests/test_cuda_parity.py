@@ -1,0 +1,228 @@
+"""GPU parity: the sm_100a kernels vs the reference's outputs (golden) and
+the CPU oracle, bit for bit.  Modelled on the reference's backend-parity
+suite (tests/test_kernels.py:26-103) and acceptance criteria 2/3/9
+(tests/test_acceptance.py:67-119,325-342).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import FIXTURES, RAY_SEEDS, digest, golden_mesh
+
+pytestmark = pytest.mark.gpu
+
+LAYOUTS4 = ("tet32", "tet20", "tet16", "tet80")
+NAMES7 = ("status", "cf", "tet", "visited", "triangle", "t", "tet_back")
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2103_02309_b200 import kernels
+
+    return kernels
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import pyoracle
+
+    return pyoracle
+
+
+def _rays(mesh, name, n=10000):
+    from paper_2103_02309_b200.scenes import interior_rays
+
+    return interior_rays(mesh, n, RAY_SEEDS[name])
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+@pytest.mark.parametrize("layout", LAYOUTS4)
+def test_cast_matches_reference_golden(golden, digests, K, name, layout):
+    """All 7 per-ray outputs (incl. fused epilogue) equal the reference's."""
+    base = golden_mesh(golden, name, "tet20" if layout == "tet80" else layout)
+    o, d, st = _rays(base, name)
+    assert digest(o, d, st) == digests[f"{name}/rays"]
+    out = K.cast_rays_full(base, o, d, st, layout=layout)
+    ref_layout = "tet32" if layout == "tet80" else layout
+    assert digest(*out[:4]) == digests[f"{name}/{ref_layout}/cast10k"]
+    assert digest(*out[4:]) == digests[f"{name}/{ref_layout}/cast10k_epilogue"]
+    for k, a in zip(NAMES7, out):
+        assert np.array_equal(a[:2000], golden[f"{name}/cast/{k}"]), k
+
+
+@pytest.mark.parametrize("name", ("pane4", "model"))
+def test_cast_protocol_and_oracle(golden, K, O, name):
+    """The 4-tuple protocol call equals the C oracle on 50k rays."""
+    from paper_2103_02309_b200.scenes import interior_rays
+
+    m = golden_mesh(golden, name)
+    o, d, st = interior_rays(m, 50000, 7)
+    got = K.cast_rays(m, o, d, st)
+    exp = O.cast_rays(m, o, d, st)
+    for a, b in zip(got, exp):
+        assert a.dtype == b.dtype and np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS4)
+def test_visit_sequences(golden, K, layout):
+    """Visit sequences equal the reference's for every layout (acceptance 3)."""
+    from paper_2103_02309_b200.scenes import interior_rays
+
+    m = golden_mesh(golden, "region4")
+    o, d, st = interior_rays(m, 500, 41)
+    *_, seq, off = K.cast_rays_csr(m, o, d, st, layout=layout)
+    assert np.array_equal(off, golden["region4/visits/offsets"])
+    assert np.array_equal(seq, golden["region4/visits/seq"])
+
+
+def test_visits_sink_protocol(golden, K):
+    """visits_sink wavefronts reassemble like the reference batch layer does."""
+    from paper_2103_02309_b200.scenes import interior_rays
+
+    m = golden_mesh(golden, "region4")
+    o, d, st = interior_rays(m, 500, 41)
+    sink: list = []
+    _, _, _, visited = K.cast_rays(m, o, d, st, visits_sink=sink)
+    offsets = np.zeros(len(o) + 1, dtype=np.int64)
+    np.cumsum(visited, out=offsets[1:])
+    visits = np.empty(int(offsets[-1]), dtype=np.int32)
+    pos = offsets[:-1].copy()
+    for rays, tets in sink:  # batch.py:103-114 scatter path
+        visits[pos[rays]] = tets
+        pos[rays] += 1
+    assert np.array_equal(visits, golden["region4/visits/seq"])
+
+
+def test_locate(golden, K):
+    m = golden_mesh(golden, "region4")
+    tet, vis = K.locate_points(m, golden["region4/locate/q"], np.full(3000, m.source_tet, np.int32))
+    assert np.array_equal(tet, golden["region4/locate/tet"])
+    assert np.array_equal(vis, golden["region4/locate/visited"])
+    assert (tet == -1).any() and (tet >= 0).any()
+
+
+@pytest.mark.parametrize("layout", ("tet32", "tet20", "tet16"))
+def test_shadow(golden, K, layout):
+    from paper_2103_02309_b200.tetmesh import relayout
+
+    m = relayout(golden_mesh(golden, "pane4"), layout)
+    occ, vis = K.shadow_rays(m, golden["pane4/shadow/p"], golden["pane4/shadow/light"], golden["pane4/shadow/p_tet"],
+                             int(golden["pane4/shadow/light_tet"][0]))
+    assert occ.dtype == bool
+    assert np.array_equal(occ, golden["pane4/shadow/occ"])
+    assert np.array_equal(vis, golden["pane4/shadow/visited"])
+    assert 0.0 < occ.mean() < 1.0
+
+
+@pytest.mark.parametrize("name", ("pane4", "region4", "model"))
+@pytest.mark.parametrize("layout", LAYOUTS4)
+def test_sctp_kernel_matches_oracle(golden, K, O, name, layout):
+    """The fp64 ScTP fallback walk: bit-exact vs the C restatement, and equal
+    to the 2-D walk except counted tie rays (walk unpinned)."""
+    base = golden_mesh(golden, name, "tet20" if layout == "tet80" else layout)
+    o, d, st = _rays(base, name)
+    got = K.cast_rays_full(base, o, d, st, layout=layout, sctp=True)
+    exp = O.cast_rays_full(base, o, d, st, layout=layout, sctp=True)
+    for k, a, b in zip(NAMES7, got, exp):
+        assert np.array_equal(a, b), k
+    two_d = K.cast_rays_full(base, o, d, st, layout=layout)
+    mism = int(np.sum((got[4] != two_d[4]) | (got[2] != two_d[2])))
+    assert mism <= len(o) // 1000  # grazing/tie rays only
+
+
+def test_cycle_guard_lattice_camera(digests, K, O):
+    """The reference's own cycle-guard rays: status 2 and
+    visited = n_tets + 1 on exactly the same 4 rays, all else identical."""
+    from paper_2103_02309_b200.ingestion import build_box_fixture
+    from paper_2103_02309_b200.scenes import camera_rays
+    from paper_2103_02309_b200.tetmesh import encode
+
+    raw, soup = build_box_fixture(8, occluders=[(0, 4, (2, 2), (6, 6))])
+    m = encode(raw, "tet20", soup)
+    o, d = camera_rays((4.0, 4.0, 0.5), (4.0, 4.0, 8.0), (0.0, 1.0, 0.0), 68.0, 1024, 1024)
+    assert digest(o, d) == digests["lattice8/rays"]
+    cam, _ = K.locate_points(m, np.array([[4.0, 4.0, 0.5]]), np.array([m.source_tet], np.int32))
+    assert int(cam[0]) == digests["lattice8/cam_tet"]
+    st = np.full(len(o), cam[0], np.int32)
+    out = K.cast_rays(m, o, d, st)
+    assert digest(*out) == digests["lattice8/cast"]
+    err = np.nonzero(out[0] == 2)[0]
+    assert err.tolist() == digests["lattice8/errors"]["rays"]
+    assert out[3][err].tolist() == [m.n_tets + 1] * len(err)
+
+
+@pytest.mark.parametrize("scheme", ("none", "hilbert"))
+def test_config1_blob12_camera(digests, K, scheme):
+    """BASELINE config 1 (blob GRID=12, 256x256 primaries) equals the
+    reference end to end: scene build, camera tet, hits, fp64 t."""
+    from paper_2103_02309_b200.scenes import BLOB_CAMERA, blob_scene, camera_rays
+    from conftest import mesh_digest
+
+    sc = blob_scene(12, layout="tet20", scheme=scheme)
+    assert mesh_digest(sc.mesh) == digests[f"blob12/{scheme}/mesh"]
+    o, d = camera_rays(BLOB_CAMERA["position"], BLOB_CAMERA["look_at"], BLOB_CAMERA["up"], BLOB_CAMERA["fov"], 256, 256)
+    assert digest(o, d) == digests["blob12/rays"]
+    cam, _ = K.locate_points(sc.mesh, np.array([BLOB_CAMERA["position"]]), np.array([sc.mesh.source_tet], np.int32))
+    assert int(cam[0]) == digests[f"blob12/{scheme}/cam_tet"]
+    out = K.cast_rays_full(sc.mesh, o, d, np.full(len(o), cam[0], np.int32))
+    assert digest(*out[:4]) == digests[f"blob12/{scheme}/cast"]
+    assert digest(*out[4:]) == digests[f"blob12/{scheme}/epilogue"]
+
+
+def test_batch_layer_mirror(golden, K):
+    """The mirrored batch API (batch.py:39-80 semantics) over the CUDA module."""
+    from paper_2103_02309_b200 import batch
+    from paper_2103_02309_b200.scenes import interior_rays
+
+    m = golden_mesh(golden, "pane4")
+    o, d, st = interior_rays(m, 4000, 40)
+    h = batch.cast_rays(m, o, d, st)
+    assert (h.visited >= 1).all() and len(h) == 4000
+    hit = h.triangle >= 0
+    assert np.all(np.isfinite(h.t[hit])) and np.all(np.isinf(h.t[~hit]))
+    tets, vis = batch.locate_points(m, o[:100].astype(np.float64))
+    assert (tets >= 0).all()
+
+
+def test_empty_and_errors(golden, K):
+    m = golden_mesh(golden, "box4")
+    z3 = np.zeros((0, 3), np.float32)
+    out = K.cast_rays(m, z3, z3, np.zeros(0, np.int32))
+    assert all(len(a) == 0 for a in out)
+    with pytest.raises(IndexError):
+        K.cast_rays(m, np.zeros((1, 3), np.float32), np.ones((1, 3), np.float32), np.array([m.n_tets], np.int32))
+    with pytest.raises(ValueError):
+        K.cast_rays(m, np.zeros((2, 3), np.float32), np.ones((1, 3), np.float32), np.array([0, 0], np.int32))
+    from paper_2103_02309_b200 import batch
+
+    bad = golden_mesh(golden, "box4")
+    with pytest.raises(RuntimeError):  # batch layer raises on cycle-guard rays (batch.py:53-55)
+        from paper_2103_02309_b200.ingestion import build_box_fixture
+        from paper_2103_02309_b200.scenes import camera_rays
+        from paper_2103_02309_b200.tetmesh import encode
+
+        raw, soup = build_box_fixture(8, occluders=[(0, 4, (2, 2), (6, 6))])
+        bad = encode(raw, "tet20", soup)
+        o, d = camera_rays((4.0, 4.0, 0.5), (4.0, 4.0, 8.0), (0.0, 1.0, 0.0), 68.0, 1024, 1024)
+        cam, _ = K.locate_points(bad, np.array([[4.0, 4.0, 0.5]]), np.array([0], np.int32))
+        batch.cast_rays(bad, o, d, np.full(len(o), cam[0], np.int32))
+
+
+def test_trace_torch_api(golden):
+    import torch
+
+    from paper_2103_02309_b200.scenes import interior_rays
+    from paper_2103_02309_b200.trace import trace
+    from oracle import pyoracle
+
+    m = golden_mesh(golden, "model", "tet16")
+    o, d, st = interior_rays(m, 20000, 11)
+    dev = torch.device("cuda", 0)
+    res = trace(m, torch.from_numpy(o).to(dev), torch.from_numpy(d).to(dev), torch.from_numpy(st).to(dev))
+    torch.cuda.synchronize()
+    exp = pyoracle.cast_rays_full(m, o, d, st)
+    got = (res.status, res.cf, res.tet, res.visited, res.triangle, res.t, res.tet_back)
+    for k, a, b in zip(NAMES7, got, exp):
+        assert np.array_equal(a.cpu().numpy(), b), k
