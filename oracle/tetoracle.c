@@ -204,7 +204,11 @@ static uint32_t walk_step(const to_mesh* m, walk_t* s, uint32_t nxt, uint32_t pr
   return out;
 }
 
-/* ---- epilogue t, _kernels_py.py:435-454 (reciprocal multiply) --------------- */
+/* ---- epilogue t, _kernels_py.py:435-454 (reciprocal multiply) ---------------
+ * Dot products follow numpy 2.3's einsum("ij,ij->i") reduction over three
+ * terms: SIMD lanes [p0, p1, p2, 0] summed pairwise, i.e. (p0 + p2) + p1. */
+static inline double einsum3(const double* x, const double* y) { return (x[0] * y[0] + x[2] * y[2]) + x[1] * y[1]; }
+
 double to_mt_t(const double* o, const double* d, const double* T) {
   double e1[3], e2[3], pv[3], tv[3], qv[3];
   for (int c = 0; c < 3; ++c) {
@@ -215,18 +219,19 @@ double to_mt_t(const double* o, const double* d, const double* T) {
   pv[0] = d[1] * e2[2] - d[2] * e2[1];
   pv[1] = d[2] * e2[0] - d[0] * e2[2];
   pv[2] = d[0] * e2[1] - d[1] * e2[0];
-  double det = (e1[0] * pv[0] + e1[1] * pv[1]) + e1[2] * pv[2];
+  double det = einsum3(e1, pv);
   if (det != 0.0) {
     double inv = 1.0 / det;
     qv[0] = tv[1] * e1[2] - tv[2] * e1[1];
     qv[1] = tv[2] * e1[0] - tv[0] * e1[2];
     qv[2] = tv[0] * e1[1] - tv[1] * e1[0];
-    return ((e2[0] * qv[0] + e2[1] * qv[1]) + e2[2] * qv[2]) * inv;
+    return einsum3(e2, qv) * inv;
   }
   double nrm[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
-  double den = (nrm[0] * d[0] + nrm[1] * d[1]) + nrm[2] * d[2];
+  double den = einsum3(nrm, d);
   if (den == 0.0) return 0.0;
-  return ((nrm[0] * (T[0] - o[0]) + nrm[1] * (T[1] - o[1])) + nrm[2] * (T[2] - o[2])) / den;
+  double rel[3] = {T[0] - o[0], T[1] - o[1], T[2] - o[2]};
+  return einsum3(nrm, rel) / den;
 }
 
 /* ---- shadow segment t, _kernels.pyx:495-524 (division form) ----------------- */

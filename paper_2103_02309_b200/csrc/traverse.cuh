@@ -317,8 +317,15 @@ __device__ __forceinline__ uint32_t advance(const MeshView& m, const Basis& b, u
 
 // ----------------------------------------------------------------------------
 // fp64 epilogue: t of the ray/triangle pair, _kernels_py._mt_t
-// (_kernels_py.py:435-454) -- reciprocal-multiply form, numpy's cross and
-// einsum operation order, plane-distance fallback for det == 0.
+// (_kernels_py.py:435-454) -- reciprocal-multiply form, numpy's np.cross
+// operation order, plane-distance fallback for det == 0.  The dot products
+// are numpy's einsum("ij,ij->i") over 3 terms, which numpy 2.3 reduces as
+// SIMD lanes [p0, p1, p2, 0] summed pairwise: (p0 + p2) + p1 (measured
+// against the reference's outputs, tests/test_oracle.py).
+__device__ __forceinline__ double einsum3(double x0, double y0, double x1, double y1, double x2, double y2) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(x0, y0), __dmul_rn(x2, y2)), __dmul_rn(x1, y1));
+}
+
 __device__ __forceinline__ double mt_t(double ox, double oy, double oz, double dx, double dy,
                                        double dz, const double* __restrict__ T) {
   const double ax = __ldg(T + 0), ay = __ldg(T + 1), az = __ldg(T + 2);
@@ -330,7 +337,7 @@ __device__ __forceinline__ double mt_t(double ox, double oy, double oz, double d
   const double pvx = __dsub_rn(__dmul_rn(dy, e2z), __dmul_rn(dz, e2y));
   const double pvy = __dsub_rn(__dmul_rn(dz, e2x), __dmul_rn(dx, e2z));
   const double pvz = __dsub_rn(__dmul_rn(dx, e2y), __dmul_rn(dy, e2x));
-  const double det = __dadd_rn(__dadd_rn(__dmul_rn(e1x, pvx), __dmul_rn(e1y, pvy)), __dmul_rn(e1z, pvz));
+  const double det = einsum3(e1x, pvx, e1y, pvy, e1z, pvz);
   const double tvx = __dsub_rn(ox, ax), tvy = __dsub_rn(oy, ay), tvz = __dsub_rn(oz, az);
   if (det != 0.0) {
     const double inv = __ddiv_rn(1.0, det);
@@ -338,17 +345,15 @@ __device__ __forceinline__ double mt_t(double ox, double oy, double oz, double d
     const double qx = __dsub_rn(__dmul_rn(tvy, e1z), __dmul_rn(tvz, e1y));
     const double qy = __dsub_rn(__dmul_rn(tvz, e1x), __dmul_rn(tvx, e1z));
     const double qz = __dsub_rn(__dmul_rn(tvx, e1y), __dmul_rn(tvy, e1x));
-    const double num = __dadd_rn(__dadd_rn(__dmul_rn(e2x, qx), __dmul_rn(e2y, qy)), __dmul_rn(e2z, qz));
-    return __dmul_rn(num, inv);
+    return __dmul_rn(einsum3(e2x, qx, e2y, qy, e2z, qz), inv);
   }
   // parallel: plane distance
   const double nx = __dsub_rn(__dmul_rn(e1y, e2z), __dmul_rn(e1z, e2y));
   const double ny = __dsub_rn(__dmul_rn(e1z, e2x), __dmul_rn(e1x, e2z));
   const double nz = __dsub_rn(__dmul_rn(e1x, e2y), __dmul_rn(e1y, e2x));
-  const double denom = __dadd_rn(__dadd_rn(__dmul_rn(nx, dx), __dmul_rn(ny, dy)), __dmul_rn(nz, dz));
+  const double denom = einsum3(nx, dx, ny, dy, nz, dz);
   if (denom == 0.0) return 0.0;
-  const double num = __dadd_rn(__dadd_rn(__dmul_rn(nx, __dsub_rn(ax, ox)), __dmul_rn(ny, __dsub_rn(ay, oy))),
-                               __dmul_rn(nz, __dsub_rn(az, oz)));
+  const double num = einsum3(nx, __dsub_rn(ax, ox), ny, __dsub_rn(ay, oy), nz, __dsub_rn(az, oz));
   return __ddiv_rn(num, denom);
 }
 
