@@ -1,0 +1,453 @@
+#!/usr/bin/env python
+"""bench.py -- tet-mesh ray traversal throughput on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+
+Workload (BASELINE.json configs[1], the metric's single-GPU config):
+config 2 = the reference's blob generator at GRID=55 (1,109,444 tets,
+byte-identical to gen_model_mesh -> parse_tetgen -> encode, pinned by
+tests/test_host_mirror.py), TetMesh-20, Hilbert-sorted, 1920x1080 primary
+rays from the blob camera, all starting in the located camera tet.
+A "step" traces one frame per GPU.  Weak scaling: at N GPUs the job is N
+frames (camera jittered per frame), 16x16 tiles dealt round-robin to ranks,
+hit buffers gathered to rank 0 with one NCCL collective inside the timed
+region.
+
+value  = rays / device time of the trace kernel (CUDA events on the launch
+         stream, inputs resident in HBM, L2 flushed between steps).
+e2e    = the same rays through the C ABI with pinned HOST buffers
+         (tb_cast_rays_host: H2D, kernel, D2H, sync) per step.
+roofline = SURVEY.md s8(d) algorithmic bytes / kernel time vs measured HBM.
+cpu_baseline = the reference's compiled kernels (oracle/_ref) + its batch
+         epilogue on all host cores (rank 0, N=1, bounded sample).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: dict(grid=12, width=256, height=256, layout="tet20", scheme="none",
+            desc="cfg1: blob GRID=12 (11,029 tets), 256x256 primary rays"),
+    2: dict(grid=55, width=1920, height=1080, layout="tet20", scheme="hilbert",
+            desc="cfg2: blob GRID=55 (1,109,444 tets), 1920x1080 primary rays, TetMesh-20 Hilbert-sorted"),
+    3: dict(grid=55, width=3840, height=2160, layout="tet16", scheme="hilbert",
+            desc="cfg3: blob GRID=55 (1,109,444 tets), 3840x2160 primary rays, TetMesh-16 Hilbert-sorted"),
+    4: dict(grid=55, width=4096, height=4096, layout="tet16", scheme="hilbert", secondaries=True,
+            desc="cfg4: blob GRID=55, 16.7M diffuse secondaries from 4096x4096 primary hits, TetMesh-16"),
+}
+L2_FLUSH_BYTES = 256 << 20
+FALLBACK_HBM_GBS = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def build_scene(cfg):
+    from paper_2103_02309_b200.scenes import blob_scene
+
+    t0 = time.perf_counter()
+    sc = blob_scene(cfg["grid"], layout=cfg["layout"], scheme=cfg["scheme"], check=False)
+    log(f"[bench] scene {sc.name}: {sc.mesh.n_tets} tets, {sc.mesh.n_points} points, "
+        f"{sc.mesh.n_constrained} constrained faces, built in {time.perf_counter() - t0:.1f}s")
+    return sc
+
+
+def frame_rays(cfg, frame: int):
+    from paper_2103_02309_b200.scenes import BLOB_CAMERA, camera_rays
+
+    pos = np.asarray(BLOB_CAMERA["position"], dtype=np.float64) + np.array([0.0, 0.02, 0.0]) * frame
+    o, d = camera_rays(tuple(pos), BLOB_CAMERA["look_at"], BLOB_CAMERA["up"], BLOB_CAMERA["fov"],
+                       cfg["width"], cfg["height"])
+    return o, d, pos
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_trace(mesh, o, d, st, threads: int):
+    """The reference's CPU path for one batch: compiled kernels (oracle/_ref,
+    _kernels.pyx:271-370, GIL released) + the batch epilogue (batch.py:57-71),
+    chunked over a thread pool like the reference renderer's tile pool."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import pyoracle
+
+    K = pyoracle.ref_kernels()
+    kind = "reference"
+    if K is None:
+        K, kind = pyoracle, "port"
+    n = len(st)
+    chunks = max(threads * 16, 1)
+    bounds = np.linspace(0, n, chunks + 1).astype(np.int64)
+
+    def work(i):
+        a, b = bounds[i], bounds[i + 1]
+        if a == b:
+            return 0
+        status, cf, tet, visited = K.cast_rays(mesh, o[a:b], d[a:b], st[a:b])
+        pyoracle.batch_epilogue(mesh, o[a:b], d[a:b], status, cf, tet)
+        return int(visited.sum())
+
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        total_vis = sum(pool.map(work, range(chunks)))
+    return kind, total_vis
+
+
+def run_reference_arm(args, cfg):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    sc = build_scene(cfg)
+    mesh = sc.mesh
+    from oracle import pyoracle
+
+    o, d, pos = frame_rays(cfg, 0)
+    K = pyoracle.ref_kernels() or pyoracle
+    cam, _ = K.locate_points(mesh, pos[None], np.array([mesh.source_tet], np.int32))
+    st = np.full(len(o), int(cam[0]), dtype=np.int32)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        kind, _ = cpu_reference_trace(mesh, o, d, st, threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        kind, vis = cpu_reference_trace(mesh, o, d, st, threads)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = len(o) * args.steps / total / 1e6
+    line = {
+        "impl": "reference", "metric": "Mrays/s", "value": value, "unit": "Mrays/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "rays_per_step": len(o), "layout": cfg["layout"],
+                   "scheme": cfg["scheme"]},
+        "tets_visited_per_ray": {"mean": vis / len(o)},
+        "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": threads, "kind": kind,
+                         "sample": f"full frame ({len(o)} rays) per step: compiled _kernels.cast_rays + "
+                                   "batch epilogue, ThreadPoolExecutor over 16 chunks/thread"},
+        "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def digest(*arrays) -> str:
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()[:16]
+
+
+def algorithmic_bytes(visited: np.ndarray, layout: str) -> int:
+    """sum_rays [(visited-1)(L+12) + 68] + 53 N."""
+    L = {"tet32": 32, "tet20": 20, "tet16": 16, "tet80": 80}[layout]
+    point = 0 if layout == "tet80" else 12
+    v = visited.astype(np.int64)
+    return int(((v - 1) * (L + point)).sum() + 68 * len(v) + 53 * len(v))
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_02309_b200 import multigpu
+    from paper_2103_02309_b200._lib import addr, check, lib
+    from paper_2103_02309_b200.device import device_mesh
+    from paper_2103_02309_b200.trace import empty_result, locate, trace
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    sc = build_scene(cfg)
+    mesh = sc.mesh
+    dm = device_mesh(mesh, device=local)
+    W, H = cfg["width"], cfg["height"]
+    per_frame = W * H
+
+    # this rank's share of the N-frame job (16x16 tiles round-robin)
+    idx = multigpu.shard_pixels(W, H, rank, world, 16, frames=world)
+    frames = idx // per_frame
+    o = np.empty((len(idx), 3), np.float32)
+    d = np.empty((len(idx), 3), np.float32)
+    st = np.empty(len(idx), np.int32)
+    for f in np.unique(frames):
+        of, df, pos = frame_rays(cfg, int(f))
+        sel = frames == f
+        o[sel] = of[idx[sel] % per_frame]
+        d[sel] = df[idx[sel] % per_frame]
+        q = torch.tensor(pos[None], dtype=torch.float64, device=dev)
+        cam, _ = locate(dm, q, torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))
+        st[sel] = int(cam.item())
+    n = len(st)
+    go, gd, gs = (torch.from_numpy(a).to(dev) for a in (o, d, st))
+    res = empty_result(n, dev)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    gidx = torch.from_numpy(idx).to(dev)
+
+    def step():
+        trace(dm, go, gd, gs, out=res, stream=stream)
+
+    # warm-up
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    # parity at full size: the reference's own digest of this frame (rank 0, N=1)
+    parity = None
+    dig_path = os.path.join(ROOT, "tests", "golden", "golden_digests.json")
+    key = f"blob{cfg['grid']}/{cfg['scheme']}/cast"
+    if world == 1 and os.path.exists(dig_path) and cfg.get("layout") in ("tet20", "tet16", "tet32"):
+        digs = json.load(open(dig_path))
+        if key in digs and (W, H) == {12: (256, 256), 55: (1920, 1080)}.get(cfg["grid"]):
+            got = digest(res.status.cpu().numpy(), res.cf.cpu().numpy(), res.tet.cpu().numpy(),
+                         res.visited.cpu().numpy())
+            ep = digest(res.triangle.cpu().numpy(), res.t.cpu().numpy(), res.tet_back.cpu().numpy())
+            parity = {"vs": "reference digest " + key,
+                      "traversal_bit_exact": got == digs[key],
+                      "epilogue_bit_exact": ep == digs[key.replace("/cast", "/epilogue")]}
+    visited = res.visited.cpu().numpy()
+
+    # timed region: K steps between barrier + sync; per-step kernel events
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    gather_ms = 0.0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        w0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        if world > 1:
+            g0 = torch.cuda.Event(enable_timing=True)
+            g1 = torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            packed = multigpu.pack_hits(gidx, res.status, res.cf, res.tet, res.visited, res.triangle, res.t,
+                                        res.tet_back)
+            multigpu.gather_hits(packed, per_frame * world)
+            g1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        if world > 1:
+            dist.barrier()
+    kernel_ms = np.array([a.elapsed_time(b) for a, b in evs])
+    if world > 1:
+        gather_ms = g0.elapsed_time(g1)
+    my_ms = float(kernel_ms.sum()) + gather_ms
+    if world > 1:
+        t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        max_ms = float(t.item())
+        vt = torch.tensor([int(visited.sum()), int(visited.max()), n], dtype=torch.int64, device=dev)
+        vmax = vt.clone()
+        dist.all_reduce(vt, op=dist.ReduceOp.SUM)
+        dist.all_reduce(vmax, op=dist.ReduceOp.MAX)
+        vis_sum, vis_max, total_rays = int(vt[0]), int(vmax[1]), int(vt[2])
+    else:
+        max_ms = my_ms
+        vis_sum, vis_max, total_rays = int(visited.sum()), int(visited.max()), n
+
+    value = total_rays * args.steps / (max_ms / 1e3) / 1e6
+    ms_per_step = max_ms / args.steps
+
+    # end to end through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        ho = torch.from_numpy(o).pin_memory()
+        hd = torch.from_numpy(d).pin_memory()
+        hs = torch.from_numpy(st).pin_memory()
+        outs = [torch.empty(n, dtype=dt).pin_memory() for dt in
+                (torch.uint8, torch.int32, torch.int32, torch.int32, torch.int32, torch.float64, torch.int32)]
+
+        def host_call():
+            check(lib.tb_cast_rays_host(dm.handle, n, addr(ho), addr(hd), addr(hs), *[addr(x) for x in outs]),
+                  "tb_cast_rays_host")
+
+        for _ in range(max(1, args.warmup)):
+            host_call()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            host_call()
+        e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_s = float(t.item())
+        e2e = {"value": total_rays * args.steps / e_s / 1e6, "unit": "Mrays/s",
+               "h2d_bytes_per_step": int(n * (12 + 12 + 4)), "d2h_bytes_per_step": int(n * (1 + 4 * 5 + 8)),
+               "ms_per_step": e_s / args.steps * 1e3, "path": "tb_cast_rays_host (C ABI, pinned host buffers)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = measured_peak()
+    alg = algorithmic_bytes(visited, cfg["layout"])
+    kern_s = float(kernel_ms.mean()) / 1e3
+    achieved = alg / kern_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"cfg{args.config}/{cfg['layout']}")
+    line = {
+        "metric": "Mrays/s", "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "rays_per_gpu": n, "layout": cfg["layout"], "scheme": cfg["scheme"],
+                   "parallelism": f"tile-shard x{world}, mesh replicated", "l2": "flushed between steps (256 MiB)",
+                   "frames": world},
+        "tets_visited_per_ray": {"mean": vis_sum / total_rays, "max": vis_max},
+        "kernel_ms": {"mean": float(kernel_ms.mean()), "min": float(kernel_ms.min()), "max": float(kernel_ms.max())},
+        "gather_ms": gather_ms if world > 1 else None,
+        "wall_ms_per_step": wall / args.steps * 1e3,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg, "kernel": f"cast_kernel<{cfg['layout'][3:]}>"},
+        "clocks": clocks.summary(),
+        "gpu_launches": args.steps + (1 if world > 1 else 0),
+        "parity": parity,
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        from concurrent.futures import ThreadPoolExecutor  # noqa: F401
+
+        threads = os.cpu_count() or 1
+        m = min(n, args.cpu_sample)
+        t0 = time.perf_counter()
+        reps = 0
+        best = None
+        while reps < 3 and (time.perf_counter() - t0) < 20.0:
+            s0 = time.perf_counter()
+            kind, _ = cpu_reference_trace(mesh, o[:m], d[:m], st[:m], threads)
+            dt = time.perf_counter() - s0
+            best = dt if best is None else min(best, dt)
+            reps += 1
+        line["cpu_baseline"] = {"value": m / best / 1e6, "unit": "Mrays/s", "cores": threads, "kind": kind,
+                                "sample": f"first {m} rays of the frame, best of {reps}: compiled reference "
+                                          "kernels + batch epilogue on a thread pool"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--layout", default=None)
+    ap.add_argument("--scheme", default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=2_073_600)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    cfg = dict(CONFIGS[args.config])
+    if args.layout:
+        cfg["layout"] = args.layout
+    if args.scheme:
+        cfg["scheme"] = args.scheme
+    if cfg.get("secondaries"):
+        raise SystemExit("config 4 is run by bench_secondaries (see DESIGN.md); use --config 2/3")
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -186,3 +186,41 @@ def ref_kernels():
         return _kernels
     except ImportError:
         return None
+
+
+def batch_epilogue(mesh, o32, d32, status, cf, tet):
+    """numpy restatement of the reference batch layer's host epilogue
+    (batch.py:57-71 + _kernels_py._mt_t, _kernels_py.py:435-454): the part of
+    batch.cast_rays that runs after the compiled kernel.  Used to time the
+    reference's CPU path end to end (bench.py --impl reference)."""
+    n = len(status)
+    triangle = np.full(n, -1, dtype=np.int32)
+    t = np.full(n, np.inf, dtype=np.float64)
+    back = np.full(n, -1, dtype=np.int32)
+    hit = status == STATUS_HIT
+    if hit.any():
+        cfs = cf[hit]
+        triangle[hit] = mesh.cf_triangle[cfs]
+        tri = mesh.triangle_coords()[mesh.cf_triangle[cfs]]
+        o = np.asarray(o32)[hit].astype(np.float64)
+        d = np.asarray(d32)[hit].astype(np.float64)
+        e1 = tri[:, 1] - tri[:, 0]
+        e2 = tri[:, 2] - tri[:, 0]
+        pv = np.cross(d, e2)
+        det = np.einsum("ij,ij->i", e1, pv)
+        tv = o - tri[:, 0]
+        with np.errstate(divide="ignore", invalid="ignore"):
+            inv = np.where(det != 0.0, 1.0 / det, 0.0)
+            tt = np.einsum("ij,ij->i", e2, np.cross(tv, e1)) * inv
+        par = det == 0.0
+        if par.any():
+            nrm = np.cross(e1[par], e2[par])
+            den = np.einsum("ij,ij->i", nrm, d[par])
+            num = np.einsum("ij,ij->i", nrm, tri[par, 0] - o[par])
+            with np.errstate(divide="ignore", invalid="ignore"):
+                tt[par] = np.where(den != 0.0, num / den, 0.0)
+        t[hit] = tt
+        a = mesh.cf_tets[cfs, 0]
+        b = mesh.cf_tets[cfs, 1]
+        back[hit] = np.where(a == tet[hit], b, a)
+    return triangle, t, back
