@@ -106,7 +106,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
         except FileNotFoundError:
@@ -115,7 +115,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def mark(self, name: str):
+        setattr(self, name, time.perf_counter())
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -125,10 +128,13 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
+        """Median SM clock and throttle reasons over samples read in [t0, t1]."""
         sm, mx, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in self.lines:
+        for ts, line in self.lines:
+            if (t0 is not None and ts < t0) or (t1 is not None and ts > t1):
+                continue
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 7:
                 continue
@@ -285,21 +291,36 @@ def run_ours(args, cfg):
     if world == 1 and os.path.exists(dig_path) and cfg.get("layout") in ("tet20", "tet16", "tet32"):
         digs = json.load(open(dig_path))
         if key in digs and (W, H) == {12: (256, 256), 55: (1920, 1080)}.get(cfg["grid"]):
-            got = digest(res.status.cpu().numpy(), res.cf.cpu().numpy(), res.tet.cpu().numpy(),
-                         res.visited.cpu().numpy())
-            ep = digest(res.triangle.cpu().numpy(), res.t.cpu().numpy(), res.tet_back.cpu().numpy())
+            inv = np.empty_like(idx)
+            inv[idx] = np.arange(len(idx))  # shard position of each row-major pixel
+
+            def rm(x):
+                return x.cpu().numpy()[inv]
+
+            got = digest(rm(res.status), rm(res.cf), rm(res.tet), rm(res.visited))
+            ep = digest(rm(res.triangle), rm(res.t), rm(res.tet_back))
             parity = {"vs": "reference digest " + key,
                       "traversal_bit_exact": got == digs[key],
                       "epilogue_bit_exact": ep == digs[key.replace("/cast", "/epilogue")]}
     visited = res.visited.cpu().numpy()
 
-    # timed region: K steps between barrier + sync; per-step kernel events
+    # timed region: K steps between barrier + sync; per-step kernel events.
+    # nvidia-smi samples clocks from a short untimed ramp (so the sampler is
+    # up and the clocks have left idle) through the end of the timed region.
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     gather_ms = 0.0
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
+        time.sleep(0.3)  # nvidia-smi start-up
+        clocks.mark("t_ramp")
+        r0 = time.perf_counter()
+        while time.perf_counter() - r0 < args.ramp_s:
+            for _ in range(8):
+                flush.zero_()
+                step()
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         w0 = time.perf_counter()
         for i in range(args.steps):
             flush.zero_()
@@ -316,8 +337,10 @@ def run_ours(args, cfg):
             g1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
+        clocks.mark("t_end")
         if world > 1:
             dist.barrier()
+        time.sleep(0.05)
     kernel_ms = np.array([a.elapsed_time(b) for a, b in evs])
     if world > 1:
         gather_ms = g0.elapsed_time(g1)
@@ -365,7 +388,8 @@ def run_ours(args, cfg):
             e_s = float(t.item())
         e2e = {"value": total_rays * args.steps / e_s / 1e6, "unit": "Mrays/s",
                "h2d_bytes_per_step": int(n * (12 + 12 + 4)), "d2h_bytes_per_step": int(n * (1 + 4 * 5 + 8)),
-               "ms_per_step": e_s / args.steps * 1e3, "path": "tb_cast_rays_host (C ABI, pinned host buffers)"}
+               "ms_per_step": e_s / args.steps * 1e3, "gpu_launches_per_step": -(-n // (1 << 18)),
+               "path": "tb_cast_rays_host (C ABI, pinned host buffers, 3-stream chunked H2D/trace/D2H)"}
 
     if rank != 0:
         if world > 1:
@@ -394,7 +418,7 @@ def run_ours(args, cfg):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg, "kernel": f"cast_kernel<{cfg['layout'][3:]}>"},
-        "clocks": clocks.summary(),
+        "clocks": dict(clocks.summary(clocks.t_ramp, clocks.t_end), window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
         "gpu_launches": args.steps + (1 if world > 1 else 0),
         "parity": parity,
         "e2e": e2e,
@@ -424,7 +448,7 @@ def run_ours(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
@@ -433,6 +457,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2_073_600)
+    ap.add_argument("--ramp-s", type=float, default=0.5, help="untimed load before the timed region (clock ramp)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -193,7 +193,7 @@ static inline const float* vertex_xyz(const to_mesh* m, const uint32_t* r, uint3
 static uint32_t walk_step(const to_mesh* m, walk_t* s, uint32_t nxt, uint32_t prev) {
   const uint32_t* r = m->recs + (int64_t)rec_words(m->layout) * nxt;
   uint32_t i3 = s->idx[0] ^ s->idx[1] ^ s->idx[2] ^ rec_xor(m, r);
-  if (m->layout != 80 && (int64_t)i3 >= m->n_points) i3 = 0; /* corrupt record: stay in bounds */
+  if (m->layout != 80 && (int64_t)i3 >= m->n_points) i3 = (uint32_t)(m->n_points - 1); /* corrupt record: stay in bounds */
   float px, py;
   frame_project(&s->f, vertex_xyz(m, r, i3), &px, &py);
   int k = alg1_exit(px, py, s->w);
@@ -397,7 +397,7 @@ static void sctp_one(const to_mesh* m, int64_t r, const float* o, const float* d
     if ((int64_t)nxt >= m->n_tets) { st = 2; break; }
     const uint32_t* rec = m->recs + (int64_t)rec_words(m->layout) * nxt;
     uint32_t i3 = face[0] ^ face[1] ^ face[2] ^ rec_xor(m, rec);
-    if (m->layout != 80 && (int64_t)i3 >= m->n_points) i3 = 0;
+    if (m->layout != 80 && (int64_t)i3 >= m->n_points) i3 = (uint32_t)(m->n_points - 1); /* corrupt record: stay in bounds */
     const float* q = vertex_xyz(m, rec, i3);
     /* sorted quad: insert i3 into the ascending face */
     int pos = (face[0] < i3) + (face[1] < i3) + (face[2] < i3);

@@ -101,7 +101,7 @@ __device__ __forceinline__ uint32_t sctp_advance(const MeshView& m, SctpWindow& 
   Record<L> rec;
   rec.load(m, nxt);
   uint32_t i3 = w.id[0] ^ w.id[1] ^ w.id[2] ^ rec.vxw();
-  if (L != 80 && i3 >= (uint32_t)m.n_points) i3 = 0;
+  if (L != 80) i3 = min(i3, (uint32_t)m.n_points - 1u);
   const float4 q = fetch_vertex<L>(m, rec, i3);
   const int pos = (w.id[0] < i3) + (w.id[1] < i3) + (w.id[2] < i3);  // entry slot
   uint32_t ids[4];

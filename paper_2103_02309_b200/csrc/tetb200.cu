@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -89,9 +90,21 @@ inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 
 
 // ----------------------------------------------------------------------------
 // Mesh build kernels (run once per upload).
+// Six axis-permuted float4 copies of the points (traverse.cuh, perm_index):
+// copy k = mx * 2 + (ot > mx ? ot - 1 : ot) holds (q[mx], q[ot], q[mn], 0).
 __global__ void pad_points_kernel(const float* __restrict__ xyz, float4* __restrict__ out, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) out[i] = make_float4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], 0.0f);
+  if (i >= n) return;
+  const float q[3] = {xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]};
+#pragma unroll
+  for (int mx = 0; mx < 3; ++mx) {
+#pragma unroll
+    for (int ot = 0; ot < 3; ++ot) {
+      if (ot == mx) continue;
+      const int mn = 3 - mx - ot;
+      out[(size_t)perm_index(mx, ot) * (size_t)n + i] = make_float4(q[mx], q[ot], q[mn], 0.0f);
+    }
+  }
 }
 
 __global__ void split_tet20_kernel(const uint32_t* __restrict__ rec, uint32_t* __restrict__ vx,
@@ -116,6 +129,37 @@ __global__ void build_tet80_kernel(const int4* __restrict__ sv, const uint4* __r
   o[2] = make_uint4(__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(a.z), __float_as_uint(b.x));
   o[3] = make_uint4(__float_as_uint(b.y), __float_as_uint(b.z), __float_as_uint(c.x), __float_as_uint(c.y));
   o[4] = make_uint4(__float_as_uint(c.z), __float_as_uint(d.x), __float_as_uint(d.y), __float_as_uint(d.z));
+}
+
+// ----------------------------------------------------------------------------
+// Warp-cooperative load of one (n, 3) float32 row per lane: the warp reads
+// its 96 consecutive floats as three fully coalesced 128 B rows and
+// redistributes them with shuffles, so every input byte is requested once
+// (this matters most when the rays live in mapped host memory and each
+// request crosses PCIe).  Must be called by all 32 lanes of the warp.
+__device__ __forceinline__ void load_xyz_warp(const float* __restrict__ a, int64_t r, int64_t n, float& x,
+                                              float& y, float& z) {
+  const int lane = threadIdx.x & 31;
+  const int64_t base = 3 * (r - lane);
+  const int64_t lim = 3 * n;
+  float v[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int64_t e = base + 32 * k + lane;
+    v[k] = (e < lim) ? __ldg(a + e) : 0.0f;
+  }
+  float out[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const int e = 3 * lane + c;  // element of the warp's 96-float window
+    const float s0 = __shfl_sync(0xffffffffu, v[0], e & 31);
+    const float s1 = __shfl_sync(0xffffffffu, v[1], e & 31);
+    const float s2 = __shfl_sync(0xffffffffu, v[2], e & 31);
+    out[c] = (e < 32) ? s0 : ((e < 64) ? s1 : s2);
+  }
+  x = out[0];
+  y = out[1];
+  z = out[2];
 }
 
 // ----------------------------------------------------------------------------
@@ -158,30 +202,31 @@ __global__ void __launch_bounds__(kBlock) cast_kernel(MeshView m, int64_t n, con
                                                       int32_t* __restrict__ triangle, double* __restrict__ t,
                                                       int32_t* __restrict__ tet_back) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  float o0, o1, o2, d0, d1, d2;
+  load_xyz_warp(o, r, n, o0, o1, o2);  // whole warp participates (shuffles)
+  load_xyz_warp(d, r, n, d0, d1, d2);
   if (r >= n) return;
-  const float o0 = __ldg(o + 3 * r), o1 = __ldg(o + 3 * r + 1), o2 = __ldg(o + 3 * r + 2);
-  const float d0 = __ldg(d + 3 * r), d1 = __ldg(d + 3 * r + 1), d2 = __ldg(d + 3 * r + 2);
   uint32_t cur = (uint32_t)__ldg(start + r);
   Basis b;
   uint32_t idx[3];
   float p[6];
   const int j = init_ray(m, o0, o1, o2, d0, d1, d2, (int)cur, b, idx, p);
   uint32_t ref = pick4u(__ldg(&m.sn[cur]), j);
-  uint32_t prev = cur;
+  const float4* __restrict__ P = ray_points(m, b);
   int vis = 1;
-  uint8_t st;
+  uint8_t st = 255;
   const uint32_t n_tets = (uint32_t)m.n_tets;
-  while (true) {
-    if (ref == kBoundary) { st = kMiss; break; }
-    if (ref & kConstrained) { st = kHit; break; }
-    const uint32_t nxt = ref & kPayload;
-    if (nxt >= n_tets) { st = kError; break; }  // corrupt reference: fail the ray, never fault
-    ref = advance<L>(m, b, idx, p, nxt, prev);
-    prev = nxt;
+  // Every plain tet reference is < n_tets; the boundary sentinel
+  // (0x7FFFFFFF) and constrained refs (bit 31) are >= n_tets, so one
+  // unsigned compare per step decides "keep walking" (corrupt refs also land
+  // outside and are classified below).
+  while (ref < n_tets) {
+    const uint32_t nxt = ref;
+    ref = advance<L>(m, P, b, idx, p, nxt, cur);
     cur = nxt;
-    ++vis;
-    if ((uint32_t)vis > n_tets) { st = kError; break; }  // cycle guard, _kernels.pyx:365-368
+    if ((uint32_t)++vis > n_tets) { st = kError; break; }  // cycle guard, _kernels.pyx:365-368
   }
+  if (st != kError) st = (ref == kBoundary) ? kMiss : ((ref & kConstrained) ? kHit : kError);
   write_result(m, r, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
                tet_back);
 }
@@ -205,16 +250,13 @@ __global__ void __launch_bounds__(kBlock) visits_kernel(MeshView m, int64_t n, c
   float p[6];
   const int j = init_ray(m, o0, o1, o2, d0, d1, d2, (int)cur, b, idx, p);
   uint32_t ref = pick4u(__ldg(&m.sn[cur]), j);
-  uint32_t prev = cur;
+  const float4* __restrict__ P = ray_points(m, b);
   if (pos < end) seq[pos++] = (int32_t)cur;
   int vis = 1;
   const uint32_t n_tets = (uint32_t)m.n_tets;
-  while (pos < end) {
-    if (ref == kBoundary || (ref & kConstrained)) break;
-    const uint32_t nxt = ref & kPayload;
-    if (nxt >= n_tets) break;
-    ref = advance<L>(m, b, idx, p, nxt, prev);
-    prev = nxt;
+  while (pos < end && ref < n_tets) {
+    const uint32_t nxt = ref;
+    ref = advance<L>(m, P, b, idx, p, nxt, cur);
     cur = nxt;
     ++vis;
     seq[pos++] = (int32_t)cur;
@@ -278,7 +320,7 @@ __global__ void __launch_bounds__(kBlock) locate_kernel(MeshView m, int64_t n, c
       entry = cur;
     }
     if (nxt >= n_tets) break;
-    ref = advance<L>(m, b, idx, p, nxt, entry);
+    ref = advance<L>(m, ray_points(m, b), b, idx, p, nxt, entry);
     cur = nxt;
     ++vis;
     if (contains(m, nxt, qq)) { res = (int32_t)nxt; break; }
@@ -344,7 +386,7 @@ __global__ void __launch_bounds__(kBlock) shadow_kernel(MeshView m, int64_t n, c
     }
     if ((int32_t)nxt == ltet) break;
     if (nxt >= n_tets) break;
-    ref = advance<L>(m, b, idx, pw, nxt, entry);
+    ref = advance<L>(m, ray_points(m, b), b, idx, pw, nxt, entry);
     cur = nxt;
     ++vis;
     if ((uint32_t)vis > n_tets) break;
@@ -504,7 +546,7 @@ int tb_mesh_create(int device, int layout, int64_t n_points, const float* points
   } while (0)
 
   float* tmp_xyz = nullptr;
-  TB_MC(cudaMalloc(&m->pts, n_points * sizeof(float4)));
+  TB_MC(cudaMalloc(&m->pts, 6 * n_points * sizeof(float4)));
   TB_MC(cudaMalloc(&tmp_xyz, n_points * 3 * sizeof(float)));
   TB_MC(cudaMemcpy(tmp_xyz, points_xyz, n_points * 3 * sizeof(float), cudaMemcpyHostToDevice));
   pad_points_kernel<<<grid_for(n_points, 256), 256>>>(tmp_xyz, m->pts, n_points);
@@ -556,7 +598,7 @@ int tb_mesh_create(int device, int layout, int64_t n_points, const float* points
     TB_MC(cudaMemcpy(m->tri, tri_coords, n_tri * 9 * sizeof(double), cudaMemcpyHostToDevice));
   }
 #undef TB_MC
-  m->hbm_bytes = n_points * 16 + n_tets * 32 + rec_bytes + n_cf * 12 + n_tri * 72;
+  m->hbm_bytes = n_points * 16 * 6 + n_tets * 32 + rec_bytes + n_cf * 12 + n_tri * 72;
   // Hot accelerator bytes as the reference counts them (records + f32 xyz points).
   m->hot_bytes = (layout == 80) ? rec_bytes : rec_bytes + n_points * 12;
   *out = m;
@@ -693,6 +735,72 @@ struct HostCall {
     return p;
   }
 };
+
+// Per-thread, per-device pipeline context for tb_cast_rays_host: streams and
+// device staging buffers are created once and reused by every call.
+struct PipeCtx {
+  static constexpr int kStreams = 3;
+  static constexpr int64_t kChunk = 1 << 18;  // rays per pipeline chunk
+  struct Slot {
+    cudaStream_t s = nullptr;
+    char* base = nullptr;
+    float *o = nullptr, *d = nullptr;
+    int32_t *st = nullptr, *cf = nullptr, *tet = nullptr, *vis = nullptr, *tri = nullptr, *back = nullptr;
+    uint8_t* status = nullptr;
+    double* t = nullptr;
+  } slot[kStreams];
+};
+
+// Device address of a mapped pinned host buffer (false for pageable memory).
+bool mapped_ptr(const void* p, void** dev) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (a.type != cudaMemoryTypeHost || a.devicePointer == nullptr) return false;
+  *dev = a.devicePointer;
+  return true;
+}
+
+// TETB200_E2E: 0 = auto (zero-copy when all host buffers are mapped pinned),
+// 1 = always stage through device buffers.
+int e2e_mode() {
+  const char* v = getenv("TETB200_E2E");
+  return v ? atoi(v) : 0;
+}
+
+int pipe_ctx(int device, PipeCtx** out) {
+  static thread_local PipeCtx* ctxs[64] = {nullptr};
+  if (device < 0 || device >= 64) return set_error(TB_E_ARG, "device %d out of range", device);
+  if (ctxs[device] == nullptr) {
+    PipeCtx* c = new PipeCtx();
+    const size_t k = (size_t)PipeCtx::kChunk;
+    for (int i = 0; i < PipeCtx::kStreams; ++i) {
+      PipeCtx::Slot& sl = c->slot[i];
+      TB_CUDA(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
+      HostCall hc;  // reuse the bump allocator arithmetic
+      const size_t total = HostCall::al(k * 12) * 2 + HostCall::al(k * 4) * 6 + HostCall::al(k) + HostCall::al(k * 8);
+      TB_CUDA(cudaMalloc((void**)&sl.base, total));
+      hc.base = sl.base;
+      sl.o = hc.take<float>(k * 3);
+      sl.d = hc.take<float>(k * 3);
+      sl.st = hc.take<int32_t>(k);
+      sl.status = hc.take<uint8_t>(k);
+      sl.cf = hc.take<int32_t>(k);
+      sl.tet = hc.take<int32_t>(k);
+      sl.vis = hc.take<int32_t>(k);
+      sl.tri = hc.take<int32_t>(k);
+      sl.t = hc.take<double>(k);
+      sl.back = hc.take<int32_t>(k);
+      hc.base = nullptr;  // owned by the slot, not freed by ~HostCall
+    }
+    ctxs[device] = c;
+  }
+  *out = ctxs[device];
+  return TB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -703,36 +811,61 @@ int tb_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, con
   if (int e = check_mesh(m)) return e;
   if (n < 0) return set_error(TB_E_ARG, "negative ray count");
   if (n == 0) return TB_OK;
+  if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
   DeviceGuard g(m->device);
-  HostCall hc;
-  TB_CUDA(cudaStreamCreateWithFlags(&hc.s, cudaStreamNonBlocking));
-  const size_t un = (size_t)n;
-  const size_t total = HostCall::al(un * 12) * 2 + HostCall::al(un * 4) * 6 + HostCall::al(un) + HostCall::al(un * 8);
-  TB_CUDA(cudaMallocAsync((void**)&hc.base, total, hc.s));
-  float* dO = hc.take<float>(un * 3);
-  float* dD = hc.take<float>(un * 3);
-  int32_t* dS = hc.take<int32_t>(un);
-  uint8_t* dSt = hc.take<uint8_t>(un);
-  int32_t* dCf = hc.take<int32_t>(un);
-  int32_t* dTet = hc.take<int32_t>(un);
-  int32_t* dVis = hc.take<int32_t>(un);
-  int32_t* dTri = hc.take<int32_t>(un);
-  double* dT = hc.take<double>(un);
-  int32_t* dBack = hc.take<int32_t>(un);
-  TB_CUDA(cudaMemcpyAsync(dO, o, un * 12, cudaMemcpyHostToDevice, hc.s));
-  TB_CUDA(cudaMemcpyAsync(dD, d, un * 12, cudaMemcpyHostToDevice, hc.s));
-  TB_CUDA(cudaMemcpyAsync(dS, start, un * 4, cudaMemcpyHostToDevice, hc.s));
-  if (int e = tb_cast_rays(m, n, dO, dD, dS, dSt, dCf, dTet, dVis, triangle ? dTri : nullptr, t ? dT : nullptr,
-                           tet_back ? dBack : nullptr, hc.s))
-    return e;
-  TB_CUDA(cudaMemcpyAsync(status, dSt, un, cudaMemcpyDeviceToHost, hc.s));
-  TB_CUDA(cudaMemcpyAsync(cf, dCf, un * 4, cudaMemcpyDeviceToHost, hc.s));
-  TB_CUDA(cudaMemcpyAsync(tet, dTet, un * 4, cudaMemcpyDeviceToHost, hc.s));
-  TB_CUDA(cudaMemcpyAsync(visited, dVis, un * 4, cudaMemcpyDeviceToHost, hc.s));
-  if (triangle) TB_CUDA(cudaMemcpyAsync(triangle, dTri, un * 4, cudaMemcpyDeviceToHost, hc.s));
-  if (t) TB_CUDA(cudaMemcpyAsync(t, dT, un * 8, cudaMemcpyDeviceToHost, hc.s));
-  if (tet_back) TB_CUDA(cudaMemcpyAsync(tet_back, dBack, un * 4, cudaMemcpyDeviceToHost, hc.s));
-  TB_CUDA(cudaStreamSynchronize(hc.s));
+  PipeCtx* ctx = nullptr;
+  if (int e = pipe_ctx(m->device, &ctx)) return e;
+  const int mode = e2e_mode();
+  // Zero-copy path: when every buffer is mapped pinned host memory
+  // (cudaHostAlloc / torch pin_memory under UVA), the trace kernel reads the
+  // rays and writes the hits straight over PCIe -- one launch, no staging
+  // copies; reads and writes use the two link directions concurrently.
+  void *dO, *dD, *dS, *dSt, *dCf, *dTet, *dVis, *dTri = nullptr, *dT = nullptr, *dBack = nullptr;
+  const bool outs_mapped = mapped_ptr(status, &dSt) && mapped_ptr(cf, &dCf) && mapped_ptr(tet, &dTet) &&
+                           mapped_ptr(visited, &dVis) && (!triangle || mapped_ptr(triangle, &dTri)) &&
+                           (!t || mapped_ptr(t, &dT)) && (!tet_back || mapped_ptr(tet_back, &dBack));
+  const bool ins_mapped = mapped_ptr(o, &dO) && mapped_ptr(d, &dD) && mapped_ptr(start, &dS);
+  if (mode == 0 && outs_mapped && ins_mapped) {
+    const cudaStream_t s = ctx->slot[0].s;
+    if (int e = tb_cast_rays(m, n, (const float*)dO, (const float*)dD, (const int32_t*)dS, (uint8_t*)dSt,
+                             (int32_t*)dCf, (int32_t*)dTet, (int32_t*)dVis, (int32_t*)dTri, (double*)dT,
+                             (int32_t*)dBack, s))
+      return e;
+    TB_CUDA(cudaStreamSynchronize(s));
+    return TB_OK;
+  }
+  // Chunked 3-stream pipeline: chunk c's H2D, kernel and D2H are ordered on
+  // stream c % 3, so copies of one chunk overlap the trace of the previous
+  // one and the D2H of the one before (H2D and D2H use separate copy engines).
+  const int64_t chunk = PipeCtx::kChunk;
+  for (int64_t c0 = 0, c = 0; c0 < n; c0 += chunk, ++c) {
+    const int64_t k = (n - c0 < chunk) ? (n - c0) : chunk;
+    const size_t uk = (size_t)k;
+    PipeCtx::Slot& sl = ctx->slot[c % PipeCtx::kStreams];
+    const cudaStream_t s = sl.s;
+    TB_CUDA(cudaMemcpyAsync(sl.o, o + 3 * c0, uk * 12, cudaMemcpyHostToDevice, s));
+    TB_CUDA(cudaMemcpyAsync(sl.d, d + 3 * c0, uk * 12, cudaMemcpyHostToDevice, s));
+    TB_CUDA(cudaMemcpyAsync(sl.st, start + c0, uk * 4, cudaMemcpyHostToDevice, s));
+    if (outs_mapped && mode == 2) {
+      // inputs by copy engine, hits written by the kernel straight to host
+      if (int e = tb_cast_rays(m, k, sl.o, sl.d, sl.st, (uint8_t*)dSt + c0, (int32_t*)dCf + c0,
+                               (int32_t*)dTet + c0, (int32_t*)dVis + c0, dTri ? (int32_t*)dTri + c0 : nullptr,
+                               dT ? (double*)dT + c0 : nullptr, dBack ? (int32_t*)dBack + c0 : nullptr, s))
+        return e;
+      continue;
+    }
+    if (int e = tb_cast_rays(m, k, sl.o, sl.d, sl.st, sl.status, sl.cf, sl.tet, sl.vis, triangle ? sl.tri : nullptr,
+                             t ? sl.t : nullptr, tet_back ? sl.back : nullptr, s))
+      return e;
+    TB_CUDA(cudaMemcpyAsync(status + c0, sl.status, uk, cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaMemcpyAsync(cf + c0, sl.cf, uk * 4, cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaMemcpyAsync(tet + c0, sl.tet, uk * 4, cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaMemcpyAsync(visited + c0, sl.vis, uk * 4, cudaMemcpyDeviceToHost, s));
+    if (triangle) TB_CUDA(cudaMemcpyAsync(triangle + c0, sl.tri, uk * 4, cudaMemcpyDeviceToHost, s));
+    if (t) TB_CUDA(cudaMemcpyAsync(t + c0, sl.t, uk * 8, cudaMemcpyDeviceToHost, s));
+    if (tet_back) TB_CUDA(cudaMemcpyAsync(tet_back + c0, sl.back, uk * 4, cudaMemcpyDeviceToHost, s));
+  }
+  for (int i = 0; i < PipeCtx::kStreams; ++i) TB_CUDA(cudaStreamSynchronize(ctx->slot[i].s));
   return TB_OK;
 }
 

@@ -28,7 +28,7 @@ constexpr uint8_t kMiss = 0, kHit = 1, kError = 2;  // _kernels.pyx:17-19
 //   tet32: rec4[2t], rec4[2t+1] = {v0, v1, v2, vx}, {n0..n3}  (32 B, one sector)
 //   tet80: rec4[5t .. 5t+4]   = {v0..v3}, {n0..n3}, 12 floats (80 B, inline xyz)
 struct MeshView {
-  const float4* __restrict__ pts;     // (p,) x,y,z,0 -- padded for one 16 B load
+  const float4* __restrict__ pts;     // 6 x (p,): copy k = (q[mx],q[ot],q[mn],0); copy 0 = x,y,z,0
   const uint4* __restrict__ rec4;     // layout records (see above)
   const uint32_t* __restrict__ vx;    // tet20 only
   const int4* __restrict__ sv;        // side_verts (t,) ascending
@@ -43,11 +43,25 @@ struct MeshView {
 __device__ __forceinline__ float pick3(float x, float y, float z, int a) {
   return a == 0 ? x : (a == 1 ? y : z);
 }
+// Component k (0..3) of a uint4 as a 2-level select on the bits of k
+// (keeps ptxas from emitting a branch island per pick).
 __device__ __forceinline__ uint32_t pick4u(uint4 v, int k) {
-  return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+  const uint32_t lo = (k & 1) ? v.y : v.x;
+  const uint32_t hi = (k & 1) ? v.w : v.z;
+  return (k & 2) ? hi : lo;
 }
 
 __device__ __forceinline__ float4 ldg_f4(const float4* p) { return __ldg(p); }
+// 16 B read-only load of base[i] with the address formed by one mad.wide
+// (base is a per-ray pointer; keeps the 64-bit index math to one IMAD.WIDE).
+__device__ __forceinline__ float4 ldg_f4_at(const float4* base, uint32_t i) {
+  float4 r;
+  asm("{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %4, 16, %5;\n\t"
+      "ld.global.nc.v4.f32 {%0, %1, %2, %3}, [a];\n\t}"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "r"(i), "l"(base));
+  return r;
+}
 __device__ __forceinline__ uint4 ldg_u4(const uint4* p) { return __ldg(p); }
 
 // ----------------------------------------------------------------------------
@@ -156,12 +170,13 @@ __device__ __forceinline__ int init_ray(const MeshView& m, float o0, float o1, f
   for (int j = 0; j < 4; ++j) {
     // SLOT_A/B/C, _kernels.pyx:105-111: the face opposite slot j.
     const int ia = (j == 0) ? 1 : 0;
-    int ib = (j <= 1) ? 2 : 1;
-    int ic = (j == 3) ? 2 : 3;
-    if (((j & 1) == 0) != rho_pos) { const int tmp = ib; ib = ic; ic = tmp; }
+    const int ib = (j <= 1) ? 2 : 1;
+    const int ic = (j == 3) ? 2 : 3;
+    // outward winding swaps b <-> c; selects keep q2[] in registers
+    const bool sw = ((j & 1) == 0) != rho_pos;
     const float ax = q2[2 * ia], ay = q2[2 * ia + 1];
-    const float bx = q2[2 * ib], by = q2[2 * ib + 1];
-    const float cx = q2[2 * ic], cy = q2[2 * ic + 1];
+    const float bx = sw ? q2[2 * ic] : q2[2 * ib], by = sw ? q2[2 * ic + 1] : q2[2 * ib + 1];
+    const float cx = sw ? q2[2 * ib] : q2[2 * ic], cy = sw ? q2[2 * ib + 1] : q2[2 * ic + 1];
     const float dd0 = __fsub_rn(__fmul_rn(ax, by), __fmul_rn(ay, bx));
     const float dd1 = __fsub_rn(__fmul_rn(bx, cy), __fmul_rn(by, cx));
     const float dd2 = __fsub_rn(__fmul_rn(cx, ay), __fmul_rn(cy, ax));
@@ -294,24 +309,65 @@ __device__ __forceinline__ float4 fetch_vertex<80>(const MeshView&, const Record
   return r.vertex(r.slot_of(i3));
 }
 
+// ----------------------------------------------------------------------------
+// Axis-permuted point copies.  The projection reads q[mx], q[ot], q[mn] in
+// that order (_kernels.pyx:89-91); selecting them per step costs six SELs
+// plus predicate traffic in an issue-bound loop.  The device keeps six
+// copies of the points, copy k holding (q[mx], q[ot], q[mn], 0) for the
+// k-th (mx, ot) pair, so one 16 B load delivers the components already in
+// projection order.  Copy 0 is (x, y, z): MeshView.pts[i] stays the plain
+// point for every other user.
+__device__ __forceinline__ int perm_index(int mx, int ot) { return mx * 2 + (ot > mx ? ot - 1 : ot); }
+
+__device__ __forceinline__ const float4* ray_points(const MeshView& m, const Basis& b) {
+  return m.pts + (size_t)perm_index(b.mx, b.ot) * (size_t)m.n_points;
+}
+
+// project() on a point already in (mx, ot, mn) order: same operations, same order.
+__device__ __forceinline__ void project_perm(const Basis& b, const float4& q, float& x, float& y) {
+  x = __fsub_rn(__fadd_rn(__fmul_rn(b.umax, q.x), q.y), b.pox);
+  y = __fsub_rn(__fadd_rn(__fadd_rn(__fmul_rn(b.vmax, q.x), __fmul_rn(b.voth, q.y)), __fmul_rn(b.sgn, q.z)),
+                b.poy);
+}
+
 // One traversal step into tet `nxt`, _kernels.pyx:238-259.  Updates the
-// window (idx, p) and returns the exit reference of `nxt`.
+// window (idx, p) and returns the exit reference of `nxt`.  `P` is the ray's
+// axis-permuted point copy (ignored for TetMesh-80, whose points are inline).
+// Written branch-free: Algorithm 1's outcome as two predicates and the
+// window update as per-register selects.
 template <int L>
-__device__ __forceinline__ uint32_t advance(const MeshView& m, const Basis& b, uint32_t (&idx)[3],
-                                            float (&p)[6], uint32_t nxt, uint32_t prev) {
+__device__ __forceinline__ uint32_t advance(const MeshView& m, const float4* __restrict__ P, const Basis& b,
+                                            uint32_t (&idx)[3], float (&p)[6], uint32_t nxt, uint32_t prev) {
   Record<L> rec;
   rec.load(m, nxt);
   uint32_t i3 = idx[0] ^ idx[1] ^ idx[2] ^ rec.vxw();
-  if (L != 80 && i3 >= (uint32_t)m.n_points) i3 = 0;  // corrupt record: stay in bounds
-  const float4 q = fetch_vertex<L>(m, rec, i3);
   float qx, qy;
-  project(b, q.x, q.y, q.z, qx, qy);
-  const int f = exit_face(qx, qy, p);
-  const uint32_t idxf = (f == 0) ? idx[0] : ((f == 1) ? idx[1] : idx[2]);
+  if constexpr (L == 80) {
+    const float4 q = rec.vertex(rec.slot_of(i3));
+    project(b, q.x, q.y, q.z, qx, qy);
+  } else {
+    i3 = min(i3, (uint32_t)m.n_points - 1u);  // corrupt record: stay in bounds
+    const float4 q = ldg_f4_at(P, i3);
+    project_perm(b, q, qx, qy);
+  }
+  // Algorithm 1 (_kernels.pyx:94-102): f = c0 ? (c2 ? 1 : 0) : (c1 ? 2 : 0)
+  const bool c0 = __fmul_rn(qx, p[1]) < __fmul_rn(qy, p[0]);
+  const bool c2 = __fmul_rn(qx, p[5]) >= __fmul_rn(qy, p[4]);
+  const bool c1 = __fmul_rn(qx, p[3]) < __fmul_rn(qy, p[2]);
+  const bool f1 = c0 && c2;
+  const bool f2 = !c0 && c1;
+  const bool f0 = !(f1 || f2);
+  const uint32_t idxf = f1 ? idx[1] : (f2 ? idx[2] : idx[0]);
   const uint32_t nref = rec.next_ref(idx, i3, idxf, prev);
-  if (f == 0) { idx[0] = i3; p[0] = qx; p[1] = qy; }
-  else if (f == 1) { idx[1] = i3; p[2] = qx; p[3] = qy; }
-  else { idx[2] = i3; p[4] = qx; p[5] = qy; }
+  idx[0] = f0 ? i3 : idx[0];
+  idx[1] = f1 ? i3 : idx[1];
+  idx[2] = f2 ? i3 : idx[2];
+  p[0] = f0 ? qx : p[0];
+  p[1] = f0 ? qy : p[1];
+  p[2] = f1 ? qx : p[2];
+  p[3] = f1 ? qy : p[3];
+  p[4] = f2 ? qx : p[4];
+  p[5] = f2 ? qy : p[5];
   return nref;
 }
 
