@@ -1,0 +1,80 @@
+"""The C-ABI boundary without a GPU: the library loads, exports every entry
+point include/tetb200.h declares, and fails loudly (error code + message,
+no crash) instead of falling back to the CPU."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from conftest import HAS_GPU, ROOT
+
+
+def _declared():
+    text = (ROOT / "include" / "tetb200.h").read_text()
+    return sorted(set(re.findall(r"\b(tb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2103_02309_b200 import _lib
+
+    names = _declared()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(_lib.lib, name), name
+    assert set(names) == set(_lib.EXPORTED)
+
+
+def test_abi_version_and_errors():
+    from paper_2103_02309_b200._lib import lib
+
+    assert lib.tb_abi_version() == 1
+    assert lib.tb_mesh_destroy(None) == 0
+    rc = lib.tb_cast_rays(None, 1, None, None, None, None, None, None, None, None, None, None, None)
+    assert rc == -1
+    assert b"NULL" in lib.tb_last_error()
+
+
+@pytest.mark.skipif(HAS_GPU, reason="checks the no-GPU failure path")
+def test_mesh_create_fails_loudly_without_gpu(meshes):
+    from paper_2103_02309_b200._lib import TetB200Error
+    from paper_2103_02309_b200.device import DeviceMesh
+
+    with pytest.raises(TetB200Error):
+        DeviceMesh(meshes["box4"], device=0)
+
+
+@pytest.mark.skipif(HAS_GPU, reason="checks the no-GPU failure path")
+def test_kernel_module_has_no_cpu_fallback(meshes):
+    from paper_2103_02309_b200 import kernels
+    from paper_2103_02309_b200._lib import TetB200Error
+
+    m = meshes["box4"]
+    import numpy as np
+
+    with pytest.raises(TetB200Error):
+        kernels.cast_rays(m, np.zeros((1, 3), np.float32), np.ones((1, 3), np.float32), np.zeros(1, np.int32))
+
+
+def test_header_cites_reference_interfaces():
+    text = (ROOT / "include" / "tetb200.h").read_text()
+    for cite in ("_kernels.pyx:271-370", "_kernels.pyx:416-492", "_kernels.pyx:527-614", "batch.py:57-71",
+                 "traversal.py:484-511"):
+        assert cite in text
+
+
+def test_oracle_library_loads():
+    from oracle import pyoracle
+
+    L = pyoracle.lib()
+    for name in ("to_cast_rays", "to_sctp_cast_rays", "to_locate_points", "to_shadow_rays", "to_mt_t"):
+        assert hasattr(L, name)
+
+
+def test_no_oracle_import_in_product():
+    for p in (ROOT / "paper_2103_02309_b200").rglob("*.py"):
+        src = p.read_text()
+        assert "import oracle" not in src and "from oracle" not in src, p
