@@ -157,7 +157,7 @@ def camera_rays(position, look_at, up, fov, width, height, xs=None, ys=None):
     sy = (1.0 - (ys + 0.5) / height * 2.0) * half_h
     d = fwd[None] + sx[:, None] * right[None] + sy[:, None] * up2[None]
     o = np.broadcast_to(pos, d.shape)
-    return o.astype(np.float32), d.astype(np.float32)
+    return np.ascontiguousarray(o, dtype=np.float32), np.ascontiguousarray(d, dtype=np.float32)
 
 
 def diffuse_secondaries(origins, dirs, t, triangle, tet_front, tri_coords, seed: int = 4):
