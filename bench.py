@@ -47,6 +47,9 @@ CONFIGS = {
             desc="cfg3: blob GRID=55 (1,109,444 tets), 3840x2160 primary rays, TetMesh-16 Hilbert-sorted"),
     4: dict(grid=55, width=4096, height=4096, layout="tet16", scheme="hilbert", secondaries=True,
             desc="cfg4: blob GRID=55, 16.7M diffuse secondaries from 4096x4096 primary hits, TetMesh-16"),
+    5: dict(kuhn=203, width=7680, height=4320, layout="tet16", scheme="none",
+            desc="cfg5: Kuhn box n=203 (50,192,562 tets) stretched 4x in z with thin strip occluders "
+                 "(long thin triangles), 7680x4320 primary rays, TetMesh-16"),
 }
 L2_FLUSH_BYTES = 256 << 20
 FALLBACK_HBM_GBS = 6650.0
@@ -72,21 +75,24 @@ def measured_peak():
 
 
 def build_scene(cfg):
-    from paper_2103_02309_b200.scenes import blob_scene
+    from paper_2103_02309_b200.scenes import blob_scene, kuhn_strip_scene
 
     t0 = time.perf_counter()
-    sc = blob_scene(cfg["grid"], layout=cfg["layout"], scheme=cfg["scheme"], check=False)
+    if "kuhn" in cfg:
+        sc = kuhn_strip_scene(cfg["kuhn"], layout=cfg["layout"], scheme=cfg["scheme"])
+    else:
+        sc = blob_scene(cfg["grid"], layout=cfg["layout"], scheme=cfg["scheme"], check=False)
     log(f"[bench] scene {sc.name}: {sc.mesh.n_tets} tets, {sc.mesh.n_points} points, "
         f"{sc.mesh.n_constrained} constrained faces, built in {time.perf_counter() - t0:.1f}s")
     return sc
 
 
 def frame_rays(cfg, frame: int):
-    from paper_2103_02309_b200.scenes import BLOB_CAMERA, camera_rays
+    from paper_2103_02309_b200.scenes import BLOB_CAMERA, camera_rays, kuhn_camera
 
-    pos = np.asarray(BLOB_CAMERA["position"], dtype=np.float64) + np.array([0.0, 0.02, 0.0]) * frame
-    o, d = camera_rays(tuple(pos), BLOB_CAMERA["look_at"], BLOB_CAMERA["up"], BLOB_CAMERA["fov"],
-                       cfg["width"], cfg["height"])
+    cam = kuhn_camera(cfg["kuhn"]) if "kuhn" in cfg else BLOB_CAMERA
+    pos = np.asarray(cam["position"], dtype=np.float64) + np.array([0.0, 0.02, 0.0]) * frame
+    o, d = camera_rays(tuple(pos), cam["look_at"], cam["up"], cam["fov"], cfg["width"], cfg["height"])
     return o, d, pos
 
 
@@ -268,6 +274,18 @@ def run_ours(args, cfg):
         q = torch.tensor(pos[None], dtype=torch.float64, device=dev)
         cam, _ = locate(dm, q, torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))
         st[sel] = int(cam.item())
+    if cfg.get("secondaries"):
+        # config 4: the timed rays are the diffuse secondaries spawned from this
+        # shard's primary hits (traced here, untimed), in shard order
+        from paper_2103_02309_b200.scenes import diffuse_secondaries
+
+        prim = trace(dm, *(torch.from_numpy(a).to(dev) for a in (o, d, st)))
+        torch.cuda.synchronize()
+        hit = prim.triangle.cpu().numpy() >= 0
+        o, d, st = diffuse_secondaries(o, d, prim.t.cpu().numpy(), prim.triangle.cpu().numpy(),
+                                       prim.tet.cpu().numpy(), mesh.triangle_coords(), seed=4 + rank)
+        idx = idx[hit]
+        del prim
     n = len(st)
     go, gd, gs = (torch.from_numpy(a).to(dev) for a in (o, d, st))
     res = empty_result(n, dev)
@@ -287,8 +305,9 @@ def run_ours(args, cfg):
     # parity at full size: the reference's own digest of this frame (rank 0, N=1)
     parity = None
     dig_path = os.path.join(ROOT, "tests", "golden", "golden_digests.json")
-    key = f"blob{cfg['grid']}/{cfg['scheme']}/cast"
-    if world == 1 and os.path.exists(dig_path) and cfg.get("layout") in ("tet20", "tet16", "tet32"):
+    key = f"blob{cfg.get('grid')}/{cfg['scheme']}/cast"
+    if world == 1 and os.path.exists(dig_path) and cfg.get("layout") in ("tet20", "tet16", "tet32") \
+            and not cfg.get("secondaries") and "grid" in cfg:
         digs = json.load(open(dig_path))
         if key in digs and (W, H) == {12: (256, 256), 55: (1920, 1080)}.get(cfg["grid"]):
             inv = np.empty_like(idx)
@@ -302,6 +321,19 @@ def run_ours(args, cfg):
             parity = {"vs": "reference digest " + key,
                       "traversal_bit_exact": got == digs[key],
                       "epilogue_bit_exact": ep == digs[key.replace("/cast", "/epilogue")]}
+    if parity is None and rank == 0 and not args.no_parity:
+        # no reference digest for this workload: check a strided sample of
+        # rays against the CPU oracle (the checker, never the measured path)
+        from oracle import pyoracle
+
+        stride = max(1, n // args.parity_sample)
+        sl = slice(0, n, stride)
+        exp = pyoracle.cast_rays_full(mesh, o[sl], d[sl], st[sl])
+        got = [x.cpu().numpy()[sl] for x in (res.status, res.cf, res.tet, res.visited, res.triangle, res.t,
+                                              res.tet_back)]
+        mism = int(sum(np.count_nonzero(a != b) for a, b in zip(got, exp)))
+        parity = {"vs": f"C oracle (oracle/tetoracle.c) on every {stride}th ray", "rays_checked": int(len(exp[0])),
+                  "mismatched_values": mism, "bit_exact": mism == 0}
     visited = res.visited.cpu().numpy()
 
     # timed region: K steps between barrier + sync; per-step kernel events.
@@ -458,6 +490,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2_073_600)
     ap.add_argument("--ramp-s", type=float, default=0.5, help="untimed load before the timed region (clock ramp)")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--parity-sample", type=int, default=262_144, help="rays checked against the oracle")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -466,8 +500,6 @@ def main():
         cfg["layout"] = args.layout
     if args.scheme:
         cfg["scheme"] = args.scheme
-    if cfg.get("secondaries"):
-        raise SystemExit("config 4 is run by bench_secondaries (see DESIGN.md); use --config 2/3")
     if args.impl == "reference":
         run_reference_arm(args, cfg)
     else:

@@ -192,6 +192,48 @@ __device__ __forceinline__ void write_result(const MeshView& m, int64_t r, uint8
 }
 
 // ----------------------------------------------------------------------------
+// Cycle guard without the O(n_tets) walk.  The reference stops a ray once it
+// has visited more than n_tets tets (_kernels.pyx:365-368); rays that tie
+// exactly on lattice-aligned meshes loop forever and pay n_tets steps (50 M
+// on config 5).  The step is a pure function of (ref, idx[3], cur) -- the
+// projected window p[] is a function of idx for a fixed ray -- so once a
+// state repeats the walk is periodic.  Brent's algorithm finds the period
+// lam; the walk then jumps a whole number of periods (state unchanged) and
+// finishes the last < lam steps, giving exactly the reference's terminating
+// tet and visited = n_tets + 1.  Only walks longer than kCycleCheckAfter
+// steps enter here, so the hot loop is untouched.  Returns true on guard.
+constexpr uint32_t kCycleCheckAfter = 1u << 14;
+
+template <int L>
+__device__ __noinline__ bool long_walk(const MeshView& m, const float4* __restrict__ P, const Basis& b,
+                                       uint32_t (&idx)[3], float (&p)[6], uint32_t& ref, uint32_t& cur, int& vis) {
+  const uint32_t n_tets = (uint32_t)m.n_tets;
+  uint32_t s_ref = ref, s_i0 = idx[0], s_i1 = idx[1], s_i2 = idx[2], s_cur = cur;
+  uint32_t power = 1, lam = 0;
+  bool jumped = false;
+  while (ref < n_tets) {
+    const uint32_t nxt = ref;
+    ref = advance<L>(m, P, b, idx, p, nxt, cur);
+    cur = nxt;
+    if ((uint32_t)++vis > n_tets) return true;
+    ++lam;
+    if (!jumped && ref == s_ref && idx[0] == s_i0 && idx[1] == s_i1 && idx[2] == s_i2 && cur == s_cur) {
+      const uint64_t remaining = (uint64_t)n_tets + 1 - (uint64_t)vis;  // steps until the guard
+      vis += (int)((remaining / lam) * lam);
+      jumped = true;
+      if ((uint32_t)vis > n_tets) return true;
+      continue;
+    }
+    if (lam == power) {  // Brent: move the tortoise, double the window
+      s_ref = ref; s_i0 = idx[0]; s_i1 = idx[1]; s_i2 = idx[2]; s_cur = cur;
+      power <<= 1;
+      lam = 0;
+    }
+  }
+  return false;
+}
+
+// ----------------------------------------------------------------------------
 // Primary traversal kernel: one lane per ray, _kernels.pyx:343-369.
 template <int L>
 __global__ void __launch_bounds__(kBlock) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
@@ -220,11 +262,16 @@ __global__ void __launch_bounds__(kBlock) cast_kernel(MeshView m, int64_t n, con
   // (0x7FFFFFFF) and constrained refs (bit 31) are >= n_tets, so one
   // unsigned compare per step decides "keep walking" (corrupt refs also land
   // outside and are classified below).
+  const uint32_t fast_limit = n_tets < kCycleCheckAfter ? n_tets : kCycleCheckAfter;
   while (ref < n_tets) {
     const uint32_t nxt = ref;
     ref = advance<L>(m, P, b, idx, p, nxt, cur);
     cur = nxt;
-    if ((uint32_t)++vis > n_tets) { st = kError; break; }  // cycle guard, _kernels.pyx:365-368
+    if ((uint32_t)++vis > fast_limit) {
+      // Long walk: finish it in the cycle-detecting slow path (exact).
+      if ((uint32_t)vis > n_tets || long_walk<L>(m, P, b, idx, p, ref, cur, vis)) st = kError;
+      break;
+    }
   }
   if (st != kError) st = (ref == kBoundary) ? kMiss : ((ref & kConstrained) ? kHit : kError);
   write_result(m, r, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,

@@ -199,6 +199,177 @@ def build_box_fixture(n: int, occluders=(), walls: str = "constrained"):
 
 
 # ---------------------------------------------------------------------------
+# Analytic Kuhn box (same mesh as build_box_fixture, no face sort) -- the
+# big-scene builder for BASELINE config 5 (n = 203: 50,192,562 tets), which
+# the reference's dict-based builder cannot construct (~60 us/tet,
+# SURVEY 3.3).  Adjacency of the Kuhn simplex (c, p) with path vertices
+# w0 = c, w1 = c + e_p0, w2 = w1 + e_p1, w3 = c + 1:
+#   face opp. w0 -> cell c + e_p0, perm (p1, p2, p0), its new vertex is w'3
+#   face opp. w3 -> cell c - e_p2, perm (p2, p0, p1), its new vertex is w'0
+#   face opp. w1 -> same cell, perm (p1, p0, p2), new vertex w'1
+#   face opp. w2 -> same cell, perm (p0, p2, p1), new vertex w'2
+# Faces opposite w0 / w3 lie on the cell-face planes axis p0 at c[p0] + 1 /
+# axis p2 at c[p2]; they are the only candidates for walls and occluders.
+
+_PERM_INDEX = {p: i for i, p in enumerate(_PERMS)}
+_PARITY = np.array([_perm_parity(p) for p in _PERMS])
+_SLOT_OF_W = np.array([[0, 1, 2, 3] if _perm_parity(p) > 0 else [0, 2, 1, 3] for p in _PERMS])  # (6, 4)
+
+
+def build_kuhn_box(n: int, occluders=(), walls: str = "constrained", scale=(1.0, 1.0, 1.0)):
+    """Analytic restatement of build_box_fixture (identical arrays for
+    scale 1, tested), optionally with axis-scaled geometry ("long thin"
+    tets and scene triangles for scale far from 1)."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    if walls not in ("constrained", "open"):
+        raise ValueError("walls must be 'constrained' or 'open'")
+    occs = _check_occluders(n, occluders)
+    m = n + 1
+    n_cells = n ** 3
+    n_tets = 6 * n_cells
+    ax = np.arange(m, dtype=np.float64)
+    ii, jj, kk = np.meshgrid(ax, ax, ax, indexing="ij")
+    points = np.stack([ii.ravel() * scale[0], jj.ravel() * scale[1], kk.ravel() * scale[2]], axis=1)
+    del ii, jj, kk
+    tets = kuhn_tets(n)
+    neighbors = np.full((n_tets, 4), BOUNDARY_REF, dtype=np.uint32)
+    cell = np.arange(n_cells, dtype=np.int64)
+    cc = np.stack([cell // (n * n), (cell // n) % n, cell % n], axis=1)  # (cells, 3)
+    stride_c = np.array([n * n, n, 1], dtype=np.int64)
+    # interior cell-face records for occluder / association handling
+    cf_parts = []  # (tet, slot, other_tet, other_slot, axis, plane, u, v, middle_is_first)
+    for k, p in enumerate(_PERMS):
+        t = cell * 6 + k
+        slot = _SLOT_OF_W[k]
+        # faces opposite w1 / w2: same cell, other permutations
+        for q, pn, qn in ((1, (p[1], p[0], p[2]), 1), (2, (p[0], p[2], p[1]), 2)):
+            kn = _PERM_INDEX[pn]
+            neighbors[t, slot[q]] = (cell * 6 + kn).astype(np.uint32)
+        # face opposite w0: cell + e_p0 (perm (p1, p2, p0), new vertex w'3)
+        inside = cc[:, p[0]] < n - 1
+        kn = _PERM_INDEX[(p[1], p[2], p[0])]
+        tn = (cell + stride_c[p[0]]) * 6 + kn
+        neighbors[t[inside], slot[0]] = tn[inside].astype(np.uint32)
+        cf_parts.append(("w0", k, p, t, slot[0], inside, tn, _SLOT_OF_W[kn][3]))
+        # face opposite w3: cell - e_p2 (perm (p2, p0, p1), new vertex w'0)
+        inside3 = cc[:, p[2]] > 0
+        kn3 = _PERM_INDEX[(p[2], p[0], p[1])]
+        tn3 = (cell - stride_c[p[2]]) * 6 + kn3
+        neighbors[t[inside3], slot[3]] = tn3[inside3].astype(np.uint32)
+        cf_parts.append(("w3", k, p, t, slot[3], inside3, tn3, _SLOT_OF_W[kn3][0]))
+
+    # constrained faces: collect (tet, slot, partner tet/slot or -1, plane info)
+    rec_t, rec_s, rec_t2, rec_s2, rec_axis, rec_plane, rec_u, rec_v, rec_mid = ([] for _ in range(9))
+    for kind, k, p, t, sl, inside, tn, sln in cf_parts:
+        if kind == "w0":
+            axis, plane = p[0], cc[:, p[0]] + 1
+            mid_axis = p[1]  # in-plane step of the middle vertex w2 - w1
+        else:
+            axis, plane = p[2], cc[:, p[2]]
+            mid_axis = p[0]  # w1 - w0
+        a1, a2 = _FREE_AXES[axis]
+        u, v = cc[:, a1], cc[:, a2]
+        sel = np.zeros(n_cells, dtype=bool)
+        # hull faces (walls)
+        if walls == "constrained":
+            sel |= ~inside
+        # occluder faces (interior); each is reached from both sides, keep the
+        # w0 side (lower cell) once and attach the partner
+        occ_hit = np.zeros(n_cells, dtype=bool)
+        if occs and kind == "w0":
+            for oa, ok_, u0, v0, u1, v1 in occs:
+                if oa != axis:
+                    continue
+                occ_hit |= inside & (plane == ok_) & (u >= u0) & (u + 1 <= u1) & (v >= v0) & (v + 1 <= v1)
+        if kind == "w3":
+            sel &= ~inside  # interior w3 faces are the partners of w0 faces
+        sel |= occ_hit
+        idx = np.nonzero(sel)[0]
+        if not idx.size:
+            continue
+        rec_t.append(t[idx])
+        rec_s.append(np.full(idx.size, sl))
+        two = inside[idx]
+        rec_t2.append(np.where(two, tn[idx], -1))
+        rec_s2.append(np.where(two, sln, -1))
+        rec_axis.append(np.full(idx.size, axis))
+        rec_plane.append(plane[idx])
+        rec_u.append(u[idx])
+        rec_v.append(v[idx])
+        rec_mid.append(np.full(idx.size, mid_axis == a1))  # middle vertex is p10 (else p01)
+    if rec_t:
+        ft = np.concatenate(rec_t)
+        fs = np.concatenate(rec_s)
+        ft2 = np.concatenate(rec_t2)
+        fs2 = np.concatenate(rec_s2)
+        faxis = np.concatenate(rec_axis)
+        fplane = np.concatenate(rec_plane)
+        fu = np.concatenate(rec_u)
+        fv = np.concatenate(rec_v)
+        fmid = np.concatenate(rec_mid)
+    else:
+        ft = fs = ft2 = fs2 = faxis = fplane = fu = fv = np.zeros(0, np.int64)
+        fmid = np.zeros(0, bool)
+    # face keys: sorted vertex triples (reference order: sorted(inc.items()))
+    tri_v = np.sort(tets[ft][:, _OTHER_SLOTS][np.arange(len(ft)), fs], axis=1).astype(np.int64)
+    order = np.lexsort((tri_v[:, 2], tri_v[:, 1], tri_v[:, 0]))
+    ft, fs, ft2, fs2, faxis, fplane, fu, fv, fmid, tri_v = (a[order] for a in
+                                                             (ft, fs, ft2, fs2, faxis, fplane, fu, fv, fmid, tri_v))
+    # front = lower tet id (first in tet-major incidence order)
+    swap = (ft2 >= 0) & (ft2 < ft)
+    front = np.where(swap, ft2, ft)
+    fslot = np.where(swap, fs2, fs)
+    back = np.where(swap, ft, ft2)
+    bslot = np.where(swap, fs, fs2)
+    cfn = np.arange(len(front), dtype=np.int64)
+    neighbors[front, fslot] = (CONSTRAINED_BIT | cfn).astype(np.uint32)
+    h2 = back >= 0
+    neighbors[back[h2], bslot[h2]] = (CONSTRAINED_BIT | cfn[h2]).astype(np.uint32)
+
+    soup = _box_soup(n, occs, walls)
+    if scale != (1.0, 1.0, 1.0):
+        soup = SceneTriangleSoup(vertices=soup.vertices * np.asarray(scale, dtype=np.float64),
+                                 triangles=soup.triangles, material_ids=soup.material_ids)
+    # analytic association: walls (2 triangles each, split along u = v) first,
+    # then per-cell occluder squares (2 triangles each), reference order
+    tri_id = np.full(len(front), -1, dtype=np.int64)
+    wall_base = 0
+    n_wall_tris = 12 if walls == "constrained" else 0
+    hull = back < 0
+    if walls == "constrained":
+        wall = faxis * 2 + (fplane == n)
+        upper = np.where(fmid, fv >= fu + 1, fv >= fu)  # triangle (p00, p11, p01) side
+        tri_id[hull] = (wall_base + 2 * wall + upper)[hull]
+    if occs:
+        base = n_wall_tris
+        claimed = np.zeros(len(front), dtype=np.int64)
+        for oa, ok_, u0, v0, u1, v1 in occs:
+            on = (~hull) & (faxis == oa) & (fplane == ok_) & (fu >= u0) & (fu + 1 <= u1) & (fv >= v0) & (fv + 1 <= v1)
+            cell_idx = (fu - u0) * (v1 - v0) + (fv - v0)
+            tri_id[on] = base + 2 * cell_idx[on] + (~fmid[on]).astype(np.int64)
+            claimed += on
+            base += 2 * (u1 - u0) * (v1 - v0)
+        if np.any(claimed > 1):
+            f = int(np.nonzero(claimed > 1)[0][0])
+            raise AssociationError(f"face {points[tri_v[f]].tolist()} matched {int(claimed[f])} scene triangles")
+    if np.any(tri_id < 0):
+        raise AssociationError("constrained face without a scene triangle")
+    raw = RawTetMesh(
+        points=points,
+        tets=tets,
+        neighbors=neighbors,
+        cf_triangle=tri_id.astype(np.int32),
+        cf_tets=np.stack([front, np.where(back >= 0, back, NO_TET)], axis=1).astype(np.int32),
+        cf_verts=tri_v.astype(np.int32),
+    )
+    return raw, soup
+
+
+_OTHER_SLOTS = np.array([[1, 2, 3], [0, 2, 3], [0, 1, 3], [0, 1, 2]])
+
+
+# ---------------------------------------------------------------------------
 # Face -> scene triangle association (ingestion.py:470-538), vectorised.
 
 

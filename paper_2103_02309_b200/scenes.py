@@ -133,6 +133,41 @@ def blob_scene(grid: int = 8, seed: int | None = None, layout: str = "tet20", sc
 
 
 # ---------------------------------------------------------------------------
+# Config 5: large Kuhn box with long thin triangles.  The reference's builder
+# cannot produce 50 M tets; build_kuhn_box is the
+# analytic restatement of its box fixture (identical arrays, tested), here
+# stretched along z so tets, wall triangles and the strip occluders are long
+# and thin, with strip occluders (1 x 4-cell-high bands across y) on x planes.
+
+KUHN5_N = 203
+KUHN5_SCALE = (1.0, 1.0, 4.0)
+
+
+def kuhn_strips(n: int):
+    """Thin strip occluders on x planes: y in [0.1n, 0.9n), 4 cells of z."""
+    ks = sorted({max(1, min(n - 1, int(round(f * n)))) for f in (0.2, 0.4, 0.6, 0.8, 0.98)})
+    y0, y1 = int(0.1 * n), max(int(0.1 * n) + 1, int(0.9 * n))
+    z0 = int(0.47 * n)
+    return [(0, k, (y0, z0), (y1, min(n, z0 + 4))) for k in ks]
+
+
+def kuhn_camera(n: int, scale=KUHN5_SCALE):
+    """Off-lattice camera looking down +x (the Kuhn-box camera of SURVEY
+    8(d), nudged off the lattice so no ray ties exactly on a diagonal)."""
+    pos = (0.11 * n + 0.0137, 0.53 * n + 0.0173, (0.52 * n + 0.0111) * scale[2])
+    look = (0.97 * n, 0.46 * n, 0.48 * n * scale[2])
+    return dict(position=pos, look_at=look, up=(0.0, 1.0, 0.0), fov=68.0)
+
+
+def kuhn_strip_scene(n: int = KUHN5_N, layout: str = "tet16", scheme: str = "none", scale=KUHN5_SCALE) -> Scene:
+    from .ingestion import build_kuhn_box
+
+    raw, soup = build_kuhn_box(n, kuhn_strips(n), walls="constrained", scale=tuple(float(s) for s in scale))
+    mesh = reorder(encode(raw, layout, soup, check=False), scheme)
+    return Scene(mesh=mesh, raw=raw, soup=soup, seed=0, name=f"kuhn{n}-strips")
+
+
+# ---------------------------------------------------------------------------
 # Rays
 
 

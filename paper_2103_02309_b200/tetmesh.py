@@ -191,6 +191,24 @@ def soup_from_faces(points: np.ndarray, face_verts: np.ndarray) -> SceneTriangle
     )
 
 
+def row_argsort4(a: np.ndarray) -> np.ndarray:
+    """np.argsort(a, axis=1, kind="stable") for (n, 4) integer rows, as a
+    16-comparison rank network (argsort along a length-4 axis is ~20x slower
+    on 50 M rows)."""
+    a = np.asarray(a)
+    n = len(a)
+    rank = np.zeros((n, 4), dtype=np.int8)
+    for j in range(4):
+        for k in range(4):
+            if k == j:
+                continue
+            # stable: equal keys keep their original order
+            rank[:, j] += (a[:, k] < a[:, j]) if k > j else (a[:, k] <= a[:, j])
+    order = np.empty((n, 4), dtype=np.int64)
+    np.put_along_axis(order, rank.astype(np.int64), np.broadcast_to(np.arange(4), (n, 4)), axis=1)
+    return order
+
+
 def signed_volumes(points: np.ndarray, tets: np.ndarray) -> np.ndarray:
     """6x signed volume per tet, float64, in the reference's einsum/cross order."""
     p = np.asarray(points, dtype=np.float64)[np.asarray(tets)]
@@ -373,7 +391,7 @@ def encode(raw: RawTetMesh, layout: str, soup: SceneTriangleSoup | None = None, 
         problems = validate_raw(raw)
         if problems:
             raise MeshError("; ".join(problems[:5]))
-    order = np.argsort(raw.tets, axis=1, kind="stable")
+    order = row_argsort4(raw.tets)
     side_verts = np.take_along_axis(raw.tets, order, axis=1).astype(np.int32)
     side_neighbors = np.take_along_axis(raw.neighbors, order, axis=1).astype(np.uint32)
     cf_verts = np.asarray(raw.cf_verts, dtype=np.int32).reshape(-1, 3)
@@ -468,7 +486,7 @@ def reorder(mesh: CompactMesh, scheme: str, *, order: int = 10, seed: int = 0) -
 
     verts = point_old2new[mesh.side_verts[tet_perm]]
     nbrs = _remap_refs(mesh.side_neighbors[tet_perm], tet_old2new)
-    row_order = np.argsort(verts, axis=1, kind="stable")
+    row_order = row_argsort4(verts)
     side_verts = np.take_along_axis(verts, row_order, axis=1).astype(np.int32)
     side_neighbors = np.take_along_axis(nbrs, row_order, axis=1)
     cf_tets = mesh.cf_tets.copy()

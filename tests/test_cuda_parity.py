@@ -153,6 +153,46 @@ def test_cycle_guard_lattice_camera(digests, K, O):
     assert out[3][err].tolist() == [m.n_tets + 1] * len(err)
 
 
+@pytest.mark.parametrize("layout", ("tet16", "tet20", "tet32"))
+def test_cycle_guard_fast_forward_exact(K, O, layout):
+    """n_tets (24,576) above the device's cycle-check threshold: the guard
+    rays go through the Brent fast-forward (long_walk) and must still give
+    the reference's status / terminating tet / visited = n_tets + 1."""
+    from paper_2103_02309_b200.ingestion import build_kuhn_box
+    from paper_2103_02309_b200.scenes import camera_rays
+    from paper_2103_02309_b200.tetmesh import encode
+
+    raw, soup = build_kuhn_box(16, [(0, 8, (4, 4), (12, 12))])
+    m = encode(raw, layout, soup)
+    o, d = camera_rays((8.0, 8.0, 0.5), (8.0, 8.0, 16.0), (0.0, 1.0, 0.0), 68.0, 512, 512)
+    cam, _ = O.locate_points(m, np.array([[8.0, 8.0, 0.5]]), np.array([0], np.int32))
+    st = np.full(len(o), cam[0], np.int32)
+    got = K.cast_rays_full(m, o, d, st)
+    exp = O.cast_rays_full(m, o, d, st)
+    for k, a, b in zip(NAMES7, got, exp):
+        assert np.array_equal(a, b), k
+    err = np.nonzero(got[0] == 2)[0]
+    assert len(err) == 3 and (got[3][err] == m.n_tets + 1).all()
+
+
+def test_config5_builder_small_scale_parity(K, O):
+    """The config-5 scene family (stretched Kuhn box + thin strip occluders)
+    at a small size: GPU == oracle on every ray of a camera frame."""
+    from paper_2103_02309_b200.scenes import camera_rays, kuhn_camera, kuhn_strip_scene
+
+    sc = kuhn_strip_scene(24, layout="tet16")
+    cam = kuhn_camera(24)
+    o, d = camera_rays(cam["position"], cam["look_at"], cam["up"], cam["fov"], 320, 240)
+    c, _ = K.locate_points(sc.mesh, np.array([cam["position"]]), np.array([sc.mesh.source_tet], np.int32))
+    assert c[0] >= 0
+    st = np.full(len(o), c[0], np.int32)
+    got = K.cast_rays_full(sc.mesh, o, d, st)
+    exp = O.cast_rays_full(sc.mesh, o, d, st)
+    for k, a, b in zip(NAMES7, got, exp):
+        assert np.array_equal(a, b), k
+    assert (got[0] == 1).all()
+
+
 @pytest.mark.parametrize("scheme", ("none", "hilbert"))
 def test_config1_blob12_camera(digests, K, scheme):
     """BASELINE config 1 (blob GRID=12, 256x256 primaries) equals the
