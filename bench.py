@@ -250,10 +250,17 @@ def run_ours(args, cfg):
     from paper_2103_02309_b200.trace import empty_result, locate, trace
 
     world, rank, local = dist_env()
+    # one rank per GPU; TETB200_DIST_BACKEND=gloo lets several ranks share one
+    # GPU to exercise the N>1 code path on a single device (test only)
+    backend = os.environ.get("TETB200_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     sc = build_scene(cfg)
     mesh = sc.mesh
     dm = device_mesh(mesh, device=local)
@@ -420,8 +427,10 @@ def run_ours(args, cfg):
             e_s = float(t.item())
         e2e = {"value": total_rays * args.steps / e_s / 1e6, "unit": "Mrays/s",
                "h2d_bytes_per_step": int(n * (12 + 12 + 4)), "d2h_bytes_per_step": int(n * (1 + 4 * 5 + 8)),
-               "ms_per_step": e_s / args.steps * 1e3, "gpu_launches_per_step": -(-n // (1 << 18)),
-               "path": "tb_cast_rays_host (C ABI, pinned host buffers, 3-stream chunked H2D/trace/D2H)"}
+               "ms_per_step": e_s / args.steps * 1e3,
+               "gpu_launches_per_step": 1 if os.environ.get("TETB200_E2E", "0") == "0" else -(-n // (1 << 18)),
+               "path": "tb_cast_rays_host (C ABI) on pinned host buffers: zero-copy trace over PCIe "
+                       "(TETB200_E2E=1: 3-stream chunked H2D/trace/D2H)"}
 
     if rank != 0:
         if world > 1:

@@ -90,6 +90,8 @@ def gather_hits(packed, total: int, root: int = 0, group=None):
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    if dist.get_backend(group) == "gloo":  # gloo collectives run on host tensors
+        packed = packed.cpu()
     dev = packed.device
     n = torch.tensor([packed.shape[0]], dtype=torch.int64, device=dev)
     sizes = [torch.zeros_like(n) for _ in range(world)]
