@@ -140,22 +140,32 @@ __global__ void build_tet80_kernel(const int4* __restrict__ sv, const uint4* __r
 __device__ __forceinline__ void load_xyz_warp(const float* __restrict__ a, int64_t r, int64_t n, float& x,
                                               float& y, float& z) {
   const int lane = threadIdx.x & 31;
-  const int64_t base = 3 * (r - lane);
+  const int64_t base = 3 * (r - lane);  // first float of the warp's window (16 B aligned: 96 floats per warp)
   const int64_t lim = 3 * n;
-  float v[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const int64_t e = base + 32 * k + lane;
-    v[k] = (e < lim) ? __ldg(a + e) : 0.0f;
+  // lanes 0..23 fetch one 16 B vector each (384 B per warp, one request per
+  // 128 B line); the ragged tail falls back to scalar loads
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t e0 = base + 4 * lane;
+  if (lane < 24) {
+    if (e0 + 3 < lim && ((reinterpret_cast<uintptr_t>(a) & 15u) == 0)) {
+      v = __ldg(reinterpret_cast<const float4*>(a + e0));
+    } else {
+      if (e0 < lim) v.x = __ldg(a + e0);
+      if (e0 + 1 < lim) v.y = __ldg(a + e0 + 1);
+      if (e0 + 2 < lim) v.z = __ldg(a + e0 + 2);
+      if (e0 + 3 < lim) v.w = __ldg(a + e0 + 3);
+    }
   }
   float out[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const int e = 3 * lane + c;  // element of the warp's 96-float window
-    const float s0 = __shfl_sync(0xffffffffu, v[0], e & 31);
-    const float s1 = __shfl_sync(0xffffffffu, v[1], e & 31);
-    const float s2 = __shfl_sync(0xffffffffu, v[2], e & 31);
-    out[c] = (e < 32) ? s0 : ((e < 64) ? s1 : s2);
+    const float s0 = __shfl_sync(0xffffffffu, v.x, e >> 2);
+    const float s1 = __shfl_sync(0xffffffffu, v.y, e >> 2);
+    const float s2 = __shfl_sync(0xffffffffu, v.z, e >> 2);
+    const float s3 = __shfl_sync(0xffffffffu, v.w, e >> 2);
+    const int k = e & 3;
+    out[c] = (k == 0) ? s0 : ((k == 1) ? s1 : ((k == 2) ? s2 : s3));
   }
   x = out[0];
   y = out[1];
@@ -205,7 +215,7 @@ __device__ __forceinline__ void write_result(const MeshView& m, int64_t r, uint8
 constexpr uint32_t kCycleCheckAfter = 1u << 14;
 
 template <int L>
-__device__ __noinline__ bool long_walk(const MeshView& m, const float4* __restrict__ P, const Basis& b,
+__device__ __forceinline__ bool long_walk(const MeshView& m, const float4* __restrict__ P, const Basis& b,
                                        uint32_t (&idx)[3], float (&p)[6], uint32_t& ref, uint32_t& cur, int& vis) {
   const uint32_t n_tets = (uint32_t)m.n_tets;
   uint32_t s_ref = ref, s_i0 = idx[0], s_i1 = idx[1], s_i2 = idx[2], s_cur = cur;
@@ -236,7 +246,10 @@ __device__ __noinline__ bool long_walk(const MeshView& m, const float4* __restri
 // ----------------------------------------------------------------------------
 // Primary traversal kernel: one lane per ray, _kernels.pyx:343-369.
 template <int L>
-__global__ void __launch_bounds__(kBlock) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
+#ifndef TB_CAST_MIN_BLOCKS
+#define TB_CAST_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(kBlock, TB_CAST_MIN_BLOCKS) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
                                                       const float* __restrict__ d,
                                                       const int32_t* __restrict__ start,
                                                       uint8_t* __restrict__ status, int32_t* __restrict__ cf,
@@ -276,6 +289,86 @@ __global__ void __launch_bounds__(kBlock) cast_kernel(MeshView m, int64_t n, con
   if (st != kError) st = (ref == kBoundary) ? kMiss : ((ref & kConstrained) ? kHit : kError);
   write_result(m, r, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
                tet_back);
+}
+
+// ----------------------------------------------------------------------------
+// Persistent variant with warp-level ray refill, for divergent (incoherent)
+// batches.  One lane per ray, but a lane whose ray terminates takes the next
+// ray of its warp's stream instead of idling until the warp's longest ray
+// ends (incoherent secondaries run at ~50 % SIMT efficiency otherwise, ncu
+// r01 cfg4).  Each warp owns the interleaved 32-ray chunks
+// c = warp, warp + n_warps, ... (static, balanced, no atomics); a refill
+// round hands consecutive stream positions to the idle lanes (ballot + popc)
+// whenever at most kRefillBelow lanes are still walking, then every lane
+// walks up to kStepsPerRound steps.  Results per ray are identical to
+// cast_kernel (same init, step, guard and epilogue code).
+constexpr int kRefillBelow = 20;
+constexpr int kStepsPerRound = 16;
+
+template <int L>
+__global__ void __launch_bounds__(kBlock) cast_persist_kernel(
+    MeshView m, int64_t n, const float* __restrict__ o, const float* __restrict__ d,
+    const int32_t* __restrict__ start, uint8_t* __restrict__ status, int32_t* __restrict__ cf,
+    int32_t* __restrict__ tet, int32_t* __restrict__ visited, int32_t* __restrict__ triangle,
+    double* __restrict__ t, int32_t* __restrict__ tet_back) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_chunks = (n + 31) >> 5;
+  const int64_t stream_len = (n_chunks > warp) ? ((n_chunks - warp + n_warps - 1) / n_warps) * 32 : 0;
+  const uint32_t n_tets = (uint32_t)m.n_tets;
+  const uint32_t fast_limit = n_tets < kCycleCheckAfter ? n_tets : kCycleCheckAfter;
+  int64_t pos = 0;  // warp-uniform position in this warp's ray stream
+  bool has = false;
+  int64_t r = 0;
+  float o0 = 0.f, o1 = 0.f, o2 = 0.f, d0 = 0.f, d1 = 0.f, d2 = 0.f;
+  Basis b;
+  uint32_t idx[3] = {0, 0, 0};
+  float p[6] = {0, 0, 0, 0, 0, 0};
+  uint32_t ref = 0, cur = 0;
+  int vis = 0;
+  const float4* __restrict__ P = m.pts;
+  while (true) {
+    const unsigned act = __ballot_sync(0xffffffffu, has);
+    if (__popc(act) <= kRefillBelow) {
+      if (pos >= stream_len && act == 0u) break;
+      const unsigned need = ~act;
+      const int64_t q = pos + __popc(need & ((1u << lane) - 1u));
+      if (!has && q < stream_len) {
+        r = (warp + (q >> 5) * n_warps) * 32 + (q & 31);
+        if (r < n) {
+          o0 = __ldg(o + 3 * r); o1 = __ldg(o + 3 * r + 1); o2 = __ldg(o + 3 * r + 2);
+          d0 = __ldg(d + 3 * r); d1 = __ldg(d + 3 * r + 1); d2 = __ldg(d + 3 * r + 2);
+          cur = (uint32_t)__ldg(start + r);
+          const int j = init_ray(m, o0, o1, o2, d0, d1, d2, (int)cur, b, idx, p);
+          ref = pick4u(__ldg(&m.sn[cur]), j);
+          P = ray_points(m, b);
+          vis = 1;
+          has = true;
+        }
+      }
+      pos += __popc(need);
+    }
+    if (!has) continue;
+    uint8_t st = 255;
+#pragma unroll 1
+    for (int s = 0; s < kStepsPerRound; ++s) {
+      if (ref >= n_tets) { st = 0; break; }
+      const uint32_t nxt = ref;
+      ref = advance<L>(m, P, b, idx, p, nxt, cur);
+      cur = nxt;
+      if ((uint32_t)++vis > fast_limit) {
+        st = ((uint32_t)vis > n_tets || long_walk<L>(m, P, b, idx, p, ref, cur, vis)) ? kError : 0;
+        break;
+      }
+    }
+    if (st != 255) {  // terminated this round
+      if (st != kError) st = (ref == kBoundary) ? kMiss : ((ref & kConstrained) ? kHit : kError);
+      write_result(m, r, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
+                   tet_back);
+      has = false;
+    }
+  }
 }
 
 // Visit-sequence recorder (second pass; offsets from a prior cast), _kernels.pyx:307-341.
@@ -507,6 +600,34 @@ struct CastL {
   static void launch(unsigned g, cudaStream_t s, A... a) { cast_kernel<L><<<g, kBlock, 0, s>>>(a...); }
 };
 template <int L>
+struct CastPersistL {
+  // grid: one full wave of resident blocks (or fewer for small batches)
+  template <typename... A>
+  static void launch(unsigned g, cudaStream_t s, A... a) {
+    static int per_sm = 0, sms = 0;
+    if (per_sm == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cast_persist_kernel<L>, kBlock, 0);
+      if (per_sm < 1) per_sm = 1;
+    }
+    const unsigned full = (unsigned)(per_sm * sms);
+    cast_persist_kernel<L><<<g < full ? g : full, kBlock, 0, s>>>(a...);
+  }
+};
+
+// TETB200_SCHED: 0 = auto, 1 = one ray per lane (cast_kernel), 2 = persistent
+// refill (cast_persist_kernel).
+int sched_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* v = getenv("TETB200_SCHED");
+    mode = v ? atoi(v) : 0;
+  }
+  return mode;
+}
+template <int L>
 struct VisitsL {
   template <typename... A>
   static void launch(unsigned g, cudaStream_t s, A... a) { visits_kernel<L><<<g, kBlock, 0, s>>>(a...); }
@@ -689,8 +810,11 @@ int tb_cast_rays(tb_mesh* m, int64_t n, const float* o, const float* d, const in
   if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
   DeviceGuard g(m->device);
   const cudaStream_t s = (cudaStream_t)stream;
-  if (int e = launch_layout<CastL>(m->layout, grid_for(n, kBlock), s, m->view(), n, o, d, start, status, cf,
-                                   tet, visited, triangle, t, tet_back))
+  const bool persist = sched_mode() == 2;
+  if (int e = persist ? launch_layout<CastPersistL>(m->layout, grid_for(n, kBlock), s, m->view(), n, o, d, start,
+                                                    status, cf, tet, visited, triangle, t, tet_back)
+                      : launch_layout<CastL>(m->layout, grid_for(n, kBlock), s, m->view(), n, o, d, start, status,
+                                             cf, tet, visited, triangle, t, tet_back))
     return e;
   TB_CUDA(cudaGetLastError());
   return TB_OK;
@@ -884,7 +1008,11 @@ int tb_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, con
   // Chunked 3-stream pipeline: chunk c's H2D, kernel and D2H are ordered on
   // stream c % 3, so copies of one chunk overlap the trace of the previous
   // one and the D2H of the one before (H2D and D2H use separate copy engines).
-  const int64_t chunk = PipeCtx::kChunk;
+  int64_t chunk = PipeCtx::kChunk;
+  if (const char* v = getenv("TETB200_CHUNK")) {  // experiment knob: rays per chunk (<= kChunk)
+    const int64_t c = atoll(v);
+    if (c > 0 && c < chunk) chunk = c;
+  }
   for (int64_t c0 = 0, c = 0; c0 < n; c0 += chunk, ++c) {
     const int64_t k = (n - c0 < chunk) ? (n - c0) : chunk;
     const size_t uk = (size_t)k;
