@@ -38,6 +38,7 @@ struct MeshView {
   const double* __restrict__ tri;     // (n_tri, 9)
   int64_t n_points;
   int64_t n_tets;
+  int32_t one;  // runtime 1 (opaque to the compiler): keeps count_less on the FMA pipe
 };
 
 __device__ __forceinline__ float pick3(float x, float y, float z, int a) {
@@ -221,20 +222,27 @@ __device__ __forceinline__ int init_ray(const MeshView& m, float o0, float o1, f
 template <int L>
 struct Record;
 
+// (Tried and measured slower, r01: moving the rank compares to the FMA pipe
+// as IMAD/IMAD.HI sign tricks -- fewer ALU ops but a longer dependent chain;
+// cfg2 -4 %, cfg4 -10 %.  The compares stay ISETP.)
+
 template <>
 struct Record<16> {
   uint4 r;
-  __device__ __forceinline__ void load(const MeshView& m, uint32_t t) { r = ldg_u4(&m.rec4[t]); }
+  int one;
+  __device__ __forceinline__ void load(const MeshView& m, uint32_t t) {
+    r = ldg_u4(&m.rec4[t]);
+    one = m.one;
+  }
   __device__ __forceinline__ uint32_t vxw() const { return r.x; }
   // Alg. 7, _kernels.pyx:222-235.
   __device__ __forceinline__ uint32_t next_ref(const uint32_t (&idx)[3], uint32_t i3, uint32_t idxf,
                                                uint32_t prev) const {
     const int rank = (idx[0] < idxf) + (idx[1] < idxf) + (idx[2] < idxf) + (i3 < idxf);
     const int order_a = (idx[0] < i3) + (idx[1] < i3) + (idx[2] < i3);
-    uint32_t nref = prev;
-    if (order_a != 3) nref ^= pick4u(r, 1 + order_a);
-    if (rank != 3) nref ^= pick4u(r, 1 + rank);
-    return nref;
+    // nx[3] := 0 makes the reference's "if order != 3" xor unconditional
+    const uint4 nx = make_uint4(r.y, r.z, r.w, 0u);
+    return prev ^ pick4u(nx, order_a) ^ pick4u(nx, rank);
   }
 };
 
@@ -242,16 +250,17 @@ template <>
 struct Record<20> {
   uint32_t v;
   uint4 n;
+  int one;
   __device__ __forceinline__ void load(const MeshView& m, uint32_t t) {
     v = __ldg(&m.vx[t]);
     n = ldg_u4(&m.rec4[t]);
+    one = m.one;
   }
   __device__ __forceinline__ uint32_t vxw() const { return v; }
   // Alg. 5, _kernels.pyx:207-221.
   __device__ __forceinline__ uint32_t next_ref(const uint32_t (&idx)[3], uint32_t i3, uint32_t idxf,
                                                uint32_t) const {
-    const int rank = (idx[0] < idxf) + (idx[1] < idxf) + (idx[2] < idxf) + (i3 < idxf);
-    return pick4u(n, rank);
+    return pick4u(n, (idx[0] < idxf) + (idx[1] < idxf) + (idx[2] < idxf) + (i3 < idxf));
   }
 };
 
