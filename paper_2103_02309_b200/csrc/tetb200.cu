@@ -65,7 +65,7 @@ struct tb_mesh {
     v.pts = pts; v.rec4 = rec4; v.vx = vx; v.sv = sv; v.sn = sn;
     v.cf_tri = cf_tri; v.cf_tets = cf_tets; v.tri = tri;
     v.n_points = n_points; v.n_tets = n_tets;
-    v.one = 1;
+    v.stride16 = 16;
     return v;
   }
 };
