@@ -126,6 +126,17 @@ int tb_locate_points(tb_mesh* mesh, int64_t n, const double* q, const int32_t* h
 int tb_locate_points_host(tb_mesh* mesh, int64_t n, const double* q, const int32_t* hints,
                           int32_t* tet, int32_t* visited);
 
+/* Hull clipping for ray origins outside the mesh.
+ * Replaces: the brute-force boundary-face search of traversal.cast_ray_auto
+ *   (traversal.py:545-589, hull_faces traversal.py:530-542).
+ *   o, d (n_all, 3) float32; rays (n,) int32 row indices into o/d, or NULL
+ *   for rows 0..n-1; hull (n_hull, 4) int32 = (tet, v0, v1, v2) per
+ *   boundary face in the reference's hull order.  Outputs, per ray: the
+ *   index of the nearest hull face hit (fp64 Moller-Trumbore with u, v, t
+ *   bounds; -1 = none) and its t. */
+int tb_hull_clip(tb_mesh* mesh, int64_t n, const float* o, const float* d, const int32_t* rays,
+                 int64_t n_hull, const int32_t* hull, int32_t* best_face, double* best_t, void* stream);
+
 /* Batch occlusion (shadow) walks.
  * Replaces: _kernels.shadow_rays (_kernels.pyx:527-614).
  *   p (n, 3) float64; light (n,3) float64 when light_stride == 3, or a single

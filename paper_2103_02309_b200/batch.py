@@ -54,6 +54,17 @@ def cast_rays(mesh, origins, dirs, start_tets, *, kernels=None) -> BatchHits:
     return BatchHits(status=status, cf=cf, triangle=triangle, t=t, tet_front=tet, tet_back=back, visited=visited)
 
 
+def cast_rays_auto(mesh, origins, dirs, *, kernels=None) -> BatchHits:
+    """Cast from arbitrary origins (no start tets): batched
+    traversal.cast_ray_auto (traversal.py:545-589) -- locate, or clip to the
+    hull.  Rays entering through a constrained hull face hit it immediately
+    (tet_front -1, tet_back = hull tet, visited 0)."""
+    k = _kernels(kernels)
+    status, cf, tet, visited, triangle, t, back = k.cast_rays_auto(mesh, origins, dirs)
+    _raise_on_error(status)
+    return BatchHits(status=status, cf=cf, triangle=triangle, t=t, tet_front=tet, tet_back=back, visited=visited)
+
+
 def cast_rays_visits(mesh, origins, dirs, start_tets, *, kernels=None):
     """Cast and also return visit sequences (batch.py:83-137):
     (hits, visits, offsets), ray i visited visits[offsets[i]:offsets[i+1]]."""

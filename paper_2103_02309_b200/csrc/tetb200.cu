@@ -65,7 +65,6 @@ struct tb_mesh {
     v.pts = pts; v.rec4 = rec4; v.vx = vx; v.sv = sv; v.sn = sn;
     v.cf_tri = cf_tri; v.cf_tets = cf_tets; v.tri = tri;
     v.n_points = n_points; v.n_tets = n_tets;
-    v.stride16 = 16;
     return v;
   }
 };
@@ -471,6 +470,82 @@ __global__ void __launch_bounds__(kBlock) locate_kernel(MeshView m, int64_t n, c
   visited[r] = vis;
 }
 
+// Hull clipping for origins outside the mesh (traversal.cast_ray_auto,
+// traversal.py:545-589): the nearest boundary face hit by the ray, tested
+// brute force in fp64 (Moller-Trumbore with u, v, t bounds, det == 0
+// skipped, first strictly-nearest face in hull order wins).  Hull faces are
+// staged through shared memory in tiles; each lane tests its ray against
+// every face.  Outputs the hull list index (-1 = no hit) and the hit t.
+constexpr int kHullTile = 128;
+
+__global__ void __launch_bounds__(kBlock) hull_clip_kernel(MeshView m, int64_t n, const float* __restrict__ o,
+                                                           const float* __restrict__ d,
+                                                           const int32_t* __restrict__ rays, int64_t n_hull,
+                                                           const int4* __restrict__ hull,  // (tet, v0, v1, v2)
+                                                           int32_t* __restrict__ best_face,
+                                                           double* __restrict__ best_t) {
+  __shared__ double tile[kHullTile][9];
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = i < n;
+  double O[3] = {0, 0, 0}, D[3] = {0, 0, 0};
+  if (live) {
+    const int64_t r = rays ? rays[i] : i;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      O[k] = (double)o[3 * r + k];
+      D[k] = (double)d[3 * r + k];
+    }
+  }
+  int32_t best = -1;
+  double bt = 0.0;
+  for (int64_t f0 = 0; f0 < n_hull; f0 += kHullTile) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < kHullTile; k += blockDim.x) {
+      if (f0 + k < n_hull) {
+        const int4 h = hull[f0 + k];
+        const int v[3] = {h.y, h.z, h.w};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const float4 P = ldg_f4(&m.pts[v[c]]);
+          tile[k][3 * c] = P.x;
+          tile[k][3 * c + 1] = P.y;
+          tile[k][3 * c + 2] = P.z;
+        }
+      }
+    }
+    __syncthreads();
+    if (!live) continue;
+    const int cnt = (int)((n_hull - f0) < kHullTile ? (n_hull - f0) : kHullTile);
+    for (int k = 0; k < cnt; ++k) {
+      const double* T = tile[k];
+      const double e1x = __dsub_rn(T[3], T[0]), e1y = __dsub_rn(T[4], T[1]), e1z = __dsub_rn(T[5], T[2]);
+      const double e2x = __dsub_rn(T[6], T[0]), e2y = __dsub_rn(T[7], T[1]), e2z = __dsub_rn(T[8], T[2]);
+      const double pvx = __dsub_rn(__dmul_rn(D[1], e2z), __dmul_rn(D[2], e2y));
+      const double pvy = __dsub_rn(__dmul_rn(D[2], e2x), __dmul_rn(D[0], e2z));
+      const double pvz = __dsub_rn(__dmul_rn(D[0], e2y), __dmul_rn(D[1], e2x));
+      const double det = __dadd_rn(__dadd_rn(__dmul_rn(e1x, pvx), __dmul_rn(e1y, pvy)), __dmul_rn(e1z, pvz));
+      if (det == 0.0) continue;
+      const double inv = __ddiv_rn(1.0, det);
+      const double tvx = __dsub_rn(O[0], T[0]), tvy = __dsub_rn(O[1], T[1]), tvz = __dsub_rn(O[2], T[2]);
+      const double u = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(tvx, pvx), __dmul_rn(tvy, pvy)), __dmul_rn(tvz, pvz)), inv);
+      const double qx = __dsub_rn(__dmul_rn(tvy, e1z), __dmul_rn(tvz, e1y));
+      const double qy = __dsub_rn(__dmul_rn(tvz, e1x), __dmul_rn(tvx, e1z));
+      const double qz = __dsub_rn(__dmul_rn(tvx, e1y), __dmul_rn(tvy, e1x));
+      const double v = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(D[0], qx), __dmul_rn(D[1], qy)), __dmul_rn(D[2], qz)), inv);
+      const double tt = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(e2x, qx), __dmul_rn(e2y, qy)), __dmul_rn(e2z, qz)), inv);
+      if (u < 0.0 || v < 0.0 || __dadd_rn(u, v) > 1.0 || tt < 0.0) continue;
+      if (best < 0 || tt < bt) {
+        best = (int32_t)(f0 + k);
+        bt = tt;
+      }
+    }
+  }
+  if (live) {
+    best_face[i] = best;
+    best_t[i] = bt;
+  }
+}
+
 // Occlusion walks, _kernels.pyx:527-614.
 template <int L>
 __global__ void __launch_bounds__(kBlock) shadow_kernel(MeshView m, int64_t n, const double* __restrict__ p,
@@ -847,6 +922,19 @@ int tb_cast_rays_visits(tb_mesh* m, int64_t n, const float* o, const float* d, c
   const cudaStream_t s = (cudaStream_t)stream;
   if (int e = launch_layout<VisitsL>(m->layout, grid_for(n, kBlock), s, m->view(), n, o, d, start, offsets, seq))
     return e;
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_hull_clip(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* rays, int64_t n_hull,
+                 const int32_t* hull, int32_t* best_face, double* best_t, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0 || n_hull < 0) return set_error(TB_E_ARG, "negative count");
+  if (n == 0) return TB_OK;
+  if (!o || !d || !best_face || !best_t || (n_hull > 0 && !hull)) return set_error(TB_E_ARG, "NULL buffer");
+  DeviceGuard g(m->device);
+  hull_clip_kernel<<<grid_for(n, kBlock), kBlock, 0, (cudaStream_t)stream>>>(
+      m->view(), n, o, d, rays, n_hull, reinterpret_cast<const int4*>(hull), best_face, best_t);
   TB_CUDA(cudaGetLastError());
   return TB_OK;
 }

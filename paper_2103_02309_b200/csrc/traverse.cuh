@@ -38,7 +38,6 @@ struct MeshView {
   const double* __restrict__ tri;     // (n_tri, 9)
   int64_t n_points;
   int64_t n_tets;
-  uint32_t stride16;  // runtime 16 (opaque to the compiler), see ldg_f4_at
 };
 
 __device__ __forceinline__ float pick3(float x, float y, float z, int a) {
@@ -53,16 +52,16 @@ __device__ __forceinline__ uint32_t pick4u(uint4 v, int k) {
 }
 
 __device__ __forceinline__ float4 ldg_f4(const float4* p) { return __ldg(p); }
-// 16 B read-only load of base[i] with the address formed by one mad.wide.
-// `stride` is a runtime 16 (MeshView.stride16): with a literal 16 ptxas
-// turns the multiply into LEA/LEA.HI.X on the saturated ALU pipe; an opaque
-// stride keeps it a single IMAD.WIDE on the FMA pipe.
-__device__ __forceinline__ float4 ldg_f4_at(const float4* base, uint32_t i, uint32_t stride) {
+// 16 B read-only load of base[i] with the address formed by one mad.wide
+// (base is a per-ray pointer; keeps the 64-bit index math off the hot
+// chain).  An opaque runtime stride (IMAD.WIDE instead of LEA) measured
+// slower (r01 A/B: cfg2 -2 %, cfg3 -2 %).
+__device__ __forceinline__ float4 ldg_f4_at(const float4* base, uint32_t i) {
   float4 r;
-  asm("{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %4, %6, %5;\n\t"
+  asm("{\n\t.reg .u64 a;\n\tmad.wide.u32 a, %4, 16, %5;\n\t"
       "ld.global.nc.v4.f32 {%0, %1, %2, %3}, [a];\n\t}"
       : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-      : "r"(i), "l"(base), "r"(stride));
+      : "r"(i), "l"(base));
   return r;
 }
 __device__ __forceinline__ uint4 ldg_u4(const uint4* p) { return __ldg(p); }
@@ -354,16 +353,16 @@ __device__ __forceinline__ uint32_t advance(const MeshView& m, const float4* __r
     project(b, q.x, q.y, q.z, qx, qy);
   } else {
     i3 = min(i3, (uint32_t)m.n_points - 1u);  // corrupt record: stay in bounds
-    const float4 q = ldg_f4_at(P, i3, m.stride16);
+    const float4 q = ldg_f4_at(P, i3);
     project_perm(b, q, qx, qy);
   }
   // Algorithm 1 (_kernels.pyx:94-102): f = c0 ? (c2 ? 1 : 0) : (c1 ? 2 : 0)
   const bool c0 = __fmul_rn(qx, p[1]) < __fmul_rn(qy, p[0]);
   const bool c2 = __fmul_rn(qx, p[5]) >= __fmul_rn(qy, p[4]);
   const bool c1 = __fmul_rn(qx, p[3]) < __fmul_rn(qy, p[2]);
-  const bool f1 = c0 & c2;
-  const bool f2 = !c0 & c1;
-  const bool f0 = c0 ? !c2 : !c1;
+  const bool f1 = c0 && c2;
+  const bool f2 = !c0 && c1;
+  const bool f0 = !(f1 || f2);
   const uint32_t idxf = f1 ? idx[1] : (f2 ? idx[2] : idx[0]);
   const uint32_t nref = rec.next_ref(idx, i3, idxf, prev);
   idx[0] = f0 ? i3 : idx[0];

@@ -155,6 +155,97 @@ def cast_rays_csr(mesh, o32, d32, start, *, layout: str | None = None):
             seq[:total].cpu().numpy(), offsets.cpu().numpy())
 
 
+def hull_clip(mesh, o32, d32):
+    """Nearest boundary face hit by each ray (GPU brute force, fp64):
+    returns (hull (k, 2) (tet, slot), face index per ray (-1 none), t)."""
+    import torch
+
+    from .tetmesh import hull_faces
+
+    o = _f32x3(o32)
+    d = _f32x3(d32)
+    n = len(o)
+    hull = hull_faces(mesh)
+    face = np.full(n, -1, dtype=np.int32)
+    tt = np.zeros(n, dtype=np.float64)
+    if n == 0 or len(hull) == 0:
+        return hull, face, tt
+    others = np.array([[1, 2, 3], [0, 2, 3], [0, 1, 3], [0, 1, 2]])
+    vids = mesh.side_verts[hull[:, 0][:, None], others[hull[:, 1]]]
+    table = np.ascontiguousarray(np.concatenate([hull[:, :1], vids], axis=1).astype(np.int32))
+    dm = device_mesh(mesh)
+    dev = torch.device("cuda", dm.device)
+    go, gd, gt = (torch.from_numpy(a).to(dev) for a in (o, d, table))
+    gf = torch.empty(n, dtype=torch.int32, device=dev)
+    gtt = torch.empty(n, dtype=torch.float64, device=dev)
+    check(lib.tb_hull_clip(dm.handle, n, addr(go), addr(gd), None, len(table), addr(gt), addr(gf), addr(gtt),
+                           torch.cuda.current_stream(dev).cuda_stream), "tb_hull_clip")
+    return hull, gf.cpu().numpy(), gtt.cpu().numpy()
+
+
+def _scalar_t(o, d, tri):
+    """traversal._ray_triangle_t (traversal.py:301-331): sequential-order fp64
+    t for the few rays that enter through a constrained hull face."""
+    e1 = tri[:, 1] - tri[:, 0]
+    e2 = tri[:, 2] - tri[:, 0]
+    p = np.stack([d[:, 1] * e2[:, 2] - d[:, 2] * e2[:, 1], d[:, 2] * e2[:, 0] - d[:, 0] * e2[:, 2],
+                  d[:, 0] * e2[:, 1] - d[:, 1] * e2[:, 0]], axis=1)
+    det = (e1[:, 0] * p[:, 0] + e1[:, 1] * p[:, 1]) + e1[:, 2] * p[:, 2]
+    tv = o - tri[:, 0]
+    q = np.stack([tv[:, 1] * e1[:, 2] - tv[:, 2] * e1[:, 1], tv[:, 2] * e1[:, 0] - tv[:, 0] * e1[:, 2],
+                  tv[:, 0] * e1[:, 1] - tv[:, 1] * e1[:, 0]], axis=1)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t = ((e2[:, 0] * q[:, 0] + e2[:, 1] * q[:, 1]) + e2[:, 2] * q[:, 2]) * (1.0 / det)
+        nrm = np.cross(e1, e2)
+        den = (nrm[:, 0] * d[:, 0] + nrm[:, 1] * d[:, 1]) + nrm[:, 2] * d[:, 2]
+        rel = tri[:, 0] - o
+        tp = np.where(den != 0.0, ((nrm[:, 0] * rel[:, 0] + nrm[:, 1] * rel[:, 1]) + nrm[:, 2] * rel[:, 2]) / den, 0.0)
+    return np.where(det != 0.0, t, tp)
+
+
+def cast_rays_auto(mesh, o32, d32):
+    """Cast without start tets (traversal.cast_ray_auto, traversal.py:545-589),
+    batched on the GPU: locate each origin; origins outside the mesh are
+    clipped to the nearest hull face -- entering through a constrained hull
+    face is an immediate hit (front -1, back = the hull tet, visited 0),
+    through an open boundary face the walk starts in that tet; no hull hit is
+    a miss with visited 0.  Returns the 7 arrays of cast_rays_full."""
+    o = _f32x3(o32)
+    d = _f32x3(d32)
+    n = len(o)
+    start, _ = locate_points(mesh, o.astype(np.float64), np.full(n, mesh.source_tet, np.int32))
+    status = np.zeros(n, np.uint8)
+    cf = np.full(n, -1, np.int32)
+    tet = np.full(n, -1, np.int32)
+    visited = np.zeros(n, np.int32)
+    triangle = np.full(n, -1, np.int32)
+    t = np.full(n, np.inf)
+    back = np.full(n, -1, np.int32)
+    out = np.nonzero(start < 0)[0]
+    if len(out):
+        hull, face, _ = hull_clip(mesh, o[out], d[out])
+        got = face >= 0
+        ht, hj = hull[face[got], 0], hull[face[got], 1]
+        refs = mesh.side_neighbors[ht, hj].astype(np.int64)
+        con = (refs & (1 << 31)) != 0
+        rays = out[got]
+        start[rays[~con]] = ht[~con]
+        hit = rays[con]
+        cfi = (refs[con] & 0x7FFFFFFF).astype(np.int32)
+        status[hit] = STATUS_HIT
+        cf[hit] = cfi
+        triangle[hit] = mesh.cf_triangle[cfi]
+        back[hit] = ht[con]
+        t[hit] = _scalar_t(o[hit].astype(np.float64), d[hit].astype(np.float64),
+                           mesh.triangle_coords()[mesh.cf_triangle[cfi]])
+    go = np.nonzero(start >= 0)[0]
+    if len(go):
+        res = cast_rays_full(mesh, o[go], d[go], start[go])
+        for dst, src in zip((status, cf, tet, visited, triangle, t, back), res):
+            dst[go] = src
+    return status, cf, tet, visited, triangle, t, back
+
+
 def locate_points(mesh, q, hints):
     """Batch point location -> (tet i32 (-1 outside), visited i32) (_kernels.pyx:416-492)."""
     qq = _f64x3(q)

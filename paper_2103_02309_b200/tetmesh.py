@@ -566,6 +566,21 @@ def validate(mesh: CompactMesh) -> list[str]:
     return problems
 
 
+def hull_faces(mesh: CompactMesh) -> np.ndarray:
+    """(k, 2) int64 (tet, slot) of the mesh boundary faces in the reference's
+    order (traversal.hull_faces, traversal.py:530-542): unconstrained boundary
+    sentinels plus hull-backed constrained faces seen from their front tet."""
+    refs = mesh.side_neighbors.astype(np.int64)
+    boundary = refs == BOUNDARY_REF
+    constrained = (refs & CONSTRAINED_BIT) != 0
+    cf = np.where(constrained, refs & REF_PAYLOAD_MASK, 0)
+    rows = np.broadcast_to(np.arange(mesh.n_tets)[:, None], refs.shape)
+    cft = np.asarray(mesh.cf_tets).reshape(-1, 2)
+    hull_cf = constrained & (cft[cf, 1] == NO_TET) & (cft[cf, 0] == rows) if len(cft) else np.zeros_like(constrained)
+    t, j = np.nonzero(boundary | hull_cf)
+    return np.stack([t, j], axis=1)
+
+
 def _cross_links(side_neighbors: np.ndarray, cf_tets: np.ndarray) -> np.ndarray:
     refs = side_neighbors.astype(np.int64)
     out = _plain_neighbor_matrix(side_neighbors)

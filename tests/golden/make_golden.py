@@ -174,6 +174,33 @@ def main():
                 h = batch.cast_rays(r, o[:2000], d[:2000], _remap_start(m, r, st[:2000]), kernels=K)
                 dig[f"{name}/reorder/{scheme}/cast2k"] = digest(h.status, h.triangle, h.visited)
 
+    # locality metric (render.py:565-591) and the reference's .npz format (cli.py:249-290)
+    from tetray.cli import save_compact
+    from tetray.render import visit_locality_metric
+
+    for name in ("region4", "model"):
+        for scheme in ("none", "hilbert", "shuffle"):
+            dig[f"{name}/locality/{scheme}"] = visit_locality_metric(reorder(fixtures[name], scheme), kernels=K)
+    save_compact(relayout(fixtures["pane4"], "tet16"), OUT / "pane4_tet16_ref.npz")
+
+    # cast_ray_auto: origins inside and outside the hull (traversal.py:545-589)
+    for name in ("box4", "pane4", "open_box4"):
+        m = fixtures[name]
+        rng = np.random.default_rng(50)
+        o = rng.uniform(-2.0, 6.0, size=(400, 3)).astype(np.float32)
+        d = rng.normal(size=(400, 3)).astype(np.float32)
+        rows = []
+        for i in range(len(o)):
+            res = traversal.cast_ray_auto(Ray(Vec3(*o[i]), Vec3(*d[i])), m)
+            if isinstance(res, traversal.HitRecord):
+                rows.append((1, res.cf_index, res.triangle_id, res.t, res.tet_front, res.tet_back, res.visited))
+            else:
+                rows.append((0, -1, -1, np.inf, -1, -1, res.visited))
+        a = np.array(rows, dtype=np.float64)
+        arrays[f"{name}/auto/o"] = o
+        arrays[f"{name}/auto/d"] = d
+        arrays[f"{name}/auto/result"] = a  # kind, cf, triangle, t, front, back, visited
+
     # visit sequences (test_kernels.py:44-51)
     m = fixtures["region4"]
     o, d, st = interior_rays(m, 500, 41)

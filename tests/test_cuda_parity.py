@@ -211,6 +211,41 @@ def test_config1_blob12_camera(digests, K, scheme):
     assert digest(*out[4:]) == digests[f"blob12/{scheme}/epilogue"]
 
 
+@pytest.mark.parametrize("name", ("box4", "pane4", "open_box4"))
+def test_cast_rays_auto_vs_reference(golden, K, name):
+    """Batched cast_ray_auto (locate or hull-clip, then walk) against the
+    reference's scalar traversal.cast_ray_auto on origins in and out of the
+    box: hit/miss, constrained face, triangle, front/back tets and visited
+    exact; t to 1e-12 relative (the scalar engine sums dot products in a
+    different order than the batch epilogue)."""
+    from paper_2103_02309_b200 import batch
+
+    m = golden_mesh(golden, name)
+    o, d = golden[f"{name}/auto/o"], golden[f"{name}/auto/d"]
+    ref = golden[f"{name}/auto/result"]
+    h = batch.cast_rays_auto(m, o, d)
+    hit = ref[:, 0] == 1
+    assert np.array_equal(h.status == 1, hit)
+    assert np.array_equal(h.cf[hit], ref[hit, 1].astype(np.int32))
+    assert np.array_equal(h.triangle[hit], ref[hit, 2].astype(np.int32))
+    assert np.allclose(h.t[hit], ref[hit, 3], rtol=1e-12, atol=0)
+    assert np.array_equal(h.tet_front[hit], ref[hit, 4].astype(np.int32))
+    assert np.array_equal(h.tet_back[hit], ref[hit, 5].astype(np.int32))
+    assert np.array_equal(h.visited, ref[:, 6].astype(np.int32))
+
+
+@pytest.mark.parametrize("name", ("region4", "model"))
+@pytest.mark.parametrize("scheme", ("none", "hilbert", "shuffle"))
+def test_visit_locality_metric(golden, digests, name, scheme):
+    """render.visit_locality_metric (render.py:565-591) from GPU visit
+    sequences equals the reference's value for every reorder scheme."""
+    from paper_2103_02309_b200.io import visit_locality_metric
+    from paper_2103_02309_b200.tetmesh import reorder
+
+    m = reorder(golden_mesh(golden, name), scheme)
+    assert visit_locality_metric(m) == digests[f"{name}/locality/{scheme}"]
+
+
 def test_batch_layer_mirror(golden, K):
     """The mirrored batch API (batch.py:39-80 semantics) over the CUDA module."""
     from paper_2103_02309_b200 import batch

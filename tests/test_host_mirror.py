@@ -9,7 +9,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import FIXTURES, PANE_OCC, REGION_OCC, digest, golden_mesh, mesh_digest
+from conftest import FIXTURES, GOLDEN as ROOT_GOLDEN, PANE_OCC, REGION_OCC, digest, golden_mesh, mesh_digest
 
 from paper_2103_02309_b200 import hilbert, scenes
 from paper_2103_02309_b200.ingestion import build_box_fixture
@@ -141,3 +141,25 @@ def test_interior_rays_match_reference(meshes, digests):
 def test_golden_mesh_roundtrip(golden):
     m = golden_mesh(golden, "pane4", "tet16")
     assert m.records_u32().shape == (m.n_tets, 4)
+
+
+def test_npz_interop_with_reference_cli(tmp_path, golden):
+    """load_compact reads a file written by the reference's cli.save_compact
+    (cli.py:249-265), and save/load round-trips byte-identically."""
+    from paper_2103_02309_b200.io import load_compact, save_compact
+
+    ref = load_compact(ROOT_GOLDEN / "pane4_tet16_ref.npz")
+    assert ref.layout == "tet16"
+    assert mesh_digest(ref) == mesh_digest(relayout(golden_mesh(golden, "pane4"), "tet16"))
+    p = tmp_path / "m.npz"
+    save_compact(ref, p)
+    assert mesh_digest(load_compact(p)) == mesh_digest(ref)
+
+
+def test_hull_faces_order(meshes):
+    from paper_2103_02309_b200.tetmesh import hull_faces
+
+    h = hull_faces(meshes["box4"])
+    assert len(h) == 6 * 2 * 16  # every wall face of the n=4 box
+    assert np.all(np.diff(h[:, 0] * 4 + h[:, 1]) > 0)  # tet-major, slot-minor
+    assert len(hull_faces(meshes["open_box4"])) == len(h)
