@@ -126,6 +126,15 @@ int tb_locate_points(tb_mesh* mesh, int64_t n, const double* q, const int32_t* h
 int tb_locate_points_host(tb_mesh* mesh, int64_t n, const double* q, const int32_t* hints,
                           int32_t* tet, int32_t* visited);
 
+/* Pinhole camera rays generated on the device (current device).
+ * Replaces: render.camera_rays (render.py:169-185) for primary rays.
+ *   frame: 14 float64 device values = fwd[3], right[3], up2[3], pos[3],
+ *   half_w, half_h (computed on the host as render.camera_rays does);
+ *   pixels (n,) int64 row-major pixel ids (y * width + x) or NULL for
+ *   0..n-1; o, d (n, 3) float32 outputs, bit-identical to the host's. */
+int tb_camera_rays(int64_t width, int64_t height, const double* frame, const int64_t* pixels, int64_t n,
+                   float* o, float* d, void* stream);
+
 /* Hull clipping for ray origins outside the mesh.
  * Replaces: the brute-force boundary-face search of traversal.cast_ray_auto
  *   (traversal.py:545-589, hull_faces traversal.py:530-542).

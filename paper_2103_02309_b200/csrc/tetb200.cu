@@ -470,6 +470,31 @@ __global__ void __launch_bounds__(kBlock) locate_kernel(MeshView m, int64_t n, c
   visited[r] = vis;
 }
 
+// Pinhole camera rays on the device (render.camera_rays, render.py:169-185):
+// the per-camera frame (fwd, right, up2, half_w, half_h) comes from the host
+// (numpy, once per frame); the per-pixel fp64 arithmetic is repeated here in
+// numpy's broadcast order -- sx = ((x + .5) / W * 2 - 1) * half_w,
+// sy = (1 - (y + .5) / H * 2) * half_h, d = (fwd + sx * right) + sy * up2 --
+// then rounded to f32, so the rays are bit-identical to the host's.  Saves
+// the 24 B/ray origin + direction upload for primary rays.
+__global__ void camera_rays_kernel(int64_t width, int64_t height, const double* __restrict__ fr,
+                                   const int64_t* __restrict__ pixels, int64_t n, float* __restrict__ o,
+                                   float* __restrict__ d) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t pix = pixels ? pixels[i] : i;
+  const double xs = (double)(pix % width), ys = (double)(pix / width);
+  const double W = (double)width, H = (double)height;
+  const double sx = __dmul_rn(__dsub_rn(__dmul_rn(__ddiv_rn(__dadd_rn(xs, 0.5), W), 2.0), 1.0), fr[12]);
+  const double sy = __dmul_rn(__dsub_rn(1.0, __dmul_rn(__ddiv_rn(__dadd_rn(ys, 0.5), H), 2.0)), fr[13]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double dk = __dadd_rn(__dadd_rn(fr[k], __dmul_rn(sx, fr[3 + k])), __dmul_rn(sy, fr[6 + k]));
+    d[3 * i + k] = __double2float_rn(dk);
+    o[3 * i + k] = __double2float_rn(fr[9 + k]);
+  }
+}
+
 // Hull clipping for origins outside the mesh (traversal.cast_ray_auto,
 // traversal.py:545-589): the nearest boundary face hit by the ray, tested
 // brute force in fp64 (Moller-Trumbore with u, v, t bounds, det == 0
@@ -922,6 +947,16 @@ int tb_cast_rays_visits(tb_mesh* m, int64_t n, const float* o, const float* d, c
   const cudaStream_t s = (cudaStream_t)stream;
   if (int e = launch_layout<VisitsL>(m->layout, grid_for(n, kBlock), s, m->view(), n, o, d, start, offsets, seq))
     return e;
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_camera_rays(int64_t width, int64_t height, const double* frame, const int64_t* pixels, int64_t n, float* o,
+                   float* d, void* stream) {
+  if (width <= 0 || height <= 0 || n < 0) return set_error(TB_E_ARG, "bad camera size");
+  if (n == 0) return TB_OK;
+  if (!frame || !o || !d) return set_error(TB_E_ARG, "NULL buffer");
+  camera_rays_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(width, height, frame, pixels, n, o, d);
   TB_CUDA(cudaGetLastError());
   return TB_OK;
 }

@@ -80,6 +80,7 @@ class DeviceMesh:
             "tb_mesh_create",
         )
         self.handle = h
+        self.source_tet = int(mesh.source_tet)
         self.n_tets = len(sv)
         self.n_points = len(pts)
         self.n_cf = len(cft)

@@ -171,13 +171,10 @@ def kuhn_strip_scene(n: int = KUHN5_N, layout: str = "tet16", scheme: str = "non
 # Rays
 
 
-def camera_rays(position, look_at, up, fov, width, height, xs=None, ys=None):
-    """f32 (origins, dirs) through pixel centres, row-major over the frame
-    unless explicit pixel coordinates are given (render.py:169-185)."""
-    if xs is None:
-        yy, xx = np.mgrid[0:height, 0:width]
-        xs = xx.ravel().astype(np.float64)
-        ys = yy.ravel().astype(np.float64)
+def camera_frame(position, look_at, up, fov, width, height) -> np.ndarray:
+    """The per-frame camera constants of render.camera_rays (render.py:169-185):
+    float64 [fwd(3), right(3), up2(3), pos(3), half_w, half_h] -- what the
+    device ray generator (tb_camera_rays) needs."""
     pos = np.asarray(position, dtype=np.float64)
     look = np.asarray(look_at, dtype=np.float64)
     upv = np.asarray(up, dtype=np.float64)
@@ -188,6 +185,19 @@ def camera_rays(position, look_at, up, fov, width, height, xs=None, ys=None):
     up2 = np.cross(right, fwd)
     half_h = np.tan(np.radians(fov) * 0.5)
     half_w = half_h * width / height
+    return np.concatenate([fwd, right, up2, pos, [half_w, half_h]]).astype(np.float64)
+
+
+def camera_rays(position, look_at, up, fov, width, height, xs=None, ys=None):
+    """f32 (origins, dirs) through pixel centres, row-major over the frame
+    unless explicit pixel coordinates are given (render.py:169-185)."""
+    if xs is None:
+        yy, xx = np.mgrid[0:height, 0:width]
+        xs = xx.ravel().astype(np.float64)
+        ys = yy.ravel().astype(np.float64)
+    fr = camera_frame(position, look_at, up, fov, width, height)
+    fwd, right, up2, pos = fr[0:3], fr[3:6], fr[6:9], fr[9:12]
+    half_w, half_h = fr[12], fr[13]
     sx = ((xs + 0.5) / width * 2.0 - 1.0) * half_w
     sy = (1.0 - (ys + 0.5) / height * 2.0) * half_h
     d = fwd[None] + sx[:, None] * right[None] + sy[:, None] * up2[None]

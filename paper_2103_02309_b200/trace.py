@@ -78,6 +78,39 @@ def trace(mesh, origins: torch.Tensor, dirs: torch.Tensor, start: torch.Tensor, 
     return res
 
 
+def camera_rays_device(camera: dict, width: int, height: int, device, pixels: torch.Tensor | None = None,
+                       stream=None):
+    """Primary rays generated in HBM (bit-identical to scenes.camera_rays):
+    (o, d) float32 (n, 3) CUDA tensors, row-major pixels or the given ids."""
+    from .scenes import camera_frame
+
+    dev = torch.device(device)
+    frame = torch.from_numpy(camera_frame(camera["position"], camera["look_at"], camera.get("up", (0.0, 1.0, 0.0)),
+                                          camera.get("fov", 68.0), width, height)).to(dev)
+    n = pixels.numel() if pixels is not None else width * height
+    o = torch.empty((n, 3), dtype=torch.float32, device=dev)
+    d = torch.empty((n, 3), dtype=torch.float32, device=dev)
+    s = (stream or torch.cuda.current_stream(dev)).cuda_stream
+    with torch.cuda.device(dev):
+        check(lib.tb_camera_rays(width, height, addr(frame), addr(pixels), n, addr(o), addr(d), s), "tb_camera_rays")
+    return o, d
+
+
+def trace_camera(mesh, camera: dict, width: int, height: int, *, device=None, out: TraceResult | None = None,
+                 stream=None, sctp: bool = False, layout: str | None = None):
+    """Render-style primary pass entirely on the device: locate the camera,
+    generate the frame's rays in HBM, trace.  Returns (TraceResult, cam_tet)."""
+    dm = device_mesh(mesh, device=None if device is None else torch.device(device).index, layout=layout)
+    dev = torch.device("cuda", dm.device)
+    q = torch.tensor([camera["position"]], dtype=torch.float64, device=dev)
+    cam, _ = locate(dm, q, torch.tensor([dm.source_tet], dtype=torch.int32, device=dev))
+    if int(cam.item()) < 0:  # render.py:478-482
+        raise ValueError("camera is outside the tetrahedralized volume")
+    o, d = camera_rays_device(camera, width, height, dev, stream=stream)
+    start = cam.repeat(o.shape[0])
+    return trace(dm, o, d, start, out=out, stream=stream, sctp=sctp), cam
+
+
 def locate(mesh, q: torch.Tensor, hints: torch.Tensor, *, stream=None):
     """Device point location: (tet, visited) int32 tensors."""
     dm = device_mesh(mesh, device=q.device.index)

@@ -246,6 +246,31 @@ def test_visit_locality_metric(golden, digests, name, scheme):
     assert visit_locality_metric(m) == digests[f"{name}/locality/{scheme}"]
 
 
+def test_device_camera_rays_and_trace_camera(digests):
+    """On-device primary rays are bit-identical to render.camera_rays, and the
+    all-device render pass reproduces the reference's config-1 digests."""
+    import torch
+
+    from paper_2103_02309_b200.scenes import BLOB_CAMERA, blob_scene, camera_rays
+    from paper_2103_02309_b200.trace import camera_rays_device, trace_camera
+
+    o_h, d_h = camera_rays(BLOB_CAMERA["position"], BLOB_CAMERA["look_at"], BLOB_CAMERA["up"], BLOB_CAMERA["fov"],
+                           256, 256)
+    o, d = camera_rays_device(BLOB_CAMERA, 256, 256, "cuda:0")
+    assert np.array_equal(o.cpu().numpy(), o_h) and np.array_equal(d.cpu().numpy(), d_h)
+    assert digest(o.cpu().numpy(), d.cpu().numpy()) == digests["blob12/rays"]
+    pix = torch.tensor([5, 70000 % 65536, 65535], dtype=torch.int64, device="cuda:0")
+    o2, d2 = camera_rays_device(BLOB_CAMERA, 256, 256, "cuda:0", pixels=pix)
+    assert np.array_equal(d2.cpu().numpy(), d_h[pix.cpu().numpy()])
+    sc = blob_scene(12, scheme="hilbert")
+    res, cam = trace_camera(sc.mesh, BLOB_CAMERA, 256, 256)
+    torch.cuda.synchronize()
+    assert int(cam.item()) == digests["blob12/hilbert/cam_tet"]
+    got = [x.cpu().numpy() for x in (res.status, res.cf, res.tet, res.visited, res.triangle, res.t, res.tet_back)]
+    assert digest(*got[:4]) == digests["blob12/hilbert/cast"]
+    assert digest(*got[4:]) == digests["blob12/hilbert/epilogue"]
+
+
 def test_batch_layer_mirror(golden, K):
     """The mirrored batch API (batch.py:39-80 semantics) over the CUDA module."""
     from paper_2103_02309_b200 import batch
