@@ -97,18 +97,24 @@ def camera_rays_device(camera: dict, width: int, height: int, device, pixels: to
 
 
 def trace_camera(mesh, camera: dict, width: int, height: int, *, device=None, out: TraceResult | None = None,
-                 stream=None, sctp: bool = False, layout: str | None = None):
-    """Render-style primary pass entirely on the device: locate the camera,
-    generate the frame's rays in HBM, trace.  Returns (TraceResult, cam_tet)."""
+                 stream=None, sctp: bool = False, layout: str | None = None, cam_tet: int | None = None):
+    """Render-style primary pass entirely on the device: locate the camera
+    (render.py:478-482; skipped when ``cam_tet`` is given), generate the
+    frame's rays in HBM, trace.  ``out`` may hold pinned host tensors: the
+    kernel then writes the hits straight to host memory over PCIe (mapped
+    pinned memory under UVA), overlapping the copy with the walk.
+    Returns (TraceResult, cam_tet)."""
     dm = device_mesh(mesh, device=None if device is None else torch.device(device).index, layout=layout)
     dev = torch.device("cuda", dm.device)
-    q = torch.tensor([camera["position"]], dtype=torch.float64, device=dev)
-    cam, _ = locate(dm, q, torch.tensor([dm.source_tet], dtype=torch.int32, device=dev))
-    if int(cam.item()) < 0:  # render.py:478-482
-        raise ValueError("camera is outside the tetrahedralized volume")
+    if cam_tet is None:
+        q = torch.tensor([camera["position"]], dtype=torch.float64, device=dev)
+        cam, _ = locate(dm, q, torch.tensor([dm.source_tet], dtype=torch.int32, device=dev))
+        cam_tet = int(cam.item())
+        if cam_tet < 0:
+            raise ValueError("camera is outside the tetrahedralized volume")
     o, d = camera_rays_device(camera, width, height, dev, stream=stream)
-    start = cam.repeat(o.shape[0])
-    return trace(dm, o, d, start, out=out, stream=stream, sctp=sctp), cam
+    start = torch.full((o.shape[0],), cam_tet, dtype=torch.int32, device=dev)
+    return trace(dm, o, d, start, out=out, stream=stream, sctp=sctp), cam_tet
 
 
 def locate(mesh, q: torch.Tensor, hints: torch.Tensor, *, stream=None):

@@ -265,10 +265,19 @@ def test_device_camera_rays_and_trace_camera(digests):
     sc = blob_scene(12, scheme="hilbert")
     res, cam = trace_camera(sc.mesh, BLOB_CAMERA, 256, 256)
     torch.cuda.synchronize()
-    assert int(cam.item()) == digests["blob12/hilbert/cam_tet"]
+    assert cam == digests["blob12/hilbert/cam_tet"]
     got = [x.cpu().numpy() for x in (res.status, res.cf, res.tet, res.visited, res.triangle, res.t, res.tet_back)]
     assert digest(*got[:4]) == digests["blob12/hilbert/cast"]
     assert digest(*got[4:]) == digests["blob12/hilbert/epilogue"]
+    # hits written straight into pinned host memory (zero-copy outputs)
+    from paper_2103_02309_b200.trace import TraceResult
+
+    host = TraceResult(*[torch.empty(256 * 256, dtype=x.dtype).pin_memory() for x in
+                         (res.status, res.cf, res.triangle, res.t, res.tet, res.tet_back, res.visited)])
+    trace_camera(sc.mesh, BLOB_CAMERA, 256, 256, out=host, cam_tet=cam)
+    torch.cuda.synchronize()
+    h = [x.numpy() for x in (host.status, host.cf, host.tet, host.visited, host.triangle, host.t, host.tet_back)]
+    assert digest(*h[:4]) == digests["blob12/hilbert/cast"] and digest(*h[4:]) == digests["blob12/hilbert/epilogue"]
 
 
 def test_batch_layer_mirror(golden, K):
