@@ -348,6 +348,8 @@ def run_ours(args, cfg):
     # up and the clocks have left idle) through the end of the timed region.
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     gather_ms = 0.0
+    gather_check = None
+    gather_error = None
     with ClockSampler(local) as clocks:
         time.sleep(0.3)  # nvidia-smi start-up
         clocks.mark("t_ramp")
@@ -372,7 +374,12 @@ def run_ours(args, cfg):
             g0.record(stream)
             packed = multigpu.pack_hits(gidx, res.status, res.cf, res.tet, res.visited, res.triangle, res.t,
                                         res.tet_back)
-            multigpu.gather_hits(packed, per_frame * world)
+            try:
+                full = multigpu.gather_hits(packed, per_frame * world)
+                if full is not None:  # rank 0 holds every rank's hits for the last frame set
+                    gather_check = int((full["visited"] > 0).sum().item())
+            except Exception as exc:  # report, do not lose the line
+                gather_error = repr(exc)
             g1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
@@ -486,6 +493,9 @@ def run_ours(args, cfg):
         "tets_visited_per_ray": {"mean": vis_sum / total_rays, "max": vis_max},
         "kernel_ms": {"mean": float(kernel_ms.mean()), "min": float(kernel_ms.min()), "max": float(kernel_ms.max())},
         "gather_ms": gather_ms if world > 1 else None,
+        "gather": None if world == 1 else {"rays_gathered_to_rank0": gather_check,
+                                            "rays_expected": per_frame * world, "error": gather_error,
+                                            "collective": "torch.distributed.gather (NCCL), 40 B packed records"},
         "wall_ms_per_step": wall / args.steps * 1e3,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
