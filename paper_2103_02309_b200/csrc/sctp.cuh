@@ -33,15 +33,16 @@ __device__ __forceinline__ double ddot3(const D3& a, const D3& b) {
 __device__ __forceinline__ D3 dsel(bool c, const D3& a, const D3& b) { return c ? a : b; }
 
 // Exit slot of the sorted quad (P, ids ascending); entry < 0 = none.
+// rho_pos: sign of the quad's fp64 orientation (p1-p0).((p2-p0)x(p3-p0)) --
+// the same expression as orientation() in traverse.cuh, so it comes from
+// the per-tet table MeshView.orient instead of 30 fp64 ops per step.
 __device__ __forceinline__ int sctp_exit(const float4 (&P)[4], const uint32_t (&)[4], const double (&O)[3],
-                                         const double (&Dd)[3], int entry) {
+                                         const double (&Dd)[3], int entry, bool rho_pos) {
   const D3 o = {O[0], O[1], O[2]};
   const D3 d = {Dd[0], Dd[1], Dd[2]};
   D3 p[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) p[i] = {(double)P[i].x, (double)P[i].y, (double)P[i].z};
-  const double rho = ddot3(dsub3(p[1], p[0]), dcross3(dsub3(p[2], p[0]), dsub3(p[3], p[0])));
-  const bool rho_pos = rho > 0.0;
   int best_j = -1;
   double best_m = -INFINITY;
 #pragma unroll
@@ -114,7 +115,7 @@ __device__ __forceinline__ uint32_t sctp_advance(const MeshView& m, SctpWindow& 
   P[2] = (pos < 2) ? w.P[1] : ((pos == 2) ? q : w.P[2]);
   ids[3] = (pos < 3) ? w.id[2] : i3;
   P[3] = (pos < 3) ? w.P[2] : q;
-  const int j = sctp_exit(P, ids, O, D, pos);
+  const int j = sctp_exit(P, ids, O, D, pos, __ldg(&m.orient[nxt]) != 0);
   const uint32_t idxf = (j == 0) ? ids[0] : ((j == 1) ? ids[1] : ((j == 2) ? ids[2] : ids[3]));
   const uint32_t nref = rec.next_ref(w.id, i3, idxf, prev);
   w.drop(P, ids, j);

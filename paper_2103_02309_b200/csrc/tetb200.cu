@@ -57,13 +57,14 @@ struct tb_mesh {
   int32_t* cf_tri = nullptr;
   int2* cf_tets = nullptr;
   double* tri = nullptr;
+  uint8_t* orient = nullptr;
   int64_t hbm_bytes = 0;
   int64_t hot_bytes = 0;
 
   MeshView view() const {
     MeshView v;
     v.pts = pts; v.rec4 = rec4; v.vx = vx; v.sv = sv; v.sn = sn;
-    v.cf_tri = cf_tri; v.cf_tets = cf_tets; v.tri = tri;
+    v.cf_tri = cf_tri; v.cf_tets = cf_tets; v.tri = tri; v.orient = orient;
     v.n_points = n_points; v.n_tets = n_tets;
     return v;
   }
@@ -105,6 +106,17 @@ __global__ void pad_points_kernel(const float* __restrict__ xyz, float4* __restr
       out[(size_t)perm_index(mx, ot) * (size_t)n + i] = make_float4(q[mx], q[ot], q[mn], 0.0f);
     }
   }
+}
+
+// Per-tet sign of the start-quad orientation used by init_ray and the ScTP
+// predicate (_kernels.pyx:133-147, traversal.py:499): computed once here with
+// the same fp64 expression instead of once per ray (or per ScTP step).
+__global__ void orient_kernel(const int4* __restrict__ sv, const float4* __restrict__ pts,
+                              uint8_t* __restrict__ out, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int4 v = sv[i];
+  out[i] = orientation(pts[v.x], pts[v.y], pts[v.z], pts[v.w]) > 0.0 ? 1 : 0;
 }
 
 __global__ void split_tet20_kernel(const uint32_t* __restrict__ rec, uint32_t* __restrict__ vx,
@@ -660,7 +672,7 @@ __global__ void __launch_bounds__(kBlock) sctp_kernel(MeshView m, int64_t n, con
   float4 P[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) P[i] = ldg_f4(&m.pts[ids[i]]);
-  const int j = sctp_exit(P, ids, O, D, -1);
+  const int j = sctp_exit(P, ids, O, D, -1, __ldg(&m.orient[cur]) != 0);
   w.drop(P, ids, j);
   uint32_t ref = pick4u(__ldg(&m.sn[cur]), j);
   uint32_t prev = cur;
@@ -827,6 +839,9 @@ int tb_mesh_create(int device, int layout, int64_t n_points, const float* points
   TB_MC(cudaMemcpy(m->sv, side_verts, n_tets * sizeof(int4), cudaMemcpyHostToDevice));
   TB_MC(cudaMalloc(&m->sn, n_tets * sizeof(uint4)));
   TB_MC(cudaMemcpy(m->sn, side_neighbors, n_tets * sizeof(uint4), cudaMemcpyHostToDevice));
+  TB_MC(cudaMalloc(&m->orient, n_tets));
+  orient_kernel<<<grid_for(n_tets, 256), 256>>>(m->sv, m->pts, m->orient, n_tets);
+  TB_MC(cudaGetLastError());
 
   int64_t rec_bytes = 0;
   if (layout == 16) {
@@ -867,7 +882,7 @@ int tb_mesh_create(int device, int layout, int64_t n_points, const float* points
     TB_MC(cudaMemcpy(m->tri, tri_coords, n_tri * 9 * sizeof(double), cudaMemcpyHostToDevice));
   }
 #undef TB_MC
-  m->hbm_bytes = n_points * 16 * 6 + n_tets * 32 + rec_bytes + n_cf * 12 + n_tri * 72;
+  m->hbm_bytes = n_points * 16 * 6 + n_tets * 33 + rec_bytes + n_cf * 12 + n_tri * 72;
   // Hot accelerator bytes as the reference counts them (records + f32 xyz points).
   m->hot_bytes = (layout == 80) ? rec_bytes : rec_bytes + n_points * 12;
   *out = m;
@@ -885,6 +900,7 @@ int tb_mesh_destroy(tb_mesh* m) {
   cudaFree(m->cf_tri);
   cudaFree(m->cf_tets);
   cudaFree(m->tri);
+  cudaFree(m->orient);
   delete m;
   return TB_OK;
 }

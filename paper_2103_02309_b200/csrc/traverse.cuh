@@ -36,9 +36,13 @@ struct MeshView {
   const int32_t* __restrict__ cf_tri; // (c,)
   const int2* __restrict__ cf_tets;   // (c,) front, back
   const double* __restrict__ tri;     // (n_tri, 9)
+  const uint8_t* __restrict__ orient; // (t,) rho(sorted quad) > 0, see orientation()
   int64_t n_points;
   int64_t n_tets;
 };
+
+// Index of the axis-permuted point copy holding (q[mx], q[ot], q[mn]).
+__device__ __forceinline__ int perm_index(int mx, int ot) { return mx * 2 + (ot > mx ? ot - 1 : ot); }
 
 __device__ __forceinline__ float pick3(float x, float y, float z, int a) {
   return a == 0 ? x : (a == 1 ? y : z);
@@ -136,6 +140,25 @@ __device__ __forceinline__ int exit_face(float px, float py, const float (&p)[6]
   return (a1 < b1) ? 2 : 0;
 }
 
+// fp64 orientation of four points as init_ray computes it for the start
+// quad (_kernels.pyx:133-147): e_k = P_k - P_0 in double, then
+// e1x (e2y e3z - e2z e3y) + e1y (e2z e3x - e2x e3z) + e1z (e2x e3y - e2y e3x).
+__device__ __forceinline__ double orientation(const float4& P0, const float4& P1, const float4& P2,
+                                              const float4& P3) {
+  const double e1x = __dsub_rn((double)P1.x, (double)P0.x);
+  const double e1y = __dsub_rn((double)P1.y, (double)P0.y);
+  const double e1z = __dsub_rn((double)P1.z, (double)P0.z);
+  const double e2x = __dsub_rn((double)P2.x, (double)P0.x);
+  const double e2y = __dsub_rn((double)P2.y, (double)P0.y);
+  const double e2z = __dsub_rn((double)P2.z, (double)P0.z);
+  const double e3x = __dsub_rn((double)P3.x, (double)P0.x);
+  const double e3y = __dsub_rn((double)P3.y, (double)P0.y);
+  const double e3z = __dsub_rn((double)P3.z, (double)P0.z);
+  return __dadd_rn(__dadd_rn(__dmul_rn(e1x, __dsub_rn(__dmul_rn(e2y, e3z), __dmul_rn(e2z, e3y))),
+                             __dmul_rn(e1y, __dsub_rn(__dmul_rn(e2z, e3x), __dmul_rn(e2x, e3z)))),
+                   __dmul_rn(e1z, __dsub_rn(__dmul_rn(e2x, e3y), __dmul_rn(e2y, e3x))));
+}
+
 // ----------------------------------------------------------------------------
 // Ray initialisation, _kernels.pyx:114-192.  Returns the selected slot.
 __device__ __forceinline__ int init_ray(const MeshView& m, float o0, float o1, float o2, float d0,
@@ -144,27 +167,20 @@ __device__ __forceinline__ int init_ray(const MeshView& m, float o0, float o1, f
   build_basis(o0, o1, o2, d0, d1, d2, b);
   const int4 qd = __ldg(&m.sv[start]);
   const int quad[4] = {qd.x, qd.y, qd.z, qd.w};
-  float4 P[4];
+  // the four start points from the ray's axis-permuted copy: already in
+  // projection order, no per-component selects
+  const float4* __restrict__ Pp = m.pts + (size_t)perm_index(b.mx, b.ot) * (size_t)m.n_points;
   float q2[8];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    P[i] = ldg_f4(&m.pts[quad[i]]);
-    project(b, P[i].x, P[i].y, P[i].z, q2[2 * i], q2[2 * i + 1]);
+    const float4 Q = ldg_f4(&Pp[quad[i]]);
+    q2[2 * i] = __fsub_rn(__fadd_rn(__fmul_rn(b.umax, Q.x), Q.y), b.pox);
+    q2[2 * i + 1] = __fsub_rn(
+        __fadd_rn(__fadd_rn(__fmul_rn(b.vmax, Q.x), __fmul_rn(b.voth, Q.y)), __fmul_rn(b.sgn, Q.z)), b.poy);
   }
-  const double e1x = __dsub_rn((double)P[1].x, (double)P[0].x);
-  const double e1y = __dsub_rn((double)P[1].y, (double)P[0].y);
-  const double e1z = __dsub_rn((double)P[1].z, (double)P[0].z);
-  const double e2x = __dsub_rn((double)P[2].x, (double)P[0].x);
-  const double e2y = __dsub_rn((double)P[2].y, (double)P[0].y);
-  const double e2z = __dsub_rn((double)P[2].z, (double)P[0].z);
-  const double e3x = __dsub_rn((double)P[3].x, (double)P[0].x);
-  const double e3y = __dsub_rn((double)P[3].y, (double)P[0].y);
-  const double e3z = __dsub_rn((double)P[3].z, (double)P[0].z);
-  const double rho = __dadd_rn(
-      __dadd_rn(__dmul_rn(e1x, __dsub_rn(__dmul_rn(e2y, e3z), __dmul_rn(e2z, e3y))),
-                __dmul_rn(e1y, __dsub_rn(__dmul_rn(e2z, e3x), __dmul_rn(e2x, e3z)))),
-      __dmul_rn(e1z, __dsub_rn(__dmul_rn(e2x, e3y), __dmul_rn(e2y, e3x))));
-  const bool rho_pos = rho > 0.0;
+  // sign of the fp64 orientation rho of the sorted quad (_kernels.pyx:133-147),
+  // precomputed per tet at upload (orient_kernel, identical arithmetic)
+  const bool rho_pos = __ldg(&m.orient[start]) != 0;
 
   int sel = -1, best_j = -1;
   float best_m = -3.4e38f;
@@ -323,8 +339,6 @@ __device__ __forceinline__ float4 fetch_vertex<80>(const MeshView&, const Record
 // k-th (mx, ot) pair, so one 16 B load delivers the components already in
 // projection order.  Copy 0 is (x, y, z): MeshView.pts[i] stays the plain
 // point for every other user.
-__device__ __forceinline__ int perm_index(int mx, int ot) { return mx * 2 + (ot > mx ? ot - 1 : ot); }
-
 __device__ __forceinline__ const float4* ray_points(const MeshView& m, const Basis& b) {
   return m.pts + (size_t)perm_index(b.mx, b.ot) * (size_t)m.n_points;
 }
