@@ -253,10 +253,10 @@ struct Record<16> {
   //   nref = prev ^ nx[order_a] (if != 3) ^ nx[rank] (if != 3).
   __device__ __forceinline__ uint32_t next_ref(const uint32_t (&idx)[3], uint32_t i3, uint32_t idxf,
                                                uint32_t prev) const {
-    const int rank = (idx[0] < idxf) + (idx[1] < idxf) + (idx[2] < idxf) + (i3 < idxf);
-    const int order_a = (idx[0] < i3) + (idx[1] < i3) + (idx[2] < i3);
     // nx[3] := 0 makes the "!= 3" xors unconditional
     const uint4 nx = make_uint4(r.y, r.z, r.w, 0u);
+    const int rank = (idx[0] < idxf) + (idx[1] < idxf) + (idx[2] < idxf) + (i3 < idxf);
+    const int order_a = (idx[0] < i3) + (idx[1] < i3) + (idx[2] < i3);
     return prev ^ pick4u(nx, order_a) ^ pick4u(nx, rank);
   }
 };
