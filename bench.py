@@ -39,8 +39,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    1: dict(grid=12, width=256, height=256, layout="tet20", scheme="none",
-            desc="cfg1: blob GRID=12 (11,029 tets), 256x256 primary rays"),
+    1: dict(grid=12, width=256, height=256, layout="tet80", walk="sctp", scheme="none",
+            desc="cfg1: blob GRID=12 (11,029 tets), 256x256 primary rays, TetMesh-80 + ScTP walk"),
     2: dict(grid=55, width=1920, height=1080, layout="tet20", scheme="hilbert",
             desc="cfg2: blob GRID=55 (1,109,444 tets), 1920x1080 primary rays, TetMesh-20 Hilbert-sorted"),
     3: dict(grid=55, width=3840, height=2160, layout="tet16", scheme="hilbert",
@@ -81,7 +81,8 @@ def build_scene(cfg):
     if "kuhn" in cfg:
         sc = kuhn_strip_scene(cfg["kuhn"], layout=cfg["layout"], scheme=cfg["scheme"])
     else:
-        sc = blob_scene(cfg["grid"], layout=cfg["layout"], scheme=cfg["scheme"], check=False)
+        host_layout = "tet32" if cfg["layout"] == "tet80" else cfg["layout"]
+        sc = blob_scene(cfg["grid"], layout=host_layout, scheme=cfg["scheme"], check=False)
     log(f"[bench] scene {sc.name}: {sc.mesh.n_tets} tets, {sc.mesh.n_points} points, "
         f"{sc.mesh.n_constrained} constrained faces, built in {time.perf_counter() - t0:.1f}s")
     return sc
@@ -263,7 +264,10 @@ def run_ours(args, cfg):
             dist.init_process_group(backend)
     sc = build_scene(cfg)
     mesh = sc.mesh
-    dm = device_mesh(mesh, device=local)
+    # tet80 has no host record dtype: the host mesh stays tet32 and the device
+    # builds the 80-byte records from the side tables
+    dm = device_mesh(mesh, device=local, layout=cfg["layout"] if cfg["layout"] == "tet80" else None)
+    sctp = cfg.get("walk") == "sctp"
     W, H = cfg["width"], cfg["height"]
     per_frame = W * H
 
@@ -301,7 +305,7 @@ def run_ours(args, cfg):
     gidx = torch.from_numpy(idx).to(dev)
 
     def step():
-        trace(dm, go, gd, gs, out=res, stream=stream)
+        trace(dm, go, gd, gs, out=res, stream=stream, sctp=sctp)
 
     # warm-up
     for _ in range(args.warmup):
@@ -335,7 +339,7 @@ def run_ours(args, cfg):
 
         stride = max(1, n // args.parity_sample)
         sl = slice(0, n, stride)
-        exp = pyoracle.cast_rays_full(mesh, o[sl], d[sl], st[sl])
+        exp = pyoracle.cast_rays_full(mesh, o[sl], d[sl], st[sl], layout=dm.layout, sctp=sctp)
         got = [x.cpu().numpy()[sl] for x in (res.status, res.cf, res.tet, res.visited, res.triangle, res.t,
                                               res.tet_back)]
         mism = int(sum(np.count_nonzero(a != b) for a, b in zip(got, exp)))
@@ -417,6 +421,11 @@ def run_ours(args, cfg):
                 (torch.uint8, torch.int32, torch.int32, torch.int32, torch.int32, torch.float64, torch.int32)]
 
         def host_call():
+            if sctp:  # the ScTP walk has no host-buffer C entry: protocol call (upload, launch, download)
+                from paper_2103_02309_b200 import kernels as K
+
+                K.cast_rays_full(dm, ho.numpy(), hd.numpy(), hs.numpy(), sctp=True)
+                return
             check(lib.tb_cast_rays_host(dm.handle, n, addr(ho), addr(hd), addr(hs), *[addr(x) for x in outs]),
                   "tb_cast_rays_host")
 
@@ -453,10 +462,10 @@ def run_ours(args, cfg):
         hres = TraceResult(*[torch.empty(W * H, dtype=dt).pin_memory() for dt in
                              (torch.uint8, torch.int32, torch.int32, torch.float64, torch.int32, torch.int32,
                               torch.int32)])
-        _, cam_tet = trace_camera(dm, cam, W, H, out=hres, stream=stream)  # camera located once
+        _, cam_tet = trace_camera(dm, cam, W, H, out=hres, stream=stream, sctp=sctp)  # camera located once
 
         def render_call():
-            trace_camera(dm, cam, W, H, out=hres, stream=stream, cam_tet=cam_tet)
+            trace_camera(dm, cam, W, H, out=hres, stream=stream, cam_tet=cam_tet, sctp=sctp)
             torch.cuda.synchronize()
 
         for _ in range(max(1, args.warmup)):
@@ -499,7 +508,8 @@ def run_ours(args, cfg):
         "wall_ms_per_step": wall / args.steps * 1e3,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": alg, "kernel": f"cast_kernel<{cfg['layout'][3:]}>"},
+                     "algorithmic_bytes_per_launch": alg,
+                     "kernel": f"{'sctp' if sctp else 'cast'}_kernel<{cfg['layout'][3:]}>"},
         "clocks": dict(clocks.summary(clocks.t_ramp, clocks.t_end), window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
         "gpu_launches": args.steps + (1 if world > 1 else 0),
         "parity": parity,
