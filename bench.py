@@ -304,8 +304,14 @@ def run_ours(args, cfg):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     gidx = torch.from_numpy(idx).to(dev)
 
+    # ray schedule: diffuse secondaries (config 4) are incoherent -> block
+    # compaction; primaries run one ray per lane.  TETB200_SCHED (sweeps)
+    # overrides through the process-wide "auto" setting.
+    schedule = args.schedule or ("auto" if os.environ.get("TETB200_SCHED") else
+                                 ("compact" if cfg.get("secondaries") else "lane"))
+
     def step():
-        trace(dm, go, gd, gs, out=res, stream=stream, sctp=sctp)
+        trace(dm, go, gd, gs, out=res, stream=stream, sctp=sctp, schedule=schedule)
 
     # warm-up
     for _ in range(args.warmup):
@@ -498,6 +504,7 @@ def run_ours(args, cfg):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg["desc"], "rays_per_gpu": n, "layout": cfg["layout"], "scheme": cfg["scheme"],
                    "parallelism": f"tile-shard x{world}, mesh replicated", "l2": "flushed between steps (256 MiB)",
+                   "schedule": schedule,
                    "frames": world},
         "tets_visited_per_ray": {"mean": vis_sum / total_rays, "max": vis_max},
         "kernel_ms": {"mean": float(kernel_ms.mean()), "min": float(kernel_ms.min()), "max": float(kernel_ms.max())},
@@ -547,6 +554,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--layout", default=None)
     ap.add_argument("--scheme", default=None)
+    ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512"),
+                    help="ray-to-lane schedule of the timed trace (default: compact for secondaries, else lane)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2_073_600)

@@ -105,6 +105,15 @@ int tb_mesh_info(const tb_mesh* mesh, int* device, int* layout, int64_t* n_point
 int tb_cast_rays(tb_mesh* mesh, int64_t n, const float* o, const float* d, const int32_t* start,
                  uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle,
                  double* t, int32_t* tet_back, void* stream);
+/* tb_cast_rays with an explicit per-call ray schedule (tb_set_schedule's
+ * modes; 0 = the process-wide setting).  Results are identical in every
+ * mode.  Block compaction (3 / 4) is the faster choice for incoherent batches
+ * (diffuse secondaries: rays starting all over the mesh), one ray per lane
+ * (1) for coherent primaries and for tb_cast_rays_host, whose zero-copy path
+ * is PCIe-bound and relies on one-ray-per-lane coalesced ray loads. */
+int tb_cast_rays_sched(tb_mesh* mesh, int64_t n, const float* o, const float* d, const int32_t* start,
+                       uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle,
+                       double* t, int32_t* tet_back, int schedule, void* stream);
 int tb_cast_rays_host(tb_mesh* mesh, int64_t n, const float* o, const float* d,
                       const int32_t* start, uint8_t* status, int32_t* cf, int32_t* tet,
                       int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back);
@@ -168,6 +177,19 @@ int tb_sctp_cast_rays(tb_mesh* mesh, int64_t n, const float* o, const float* d,
                       const int32_t* start, uint8_t* status, int32_t* cf, int32_t* tet,
                       int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back,
                       void* stream);
+
+/* Ray scheduling of tb_cast_rays / tb_cast_rays_host (no reference
+ * counterpart: the reference walks one ray per loop iteration,
+ * _kernels.pyx:343-369).  Results are identical in every mode; only the
+ * mapping of rays to lanes changes.
+ *   mode 0 = auto (= one ray per lane), 1 = one ray per lane, 2 = per-lane
+ *   persistent refill,
+ *   3 / 4 = block compaction (256 / 512 threads per block) for incoherent
+ *   batches; steps_per_round = walk steps between compactions (>= 1).
+ * Process-wide; overrides TETB200_SCHED / TETB200_ROUND.  A negative
+ * argument leaves that setting unchanged. */
+int tb_set_schedule(int mode, int steps_per_round);
+int tb_get_schedule(int* mode, int* steps_per_round);
 
 /* Pinned host memory helpers for end-to-end callers. */
 int tb_host_alloc(size_t bytes, void** out);

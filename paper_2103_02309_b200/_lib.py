@@ -38,6 +38,7 @@ _SIGS = {
          POINTER(c_int64), POINTER(c_int64)],
     ),
     "tb_cast_rays": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),
+    "tb_cast_rays_sched": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_int, c_void_p]),
     "tb_cast_rays_host": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P]),
     "tb_sctp_cast_rays": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),
     "tb_cast_rays_visits": (c_int, [c_void_p, c_int64, P, P, P, P, P, c_void_p]),
@@ -47,6 +48,8 @@ _SIGS = {
     "tb_locate_points_host": (c_int, [c_void_p, c_int64, P, P, P, P]),
     "tb_shadow_rays": (c_int, [c_void_p, c_int64, P, P, c_int, P, P, c_int, c_double, P, P, c_void_p]),
     "tb_shadow_rays_host": (c_int, [c_void_p, c_int64, P, P, c_int, P, P, c_int, c_double, P, P]),
+    "tb_set_schedule": (c_int, [c_int, c_int]),
+    "tb_get_schedule": (c_int, [POINTER(c_int), POINTER(c_int)]),
     "tb_host_alloc": (c_int, [c_size_t, POINTER(c_void_p)]),
     "tb_host_free": (c_int, [c_void_p]),
 }
@@ -70,6 +73,22 @@ def check(code: int, what: str) -> None:
     if code != 0:
         msg = lib.tb_last_error()
         raise TetB200Error(f"{what} failed ({code}): {msg.decode() if msg else 'unknown error'}")
+
+
+SCHEDULES = {"auto": 0, "lane": 1, "refill": 2, "compact": 3, "compact512": 4}
+
+
+def set_schedule(mode: str | int | None = None, steps_per_round: int | None = None) -> None:
+    """Process-wide ray-to-lane schedule of the cast kernels (tb_set_schedule).
+    Results are identical in every mode."""
+    m = -1 if mode is None else (SCHEDULES[mode] if isinstance(mode, str) else int(mode))
+    check(lib.tb_set_schedule(m, -1 if steps_per_round is None else int(steps_per_round)), "tb_set_schedule")
+
+
+def get_schedule() -> tuple[int, int]:
+    m, k = c_int(), c_int()
+    check(lib.tb_get_schedule(ctypes.byref(m), ctypes.byref(k)), "tb_get_schedule")
+    return m.value, k.value
 
 
 def addr(a) -> int | None:

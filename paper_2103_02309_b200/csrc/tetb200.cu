@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -383,6 +384,167 @@ __global__ void __launch_bounds__(kBlock) cast_persist_kernel(
   }
 }
 
+// ----------------------------------------------------------------------------
+// Block-compacting persistent variant, for divergent (incoherent) batches.
+//
+// The per-lane refill above loses because every refill runs init_ray with
+// only the idle lanes of a warp active, so init is paid at a fraction of
+// SIMT width over and over.  Here the unit of scheduling is the block:
+// every round each walking lane takes up to `rounds` steps, then the block
+// compacts its surviving rays into the lowest thread slots through shared
+// memory (20 words of walk state per ray, SoA so the exchange is
+// bank-conflict free) and refills the free tail slots -- whole warps plus
+// at most one partial warp -- with fresh rays, which therefore initialise at
+// (nearly) full SIMT width.  Walking warps stay dense until the block's ray
+// stream runs dry; then survivors concentrate in the fewest warps and the
+// emptied warps only wait at the barriers.  Per-ray results are identical to
+// cast_kernel: same init_ray / advance / long_walk / write_result code, and
+// a ray's step sequence does not depend on which lane walks it.
+//
+// Rays are dealt to blocks in 32-ray chunks round-robin (chunk c -> block
+// c mod gridDim), so every block sees the whole image/batch and the tail is
+// balanced without atomics or per-call scratch.
+constexpr int kCompactWords = 20;
+
+template <int L, int BT>
+__global__ void __launch_bounds__(BT) cast_compact_kernel(
+    MeshView m, int64_t n, const float* __restrict__ o, const float* __restrict__ d,
+    const int32_t* __restrict__ start, uint8_t* __restrict__ status, int32_t* __restrict__ cf,
+    int32_t* __restrict__ tet, int32_t* __restrict__ visited, int32_t* __restrict__ triangle,
+    double* __restrict__ t, int32_t* __restrict__ tet_back, int steps_per_round) {
+  constexpr int NW = BT / 32;
+  __shared__ uint32_t sw[kCompactWords][BT];
+  __shared__ int warp_cnt[NW];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t G = gridDim.x;
+  const int64_t n_chunks = (n + 31) >> 5;
+  const int64_t my_chunks = n_chunks > (int64_t)blockIdx.x ? (n_chunks - 1 - blockIdx.x) / G + 1 : 0;
+  const int64_t stream_len = my_chunks * 32;
+  const uint32_t n_tets = (uint32_t)m.n_tets;
+  const uint32_t fast_limit = n_tets < kCycleCheckAfter ? n_tets : kCycleCheckAfter;
+
+  int64_t qpos = 0;  // block-uniform position in this block's ray stream
+  int A = 0;         // block-uniform: threads [0, A) hold a walking ray
+  bool has = false;
+  uint32_t r = 0;
+  Basis b;
+  b.mn = b.mx = b.ot = 0;
+  b.umax = b.vmax = b.voth = b.sgn = b.pox = b.poy = 0.f;
+  int perm = 0;
+  uint32_t idx[3] = {0, 0, 0};
+  float p[6] = {0, 0, 0, 0, 0, 0};
+  uint32_t ref = 0, cur = 0;
+  int vis = 0;
+  while (true) {
+    // refill: free slots [A, BT) take the next rays of the block's stream
+    if (tid >= A) {
+      const int64_t q = qpos + (tid - A);
+      if (q < stream_len) {
+        const int64_t rr = (blockIdx.x + (q >> 5) * G) * 32 + (q & 31);
+        if (rr < n) {
+          r = (uint32_t)rr;
+          const float o0 = __ldg(o + 3 * rr), o1 = __ldg(o + 3 * rr + 1), o2 = __ldg(o + 3 * rr + 2);
+          const float d0 = __ldg(d + 3 * rr), d1 = __ldg(d + 3 * rr + 1), d2 = __ldg(d + 3 * rr + 2);
+          cur = (uint32_t)__ldg(start + rr);
+          const int j = init_ray(m, o0, o1, o2, d0, d1, d2, (int)cur, b, idx, p);
+          ref = pick4u(__ldg(&m.sn[cur]), j);
+          perm = perm_index(b.mx, b.ot);
+          vis = 1;
+          has = true;
+        }
+      }
+    }
+    qpos += BT - A;
+    // walk: up to steps_per_round steps per lane
+    if (has) {
+      const float4* __restrict__ P = m.pts + (size_t)perm * (size_t)m.n_points;
+      bool done = false, guard = false;
+#pragma unroll 1
+      for (int s = 0; s < steps_per_round; ++s) {
+        if (ref >= n_tets) { done = true; break; }
+        const uint32_t nxt = ref;
+        ref = advance<L>(m, P, b, idx, p, nxt, cur);
+        cur = nxt;
+        if ((uint32_t)++vis > fast_limit) {
+          guard = (uint32_t)vis > n_tets || long_walk<L>(m, P, b, idx, p, ref, cur, vis);
+          done = true;
+          break;
+        }
+      }
+      if (!done && ref >= n_tets) done = true;
+      if (done) {
+        const uint8_t st = guard ? kError : ((ref == kBoundary) ? kMiss : ((ref & kConstrained) ? kHit : kError));
+        const float o0 = __ldg(o + 3 * (int64_t)r), o1 = __ldg(o + 3 * (int64_t)r + 1),
+                    o2 = __ldg(o + 3 * (int64_t)r + 2);
+        const float d0 = __ldg(d + 3 * (int64_t)r), d1 = __ldg(d + 3 * (int64_t)r + 1),
+                    d2 = __ldg(d + 3 * (int64_t)r + 2);
+        write_result(m, r, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
+                     tet_back);
+        has = false;
+      }
+    }
+    // compaction: survivors move to slots [0, total)
+    const unsigned bal = __ballot_sync(0xffffffffu, has);
+    if (lane == 0) warp_cnt[wid] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const int c = warp_cnt[w];
+      before += (w < wid) ? c : 0;
+      total += c;
+    }
+    if (total == 0 && qpos >= stream_len) break;
+    const int slot = before + __popc(bal & ((1u << lane) - 1u));
+    const bool move_out = has && slot != tid;
+    if (move_out) {
+      sw[0][slot] = r;
+      sw[1][slot] = __float_as_uint(b.umax);
+      sw[2][slot] = __float_as_uint(b.vmax);
+      sw[3][slot] = __float_as_uint(b.voth);
+      sw[4][slot] = __float_as_uint(b.sgn);
+      sw[5][slot] = __float_as_uint(b.pox);
+      sw[6][slot] = __float_as_uint(b.poy);
+      sw[7][slot] = (uint32_t)perm;
+      sw[8][slot] = idx[0];
+      sw[9][slot] = idx[1];
+      sw[10][slot] = idx[2];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) sw[11 + k][slot] = __float_as_uint(p[k]);
+      sw[17][slot] = ref;
+      sw[18][slot] = cur;
+      sw[19][slot] = (uint32_t)vis;
+    }
+    __syncthreads();
+    // a slot keeps its registers when its own ray stayed in place
+    const bool stay = has && slot == tid;
+    if (tid < total && !stay) {
+      r = sw[0][tid];
+      b.umax = __uint_as_float(sw[1][tid]);
+      b.vmax = __uint_as_float(sw[2][tid]);
+      b.voth = __uint_as_float(sw[3][tid]);
+      b.sgn = __uint_as_float(sw[4][tid]);
+      b.pox = __uint_as_float(sw[5][tid]);
+      b.poy = __uint_as_float(sw[6][tid]);
+      perm = (int)sw[7][tid];
+      // the axes, for project() (TetMesh-80 reads inline xyz): invert perm_index
+      b.mx = perm >> 1;
+      b.ot = ((perm & 1) >= b.mx) ? (perm & 1) + 1 : (perm & 1);
+      b.mn = 3 - b.mx - b.ot;
+      idx[0] = sw[8][tid];
+      idx[1] = sw[9][tid];
+      idx[2] = sw[10][tid];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) p[k] = __uint_as_float(sw[11 + k][tid]);
+      ref = sw[17][tid];
+      cur = sw[18][tid];
+      vis = (int)sw[19][tid];
+    }
+    has = tid < total;
+    A = total;
+  }
+}
+
 // Visit-sequence recorder (second pass; offsets from a prior cast), _kernels.pyx:307-341.
 template <int L>
 __global__ void __launch_bounds__(kBlock) visits_kernel(MeshView m, int64_t n, const float* __restrict__ o,
@@ -731,14 +893,62 @@ struct CastPersistL {
 };
 
 // TETB200_SCHED: 0 = auto, 1 = one ray per lane (cast_kernel), 2 = persistent
-// refill (cast_persist_kernel).
+// refill (cast_persist_kernel), 3 / 4 = block compaction with 256 / 512
+// threads (cast_compact_kernel).  TETB200_ROUND: steps per compaction round.
+std::atomic<int> g_sched_mode{-1}, g_round_steps{-1};
 int sched_mode() {
-  static int mode = -1;
+  int mode = g_sched_mode.load(std::memory_order_relaxed);
   if (mode < 0) {
     const char* v = getenv("TETB200_SCHED");
     mode = v ? atoi(v) : 0;
+    if (mode < 0 || mode > 4) mode = 0;
+    int expect = -1;
+    g_sched_mode.compare_exchange_strong(expect, mode);
+    mode = g_sched_mode.load();
   }
   return mode;
+}
+int round_steps() {
+  int k = g_round_steps.load(std::memory_order_relaxed);
+  if (k < 0) {
+    const char* v = getenv("TETB200_ROUND");
+    k = v ? atoi(v) : 32;  // r01 sweep, config 4: 8 / 16 / 32 / 48 / 64 -> best at 32
+    if (k < 1) k = 1;
+    int expect = -1;
+    g_round_steps.compare_exchange_strong(expect, k);
+    k = g_round_steps.load();
+  }
+  return k;
+}
+template <int L, int BT>
+struct CastCompactL {
+  // grid: one full wave of resident blocks (or fewer for small batches)
+  template <typename... A>
+  static void launch(int64_t n, cudaStream_t s, A... a) {
+    static int per_sm = 0, sms = 0;
+    if (per_sm == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cast_compact_kernel<L, BT>, BT, 0);
+      if (per_sm < 1) per_sm = 1;
+    }
+    const int64_t full = (int64_t)per_sm * sms;
+    const int64_t chunks = (n + 31) / 32;
+    const unsigned g = (unsigned)(chunks < full ? chunks : full);
+    cast_compact_kernel<L, BT><<<g, BT, 0, s>>>(a..., round_steps());
+  }
+};
+template <int BT, typename... A>
+int launch_compact(int layout, int64_t n, cudaStream_t s, A... a) {
+  switch (layout) {
+    case 16: CastCompactL<16, BT>::launch(n, s, a...); break;
+    case 20: CastCompactL<20, BT>::launch(n, s, a...); break;
+    case 32: CastCompactL<32, BT>::launch(n, s, a...); break;
+    case 80: CastCompactL<80, BT>::launch(n, s, a...); break;
+    default: return set_error(TB_E_LAYOUT, "unsupported layout %d", layout);
+  }
+  return TB_OK;
 }
 template <int L>
 struct VisitsL {
@@ -765,6 +975,31 @@ int check_mesh(const tb_mesh* m) {
   if (m == nullptr) return set_error(TB_E_ARG, "mesh handle is NULL");
   return TB_OK;
 }
+
+// Launch the traversal with an explicit schedule (see sched_mode).
+int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start, uint8_t* status,
+                  int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back,
+                  cudaStream_t s, int mode) {
+  DeviceGuard g(m->device);
+  const MeshView v = m->view();
+  int e = TB_OK;
+  if ((mode == 3 || mode == 4) && n < (int64_t)1 << 32) {
+    e = mode == 3 ? launch_compact<256>(m->layout, n, s, v, n, o, d, start, status, cf, tet, visited, triangle, t,
+                                        tet_back)
+                  : launch_compact<512>(m->layout, n, s, v, n, o, d, start, status, cf, tet, visited, triangle, t,
+                                        tet_back);
+  } else if (mode == 2) {
+    e = launch_layout<CastPersistL>(m->layout, grid_for(n, kBlock), s, v, n, o, d, start, status, cf, tet, visited,
+                                    triangle, t, tet_back);
+  } else {
+    e = launch_layout<CastL>(m->layout, grid_for(n, kBlock), s, v, n, o, d, start, status, cf, tet, visited,
+                             triangle, t, tet_back);
+  }
+  if (e) return e;
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
 
 // Stream-ordered scratch for the *_host entry points.
 struct Scratch {
@@ -925,16 +1160,23 @@ int tb_cast_rays(tb_mesh* m, int64_t n, const float* o, const float* d, const in
   if (n < 0) return set_error(TB_E_ARG, "negative ray count");
   if (n == 0) return TB_OK;
   if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
-  DeviceGuard g(m->device);
-  const cudaStream_t s = (cudaStream_t)stream;
-  const bool persist = sched_mode() == 2;
-  if (int e = persist ? launch_layout<CastPersistL>(m->layout, grid_for(n, kBlock), s, m->view(), n, o, d, start,
-                                                    status, cf, tet, visited, triangle, t, tet_back)
-                      : launch_layout<CastL>(m->layout, grid_for(n, kBlock), s, m->view(), n, o, d, start, status,
-                                             cf, tet, visited, triangle, t, tet_back))
-    return e;
-  TB_CUDA(cudaGetLastError());
-  return TB_OK;
+  // device pointers: auto = one ray per lane (deciding coherence would need
+  // a host round trip; callers that know their batch is incoherent select
+  // compaction with tb_set_schedule)
+  return cast_dispatch(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, (cudaStream_t)stream,
+                       sched_mode());
+}
+
+int tb_cast_rays_sched(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
+                       uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t,
+                       int32_t* tet_back, int schedule, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  if (schedule < 0 || schedule > 4) return set_error(TB_E_ARG, "schedule %d not in 0..4", schedule);
+  if (n == 0) return TB_OK;
+  if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
+  return cast_dispatch(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, (cudaStream_t)stream,
+                       schedule == 0 ? sched_mode() : schedule);
 }
 
 int tb_sctp_cast_rays(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
@@ -1127,6 +1369,13 @@ int tb_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, con
   PipeCtx* ctx = nullptr;
   if (int e = pipe_ctx(m->device, &ctx)) return e;
   const int mode = e2e_mode();
+  // Host batches run one ray per lane unless a schedule is set: the walk
+  // hides under PCIe time here, and the zero-copy path depends on
+  // cast_kernel's warp-cooperative coalesced ray loads (r01: config 4 e2e
+  // 1354 Mrays/s zero-copy lane vs 1156 staged compaction; zero-copy
+  // compaction, whose refills and epilogue read rays lane by lane over
+  // PCIe, 64 Mrays/s).
+  const int sched = sched_mode();
   // Zero-copy path: when every buffer is mapped pinned host memory
   // (cudaHostAlloc / torch pin_memory under UVA), the trace kernel reads the
   // rays and writes the hits straight over PCIe -- one launch, no staging
@@ -1138,9 +1387,9 @@ int tb_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, con
   const bool ins_mapped = mapped_ptr(o, &dO) && mapped_ptr(d, &dD) && mapped_ptr(start, &dS);
   if (mode == 0 && outs_mapped && ins_mapped) {
     const cudaStream_t s = ctx->slot[0].s;
-    if (int e = tb_cast_rays(m, n, (const float*)dO, (const float*)dD, (const int32_t*)dS, (uint8_t*)dSt,
-                             (int32_t*)dCf, (int32_t*)dTet, (int32_t*)dVis, (int32_t*)dTri, (double*)dT,
-                             (int32_t*)dBack, s))
+    if (int e = cast_dispatch(m, n, (const float*)dO, (const float*)dD, (const int32_t*)dS, (uint8_t*)dSt,
+                              (int32_t*)dCf, (int32_t*)dTet, (int32_t*)dVis, (int32_t*)dTri, (double*)dT,
+                              (int32_t*)dBack, s, sched))
       return e;
     TB_CUDA(cudaStreamSynchronize(s));
     return TB_OK;
@@ -1163,14 +1412,14 @@ int tb_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, con
     TB_CUDA(cudaMemcpyAsync(sl.st, start + c0, uk * 4, cudaMemcpyHostToDevice, s));
     if (outs_mapped && mode == 2) {
       // inputs by copy engine, hits written by the kernel straight to host
-      if (int e = tb_cast_rays(m, k, sl.o, sl.d, sl.st, (uint8_t*)dSt + c0, (int32_t*)dCf + c0,
-                               (int32_t*)dTet + c0, (int32_t*)dVis + c0, dTri ? (int32_t*)dTri + c0 : nullptr,
-                               dT ? (double*)dT + c0 : nullptr, dBack ? (int32_t*)dBack + c0 : nullptr, s))
+      if (int e = cast_dispatch(m, k, sl.o, sl.d, sl.st, (uint8_t*)dSt + c0, (int32_t*)dCf + c0,
+                                (int32_t*)dTet + c0, (int32_t*)dVis + c0, dTri ? (int32_t*)dTri + c0 : nullptr,
+                                dT ? (double*)dT + c0 : nullptr, dBack ? (int32_t*)dBack + c0 : nullptr, s, sched))
         return e;
       continue;
     }
-    if (int e = tb_cast_rays(m, k, sl.o, sl.d, sl.st, sl.status, sl.cf, sl.tet, sl.vis, triangle ? sl.tri : nullptr,
-                             t ? sl.t : nullptr, tet_back ? sl.back : nullptr, s))
+    if (int e = cast_dispatch(m, k, sl.o, sl.d, sl.st, sl.status, sl.cf, sl.tet, sl.vis, triangle ? sl.tri : nullptr,
+                              t ? sl.t : nullptr, tet_back ? sl.back : nullptr, s, sched))
       return e;
     TB_CUDA(cudaMemcpyAsync(status + c0, sl.status, uk, cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaMemcpyAsync(cf + c0, sl.cf, uk * 4, cudaMemcpyDeviceToHost, s));
@@ -1238,6 +1487,20 @@ int tb_shadow_rays_host(tb_mesh* m, int64_t n, const double* p, const double* li
   TB_CUDA(cudaMemcpyAsync(occluded, dOcc, un, cudaMemcpyDeviceToHost, hc.s));
   TB_CUDA(cudaMemcpyAsync(visited, dV, un * 4, cudaMemcpyDeviceToHost, hc.s));
   TB_CUDA(cudaStreamSynchronize(hc.s));
+  return TB_OK;
+}
+
+int tb_set_schedule(int mode, int steps_per_round) {
+  if (mode > 4) return set_error(TB_E_ARG, "schedule mode %d not in 0..4", mode);
+  if (steps_per_round == 0) return set_error(TB_E_ARG, "steps_per_round must be >= 1");
+  if (mode >= 0) g_sched_mode.store(mode);
+  if (steps_per_round > 0) g_round_steps.store(steps_per_round);
+  return TB_OK;
+}
+
+int tb_get_schedule(int* mode, int* steps_per_round) {
+  if (mode) *mode = sched_mode();
+  if (steps_per_round) *steps_per_round = round_steps();
   return TB_OK;
 }
 

@@ -13,7 +13,7 @@ from dataclasses import dataclass
 
 import torch
 
-from ._lib import addr, check, lib
+from ._lib import SCHEDULES, addr, check, lib
 from .device import DeviceMesh, device_mesh
 
 
@@ -57,24 +57,32 @@ def _check_inputs(dm: DeviceMesh, origins, dirs, start):
 
 def trace(mesh, origins: torch.Tensor, dirs: torch.Tensor, start: torch.Tensor, *, out: TraceResult | None = None,
           stream: torch.cuda.Stream | None = None, epilogue: bool = True, sctp: bool = False,
-          layout: str | None = None) -> TraceResult:
+          layout: str | None = None, schedule: str | int = "auto") -> TraceResult:
     """Trace rays on the GPU; returns hit triangle id, t and terminating tet.
 
     ``sctp=True`` runs the fp64 scalar-triple-product fallback walk instead
-    of the 2-D modified-basis walk.  Start tets are not range-checked here
-    (device inputs stay on the device); ``kernels.cast_rays`` checks them.
+    of the 2-D modified-basis walk.  ``schedule`` maps rays to lanes (results
+    are identical either way): "lane" suits coherent primaries, "compact"
+    (block compaction) incoherent batches such as diffuse secondaries;
+    "auto" uses the process-wide setting (default: "lane" -- deciding from
+    device-resident start tets would need a host round trip).  Start tets
+    are not range-checked here (device inputs stay on the device);
+    ``kernels.cast_rays`` checks them.
     """
     dm = device_mesh(mesh, device=origins.device.index, layout=layout)
     n = _check_inputs(dm, origins, dirs, start)
     res = out if out is not None else empty_result(n, origins.device)
     s = (stream or torch.cuda.current_stream(origins.device)).cuda_stream
-    fn = lib.tb_sctp_cast_rays if sctp else lib.tb_cast_rays
-    check(
-        fn(dm.handle, n, addr(origins), addr(dirs), addr(start), addr(res.status), addr(res.cf), addr(res.tet),
-           addr(res.visited), addr(res.triangle) if epilogue else None, addr(res.t) if epilogue else None,
-           addr(res.tet_back) if epilogue else None, s),
-        "tb_sctp_cast_rays" if sctp else "tb_cast_rays",
-    )
+    tri = addr(res.triangle) if epilogue else None
+    tt = addr(res.t) if epilogue else None
+    back = addr(res.tet_back) if epilogue else None
+    ins = (dm.handle, n, addr(origins), addr(dirs), addr(start), addr(res.status), addr(res.cf), addr(res.tet),
+           addr(res.visited), tri, tt, back)
+    if sctp:
+        check(lib.tb_sctp_cast_rays(*ins, s), "tb_sctp_cast_rays")
+    else:
+        mode = SCHEDULES[schedule] if isinstance(schedule, str) else int(schedule)
+        check(lib.tb_cast_rays_sched(*ins, mode, s), "tb_cast_rays_sched")
     return res
 
 

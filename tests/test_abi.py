@@ -78,3 +78,31 @@ def test_no_oracle_import_in_product():
     for p in (ROOT / "paper_2103_02309_b200").rglob("*.py"):
         src = p.read_text()
         assert "import oracle" not in src and "from oracle" not in src, p
+
+
+def test_schedule_setter_roundtrip_and_validation():
+    from paper_2103_02309_b200 import _lib
+
+    mode0, k0 = _lib.get_schedule()
+    try:
+        _lib.set_schedule("compact", 8)
+        assert _lib.get_schedule() == (3, 8)
+        _lib.set_schedule(None, 24)  # leaves the mode alone
+        assert _lib.get_schedule() == (3, 24)
+        with pytest.raises(_lib.TetB200Error):
+            _lib.set_schedule(9)
+        assert _lib.lib.tb_set_schedule(-1, 0) != 0
+        assert _lib.get_schedule() == (3, 24)
+    finally:
+        _lib.set_schedule(mode0, k0)
+
+
+def test_cast_rays_sched_validates_arguments():
+    from paper_2103_02309_b200._lib import lib
+
+    args = (None,) * 10
+    assert lib.tb_cast_rays_sched(None, 1, *args, 0, None) == -1
+    assert b"NULL" in lib.tb_last_error()
+    fake = ctypes.c_void_p(1)  # never dereferenced: the schedule is checked first
+    assert lib.tb_cast_rays_sched(fake, 1, *args, 9, None) == -1
+    assert b"schedule" in lib.tb_last_error()

@@ -335,3 +335,114 @@ def test_trace_torch_api(golden):
     got = (res.status, res.cf, res.tet, res.visited, res.triangle, res.t, res.tet_back)
     for k, a, b in zip(NAMES7, got, exp):
         assert np.array_equal(a.cpu().numpy(), b), k
+
+
+@pytest.fixture
+def schedule():
+    from paper_2103_02309_b200 import _lib
+
+    saved = _lib.get_schedule()
+    yield _lib.set_schedule
+    _lib.set_schedule(*saved)
+
+
+@pytest.mark.parametrize("mode,rounds", [("lane", 16), ("refill", 16), ("compact", 1), ("compact", 7),
+                                          ("compact", 16), ("compact512", 32)])
+@pytest.mark.parametrize("layout", LAYOUTS4)
+def test_schedules_identical_results(golden, digests, K, O, schedule, mode, rounds, layout):
+    """Every ray-to-lane schedule (one ray per lane, per-lane refill, block
+    compaction at several round lengths) gives the reference's results bit
+    for bit: golden fixtures, incoherent random rays, and a ragged batch."""
+    schedule(mode, rounds)
+    for name in ("pane4", "model"):
+        base = golden_mesh(golden, name, "tet20" if layout == "tet80" else layout)
+        o, d, st = _rays(base, name)
+        out = K.cast_rays_full(base, o, d, st, layout=layout)
+        ref_layout = "tet32" if layout == "tet80" else layout
+        assert digest(*out[:4]) == digests[f"{name}/{ref_layout}/cast10k"]
+        assert digest(*out[4:]) == digests[f"{name}/{ref_layout}/cast10k_epilogue"]
+        # ragged: not a multiple of 32 / of the block, fewer rays than one block
+        for n in (1, 33, 257, 4099):
+            got = K.cast_rays_full(base, o[:n], d[:n], st[:n], layout=layout)
+            for k, a, b in zip(NAMES7, got, out):
+                assert np.array_equal(a, b[:n]), (k, n)
+
+
+@pytest.mark.parametrize("mode", ("compact", "compact512", "refill"))
+def test_schedules_cycle_guard(digests, K, O, schedule, mode):
+    """Guard rays (status 2, visited = n_tets + 1) through the compacting
+    scheduler, on the lattice camera and on the Brent fast-forward mesh."""
+    from paper_2103_02309_b200.ingestion import build_box_fixture, build_kuhn_box
+    from paper_2103_02309_b200.scenes import camera_rays
+    from paper_2103_02309_b200.tetmesh import encode
+
+    schedule(mode, 5)
+    raw, soup = build_box_fixture(8, occluders=[(0, 4, (2, 2), (6, 6))])
+    m = encode(raw, "tet20", soup)
+    o, d = camera_rays((4.0, 4.0, 0.5), (4.0, 4.0, 8.0), (0.0, 1.0, 0.0), 68.0, 1024, 1024)
+    st = np.full(len(o), digests["lattice8/cam_tet"], np.int32)
+    out = K.cast_rays(m, o, d, st)
+    assert digest(*out) == digests["lattice8/cast"]
+    raw, soup = build_kuhn_box(16, [(0, 8, (4, 4), (12, 12))])
+    m = encode(raw, "tet16", soup)
+    o, d = camera_rays((8.0, 8.0, 0.5), (8.0, 8.0, 16.0), (0.0, 1.0, 0.0), 68.0, 512, 512)
+    cam, _ = O.locate_points(m, np.array([[8.0, 8.0, 0.5]]), np.array([0], np.int32))
+    st = np.full(len(o), cam[0], np.int32)
+    got = K.cast_rays_full(m, o, d, st)
+    exp = O.cast_rays_full(m, o, d, st)
+    for k, a, b in zip(NAMES7, got, exp):
+        assert np.array_equal(a, b), k
+
+
+@pytest.mark.parametrize("schedule", ("lane", "refill", "compact", "compact512"))
+def test_trace_schedule_argument(golden, K, O, schedule):
+    """trace(schedule=...) on device tensors (tb_cast_rays_sched) equals the
+    oracle for an incoherent batch larger than one wave of blocks."""
+    import torch
+
+    from paper_2103_02309_b200.scenes import interior_rays
+    from paper_2103_02309_b200.trace import trace
+
+    m = golden_mesh(golden, "model", "tet16")
+    o, d, st = interior_rays(m, 300_000, 11)
+    dev = torch.device("cuda", 0)
+    res = trace(m, *(torch.from_numpy(a).to(dev) for a in (o, d, st)), schedule=schedule)
+    exp = O.cast_rays_full(m, o, d, st)
+    got = (res.status, res.cf, res.tet, res.visited, res.triangle, res.t, res.tet_back)
+    for k, a, b in zip(NAMES7, got, exp):
+        assert np.array_equal(a.cpu().numpy(), b), k
+
+
+@pytest.mark.parametrize("mode", ("auto", "compact"))
+def test_host_path_coherent_and_incoherent(golden, K, O, schedule, mode):
+    """tb_cast_rays_host on a camera batch (one start tet) and an incoherent
+    batch: both equal the oracle, with pinned (zero-copy) and pageable
+    buffers, under the default and the compacting schedule."""
+    from paper_2103_02309_b200.scenes import camera_rays, interior_rays
+
+    schedule(mode, 32)
+    m = golden_mesh(golden, "model", "tet20")
+    o, d, st = interior_rays(m, 100_000, 12)
+    cam = np.asarray(o[0], np.float64)
+    oc, dc = camera_rays(tuple(cam), (0.5, 0.5, 0.5), (0.0, 1.0, 0.0), 60.0, 320, 200)
+    stc = np.full(len(oc), st[0], np.int32)
+    import torch
+
+    from paper_2103_02309_b200._lib import addr, check, lib
+    from paper_2103_02309_b200.device import device_mesh
+
+    dm = device_mesh(m)
+    for oo, dd, ss in ((o, d, st), (oc, dc, stc)):
+        exp = O.cast_rays_full(m, oo, dd, ss)
+        got = K.cast_rays_full(m, oo, dd, ss)  # pageable: staged copies
+        for k, a, b in zip(NAMES7, got, exp):
+            assert np.array_equal(a, b), k
+        # pinned: the zero-copy path (kernel reads rays / writes hits over PCIe)
+        n = len(ss)
+        pin = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (oo, dd, ss)]
+        outs = [torch.empty(n, dtype=dt).pin_memory() for dt in (torch.uint8, torch.int32, torch.int32, torch.int32,
+                                                                  torch.int32, torch.float64, torch.int32)]
+        check(lib.tb_cast_rays_host(dm.handle, n, *(addr(x) for x in pin), *(addr(x) for x in outs)),
+              "tb_cast_rays_host")
+        for k, a, b in zip(NAMES7, outs, exp):
+            assert np.array_equal(a.numpy(), b), (k, "pinned")
