@@ -239,13 +239,17 @@ __device__ __forceinline__ int init_ray(const MeshView& m, float o0, float o1, f
 template <int L>
 struct Record;
 
-// (Tried and measured slower, r01: moving the rank compares to the FMA pipe
-// as IMAD/IMAD.HI sign tricks -- fewer ALU ops but a longer dependent chain;
-// cfg2 -4 %, cfg4 -10 %.  The compares stay ISETP.)
+// (r01: ranks as IMAD/IMAD.HI sign products measured slower -- a longer
+// dependent chain; the sign-bit sums of decide<L> compile to IMAD.IADD +
+// LEA.HI pairs instead and are faster, see profiles/r01_experiments.md.)
 
+// next_ref: the exit reference given the exited vertex idxf (Alg. 3/5/7).
+// The 2-D walk computes it inside decide<L> (PTX, below) together with
+// Algorithm 1 and the window update; these C++ forms serve the ScTP walk,
+// which picks idxf with the fp64 predicate instead.
 template <>
 struct Record<16> {
-  uint4 r;
+  uint4 r;  // {vx, n0^n3, n1^n3, n2^n3}
   __device__ __forceinline__ void load(const MeshView& m, uint32_t t) { r = ldg_u4(&m.rec4[t]); }
   __device__ __forceinline__ uint32_t vxw() const { return r.x; }
   // Alg. 7, _kernels.pyx:222-235:
@@ -253,8 +257,7 @@ struct Record<16> {
   //   nref = prev ^ nx[order_a] (if != 3) ^ nx[rank] (if != 3).
   __device__ __forceinline__ uint32_t next_ref(const uint32_t (&idx)[3], uint32_t i3, uint32_t idxf,
                                                uint32_t prev) const {
-    // nx[3] := 0 makes the "!= 3" xors unconditional
-    const uint4 nx = make_uint4(r.y, r.z, r.w, 0u);
+    const uint4 nx = make_uint4(r.y, r.z, r.w, 0u);  // nx[3] := 0 makes the "!= 3" xors unconditional
     const int rank = (idx[0] < idxf) + (idx[1] < idxf) + (idx[2] < idxf) + (i3 < idxf);
     const int order_a = (idx[0] < i3) + (idx[1] < i3) + (idx[2] < i3);
     return prev ^ pick4u(nx, order_a) ^ pick4u(nx, rank);
@@ -263,8 +266,8 @@ struct Record<16> {
 
 template <>
 struct Record<20> {
-  uint32_t v;
-  uint4 n;
+  uint32_t v;  // vx
+  uint4 n;     // n0..n3
   __device__ __forceinline__ void load(const MeshView& m, uint32_t t) {
     v = __ldg(&m.vx[t]);
     n = ldg_u4(&m.rec4[t]);
@@ -279,7 +282,7 @@ struct Record<20> {
 
 template <>
 struct Record<32> {
-  uint4 a, n;
+  uint4 a, n;  // {v0, v1, v2, vx}, {n0..n3}
   __device__ __forceinline__ void load(const MeshView& m, uint32_t t) {
     a = ldg_u4(&m.rec4[2 * (size_t)t]);
     n = ldg_u4(&m.rec4[2 * (size_t)t + 1]);
@@ -350,26 +353,165 @@ __device__ __forceinline__ void project_perm(const Basis& b, const float4& q, fl
                 b.poy);
 }
 
+// ----------------------------------------------------------------------------
+// The decision half of a step in PTX: Algorithm 1 (_kernels.pyx:94-102), the
+// exit reference (Alg. 3/5/7, _kernels.pyx:195-235) and the window update,
+// with the exit face kept in predicates.  Written in C++ the compiler
+// materialises "f == 0" as an integer (4 ALU ops) because every predicate
+// register is live at that point, recomputes one compare, and extracts the
+// rank bits with three more ops; here f0 is one PLOP3, the rank bits one R2P,
+// and the ranks are sums of sign bits ((a - b) >> 31 == [a < b] for ids
+// < 2^31) whose subtractions run on the FMA pipe as IMAD.IADD.  The walk is
+// ALU-pipe bound (ncu, r01), so this is where its time goes: tet20
+// 71 -> 59 SASS per step, 41 -> 30 ALU-pipe ops (tools/sass_steps.py).
+// Same IEEE operations in the same order as before (mul.rn, ordered
+// setp.lt / setp.ge), so results are bit-identical.
+//
+// Operands: %0 nref; %1-%3 idx (in/out); %4-%9 p (in/out); %10 qx; %11 qy;
+// %12 i3; %13.. layout words.
+#define TB_STEP_HEAD                                   \
+  "{\n\t"                                              \
+  ".reg .pred c0, c1, c2, f1, f2, g, q0, q1;\n\t"      \
+  ".reg .f32 a0, a1, a2, e0, e1, e2;\n\t"              \
+  ".reg .b32 fi, rk, t, lo, hi;\n\t"                   \
+  "mul.rn.f32 a0, %10, %5;\n\t"                        \
+  "mul.rn.f32 e0, %11, %4;\n\t"                        \
+  "mul.rn.f32 a2, %10, %9;\n\t"                        \
+  "mul.rn.f32 e2, %11, %8;\n\t"                        \
+  "mul.rn.f32 a1, %10, %7;\n\t"                        \
+  "mul.rn.f32 e1, %11, %6;\n\t"                        \
+  "setp.lt.f32 c0, a0, e0;\n\t"                        \
+  "setp.ge.f32 c2, a2, e2;\n\t"                        \
+  "setp.lt.f32 c1, a1, e1;\n\t"                        \
+  "and.pred f1, c0, c2;\n\t"                           \
+  "not.pred c0, c0;\n\t"                               \
+  "and.pred f2, c0, c1;\n\t"                           \
+  "or.pred g, f1, f2;\n\t"                             \
+  "selp.b32 fi, %2, %1, f1;\n\t"                       \
+  "@f2 mov.b32 fi, %3;\n\t"
+// rk = #{idx0, idx1, idx2, i3 < fi}
+#define TB_STEP_RANK                                   \
+  "sub.u32 t, %1, fi;\n\t"                             \
+  "shr.u32 rk, t, 31;\n\t"                             \
+  "sub.u32 t, %2, fi;\n\t"                             \
+  "shr.u32 t, t, 31;\n\t"                              \
+  "add.u32 rk, rk, t;\n\t"                             \
+  "sub.u32 t, %3, fi;\n\t"                             \
+  "shr.u32 t, t, 31;\n\t"                              \
+  "add.u32 rk, rk, t;\n\t"                             \
+  "sub.u32 t, %12, fi;\n\t"                            \
+  "shr.u32 t, t, 31;\n\t"                              \
+  "add.u32 rk, rk, t;\n\t"                             \
+  "and.b32 t, rk, 1;\n\t"                              \
+  "setp.ne.u32 q0, t, 0;\n\t"                          \
+  "and.b32 t, rk, 2;\n\t"                              \
+  "setp.ne.u32 q1, t, 0;\n\t"
+#define TB_STEP_TAIL                                   \
+  "@!g mov.b32 %1, %12;\n\t"                           \
+  "@!g mov.f32 %4, %10;\n\t"                           \
+  "@!g mov.f32 %5, %11;\n\t"                           \
+  "@f1 mov.b32 %2, %12;\n\t"                           \
+  "@f1 mov.f32 %6, %10;\n\t"                           \
+  "@f1 mov.f32 %7, %11;\n\t"                           \
+  "@f2 mov.b32 %3, %12;\n\t"                           \
+  "@f2 mov.f32 %8, %10;\n\t"                           \
+  "@f2 mov.f32 %9, %11;\n\t"                           \
+  "}"
+#define TB_STEP_OUTS                                                                                        \
+  "=r"(nref), "+r"(idx[0]), "+r"(idx[1]), "+r"(idx[2]), "+f"(p[0]), "+f"(p[1]), "+f"(p[2]), "+f"(p[3]), \
+      "+f"(p[4]), "+f"(p[5])
+
+template <int L>
+__device__ __forceinline__ uint32_t decide(const Record<L>& rec, uint32_t (&idx)[3], float (&p)[6], float qx,
+                                           float qy, uint32_t i3, uint32_t prev);
+
+// Alg. 5 (Tet20): nref = n[rank].  %13-%16 = n0..n3.
+template <>
+__device__ __forceinline__ uint32_t decide<20>(const Record<20>& rec, uint32_t (&idx)[3], float (&p)[6], float qx,
+                                               float qy, uint32_t i3, uint32_t) {
+  uint32_t nref;
+  asm(TB_STEP_HEAD TB_STEP_RANK
+      "selp.b32 lo, %14, %13, q0;\n\t"
+      "selp.b32 hi, %16, %15, q0;\n\t"
+      "selp.b32 %0, hi, lo, q1;\n\t" TB_STEP_TAIL
+      : TB_STEP_OUTS
+      : "f"(qx), "f"(qy), "r"(i3), "r"(rec.n.x), "r"(rec.n.y), "r"(rec.n.z), "r"(rec.n.w));
+  return nref;
+}
+
+// Alg. 7 (Tet16): nref = prev ^ nx[order_a] ^ nx[rank], nx[3] = 0,
+// order_a = #{idx0, idx1, idx2 < i3}.  %13-%15 = nx0..nx2, %16 = prev.
+template <>
+__device__ __forceinline__ uint32_t decide<16>(const Record<16>& rec, uint32_t (&idx)[3], float (&p)[6], float qx,
+                                               float qy, uint32_t i3, uint32_t prev) {
+  uint32_t nref;
+  asm(TB_STEP_HEAD TB_STEP_RANK
+      "selp.b32 lo, %14, %13, q0;\n\t"
+      "selp.b32 hi, 0, %15, q0;\n\t"
+      "selp.b32 rk, hi, lo, q1;\n\t"
+      "sub.u32 t, %1, %12;\n\t"
+      "shr.u32 fi, t, 31;\n\t"
+      "sub.u32 t, %2, %12;\n\t"
+      "shr.u32 t, t, 31;\n\t"
+      "add.u32 fi, fi, t;\n\t"
+      "sub.u32 t, %3, %12;\n\t"
+      "shr.u32 t, t, 31;\n\t"
+      "add.u32 fi, fi, t;\n\t"
+      "and.b32 t, fi, 1;\n\t"
+      "setp.ne.u32 q0, t, 0;\n\t"
+      "and.b32 t, fi, 2;\n\t"
+      "setp.ne.u32 q1, t, 0;\n\t"
+      "selp.b32 lo, %14, %13, q0;\n\t"
+      "selp.b32 hi, 0, %15, q0;\n\t"
+      "selp.b32 lo, hi, lo, q1;\n\t"
+      "xor.b32 %0, %16, rk;\n\t"
+      "xor.b32 %0, %0, lo;\n\t" TB_STEP_TAIL
+      : TB_STEP_OUTS
+      : "f"(qx), "f"(qy), "r"(i3), "r"(rec.r.y), "r"(rec.r.z), "r"(rec.r.w), "r"(prev));
+  return nref;
+}
+
+// Alg. 3 (Tet32): nref = n_i where v_i == idxf (i = 0..2), else n3.
+// %13-%15 = v0..v2, %16-%19 = n0..n3.
+template <>
+__device__ __forceinline__ uint32_t decide<32>(const Record<32>& rec, uint32_t (&idx)[3], float (&p)[6], float qx,
+                                               float qy, uint32_t i3, uint32_t) {
+  uint32_t nref;
+  asm(TB_STEP_HEAD
+      "mov.b32 %0, %19;\n\t"
+      "setp.eq.u32 q0, %13, fi;\n\t"
+      "@q0 mov.b32 %0, %16;\n\t"
+      "setp.eq.u32 q0, %14, fi;\n\t"
+      "@q0 mov.b32 %0, %17;\n\t"
+      "setp.eq.u32 q0, %15, fi;\n\t"
+      "@q0 mov.b32 %0, %18;\n\t" TB_STEP_TAIL
+      : TB_STEP_OUTS
+      : "f"(qx), "f"(qy), "r"(i3), "r"(rec.a.x), "r"(rec.a.y), "r"(rec.a.z), "r"(rec.n.x), "r"(rec.n.y),
+        "r"(rec.n.z), "r"(rec.n.w));
+  return nref;
+}
+
 // One traversal step into tet `nxt`, _kernels.pyx:238-259.  Updates the
 // window (idx, p) and returns the exit reference of `nxt`.  `P` is the ray's
 // axis-permuted point copy (ignored for TetMesh-80, whose points are inline).
-// Written branch-free: Algorithm 1's outcome as two predicates and the
-// window update as per-register selects.
-template <int L>
+// kClamp keeps the point index in bounds for meshes whose records were not
+// validated at upload (a corrupt record could send i3 anywhere); a mesh that
+// passed validate_kernel cannot produce an out-of-range i3 (see there).
+template <int L, bool kClamp = true>
 __device__ __forceinline__ uint32_t advance(const MeshView& m, const float4* __restrict__ P, const Basis& b,
                                             uint32_t (&idx)[3], float (&p)[6], uint32_t nxt, uint32_t prev) {
   Record<L> rec;
   rec.load(m, nxt);
   uint32_t i3 = idx[0] ^ idx[1] ^ idx[2] ^ rec.vxw();
   float qx, qy;
-  if constexpr (L == 80) {
-    const float4 q = rec.vertex(rec.slot_of(i3));
-    project(b, q.x, q.y, q.z, qx, qy);
-  } else {
-    i3 = min(i3, (uint32_t)m.n_points - 1u);  // corrupt record: stay in bounds
+  if constexpr (L != 80) {
+    if (kClamp) i3 = min(i3, (uint32_t)m.n_points - 1u);  // corrupt record: stay in bounds
     const float4 q = ldg_f4_at(P, i3);
     project_perm(b, q, qx, qy);
-  }
+    return decide<L>(rec, idx, p, qx, qy, i3, prev);
+  } else {
+  const float4 q = rec.vertex(rec.slot_of(i3));
+  project(b, q.x, q.y, q.z, qx, qy);
   // Algorithm 1 (_kernels.pyx:94-102): f = c0 ? (c2 ? 1 : 0) : (c1 ? 2 : 0)
   const bool c0 = __fmul_rn(qx, p[1]) < __fmul_rn(qy, p[0]);
   const bool c2 = __fmul_rn(qx, p[5]) >= __fmul_rn(qy, p[4]);
@@ -389,6 +531,7 @@ __device__ __forceinline__ uint32_t advance(const MeshView& m, const float4* __r
   p[4] = f2 ? qx : p[4];
   p[5] = f2 ? qy : p[5];
   return nref;
+  }
 }
 
 // ----------------------------------------------------------------------------
