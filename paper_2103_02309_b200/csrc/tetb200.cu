@@ -348,17 +348,25 @@ __global__ void __launch_bounds__(kBlock) cast_kernel(MeshView m, int64_t n, con
   // kUnroll steps (saves ~2.5 ALU-pipe ops per step, r01 A/B +1.5-3 %).  It
   // only runs while all kUnroll steps fit under fast_limit; the exact
   // single-step loop below finishes the walk.
+  // (The early exits add their own step count, so no per-step counter.)
+  static_assert(kUnroll == 4, "the unrolled body below is written out for 4 steps");
   while (ref < n_tets && vis + kUnroll <= (int)fast_limit) {
-    int k = 0;
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (u > 0 && ref >= n_tets) break;
-      const uint32_t nxt = ref;
-      ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
-      cur = nxt;
-      k = u + 1;
-    }
-    vis += k;
+    uint32_t nxt = ref;
+    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+    cur = nxt;
+    if (ref >= n_tets) { vis += 1; break; }
+    nxt = ref;
+    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+    cur = nxt;
+    if (ref >= n_tets) { vis += 2; break; }
+    nxt = ref;
+    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+    cur = nxt;
+    if (ref >= n_tets) { vis += 3; break; }
+    nxt = ref;
+    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+    cur = nxt;
+    vis += 4;
   }
   while (ref < n_tets) {
     const uint32_t nxt = ref;
