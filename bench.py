@@ -494,6 +494,28 @@ def run_ours(args, cfg):
     alg = algorithmic_bytes(visited, cfg["layout"])
     kern_s = float(kernel_ms.mean()) / 1e3
     achieved = alg / kern_s / 1e9
+    # Issue roofline of the walk (the kernel is instruction-issue / ALU-pipe
+    # bound, ncu r01): peak ray-steps/s if every scheduler issued one
+    # full-warp step instruction per cycle = SMs x 4 x clock x 32 lanes /
+    # SASS instructions per step (tools/sass_steps.py, committed per build).
+    roofline_issue = None
+    sp = os.path.join(ROOT, "profiles", "sass_step_counts.json")
+    clk_mhz = clocks.summary(clocks.t_ramp, clocks.t_end).get("sm_mhz")
+    if os.path.exists(sp) and clk_mhz and not sctp:
+        counts = json.load(open(sp))
+        kname = ("cast_compact_kernel" if schedule in ("compact", "compact512") else "cast_kernel")
+        entry = counts.get(f"{kname}<{cfg['layout'][3:]}, validated>") or counts.get(f"{kname}<{cfg['layout'][3:]}, clamp>")
+        if entry:
+            per_step = (entry.get("unrolled_x4_per_step") or entry["single_step"])["total"]
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            peak_steps = sms * 4 * clk_mhz * 1e6 * 32 / per_step
+            steps = (vis_sum - total_rays) / world  # walk steps of one rank's launch
+            ach_steps = steps / kern_s
+            roofline_issue = {"bound": "issue", "achieved": ach_steps / 1e9, "peak": peak_steps / 1e9,
+                              "unit": "G ray-steps/s", "frac": ach_steps / peak_steps,
+                              "sass_per_step": per_step, "sms": sms, "sm_mhz": clk_mhz,
+                              "note": "peak = SMs x 4 schedulers x clock x 32 lanes / SASS per walk step; "
+                                      "the gap is init/epilogue, SIMT divergence, latency and the tail"}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -516,7 +538,13 @@ def run_ours(args, cfg):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg,
-                     "kernel": f"{'sctp' if sctp else 'cast'}_kernel<{cfg['layout'][3:]}>"},
+                     "kernel": (f"sctp_kernel<{cfg['layout'][3:]}>" if sctp else
+                                f"{'cast_compact_kernel' if schedule in ('compact', 'compact512') else 'cast_kernel'}"
+                                f"<{cfg['layout'][3:]}>"),
+                     "note": "algorithmic gather bytes (SURVEY s8d) over the HBM copy peak; the walk's "
+                             "gathers are served by L1/L2 (ncu: DRAM traffic is a few % of them), so frac "
+                             "can exceed 1 -- the binding roofline is roofline_issue"},
+        "roofline_issue": roofline_issue,
         "clocks": dict(clocks.summary(clocks.t_ramp, clocks.t_end), window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
         "gpu_launches": args.steps + (1 if world > 1 else 0),
         "parity": parity,
