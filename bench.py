@@ -426,14 +426,11 @@ def run_ours(args, cfg):
         outs = [torch.empty(n, dtype=dt).pin_memory() for dt in
                 (torch.uint8, torch.int32, torch.int32, torch.int32, torch.int32, torch.float64, torch.int32)]
 
-        def host_call():
-            if sctp:  # the ScTP walk has no host-buffer C entry: protocol call (upload, launch, download)
-                from paper_2103_02309_b200 import kernels as K
+        host_fn = lib.tb_sctp_cast_rays_host if sctp else lib.tb_cast_rays_host
 
-                K.cast_rays_full(dm, ho.numpy(), hd.numpy(), hs.numpy(), sctp=True)
-                return
-            check(lib.tb_cast_rays_host(dm.handle, n, addr(ho), addr(hd), addr(hs), *[addr(x) for x in outs]),
-                  "tb_cast_rays_host")
+        def host_call():
+            check(host_fn(dm.handle, n, addr(ho), addr(hd), addr(hs), *[addr(x) for x in outs]),
+                  "tb_sctp_cast_rays_host" if sctp else "tb_cast_rays_host")
 
         for _ in range(max(1, args.warmup)):
             host_call()
@@ -451,8 +448,8 @@ def run_ours(args, cfg):
                "h2d_bytes_per_step": int(n * (12 + 12 + 4)), "d2h_bytes_per_step": int(n * (1 + 4 * 5 + 8)),
                "ms_per_step": e_s / args.steps * 1e3,
                "gpu_launches_per_step": 1 if os.environ.get("TETB200_E2E", "0") == "0" else -(-n // (1 << 18)),
-               "path": "tb_cast_rays_host (C ABI) on pinned host buffers: zero-copy trace over PCIe "
-                       "(TETB200_E2E=1: 3-stream chunked H2D/trace/D2H)"}
+               "path": f"{'tb_sctp_cast_rays_host' if sctp else 'tb_cast_rays_host'} (C ABI) on pinned host "
+                       "buffers: zero-copy trace over PCIe (TETB200_E2E=1: 3-stream chunked H2D/trace/D2H)"}
 
     # render-style end to end: camera rays generated in HBM (no ray upload),
     # trace, all 7 hit arrays copied back to pinned host memory, per step

@@ -177,6 +177,9 @@ int tb_sctp_cast_rays(tb_mesh* mesh, int64_t n, const float* o, const float* d,
                       const int32_t* start, uint8_t* status, int32_t* cf, int32_t* tet,
                       int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back,
                       void* stream);
+int tb_sctp_cast_rays_host(tb_mesh* mesh, int64_t n, const float* o, const float* d,
+                           const int32_t* start, uint8_t* status, int32_t* cf, int32_t* tet,
+                           int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back);
 
 /* Ray scheduling of tb_cast_rays / tb_cast_rays_host (no reference
  * counterpart: the reference walks one ray per loop iteration,

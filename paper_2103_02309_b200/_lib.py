@@ -41,6 +41,7 @@ _SIGS = {
     "tb_cast_rays_sched": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_int, c_void_p]),
     "tb_cast_rays_host": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P]),
     "tb_sctp_cast_rays": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),
+    "tb_sctp_cast_rays_host": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P]),
     "tb_cast_rays_visits": (c_int, [c_void_p, c_int64, P, P, P, P, P, c_void_p]),
     "tb_locate_points": (c_int, [c_void_p, c_int64, P, P, P, P, c_void_p]),
     "tb_hull_clip": (c_int, [c_void_p, c_int64, P, P, P, c_int64, P, P, P, c_void_p]),

@@ -901,9 +901,10 @@ __global__ void __launch_bounds__(kBlock) sctp_kernel(MeshView m, int64_t n, con
                                                       int32_t* __restrict__ triangle, double* __restrict__ t,
                                                       int32_t* __restrict__ tet_back) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  float o0, o1, o2, d0, d1, d2;
+  load_xyz_warp(o, r, n, o0, o1, o2);  // whole warp participates (shuffles)
+  load_xyz_warp(d, r, n, d0, d1, d2);
   if (r >= n) return;
-  const float o0 = o[3 * r], o1 = o[3 * r + 1], o2 = o[3 * r + 2];
-  const float d0 = d[3 * r], d1 = d[3 * r + 1], d2 = d[3 * r + 2];
   const double O[3] = {o0, o1, o2};
   const double D[3] = {d0, d1, d2};
   uint32_t cur = (uint32_t)start[r];
@@ -1457,9 +1458,15 @@ int pipe_ctx(int device, PipeCtx** out) {
 
 extern "C" {
 
-int tb_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
-                      uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle,
-                      double* t, int32_t* tet_back) {
+}  // extern "C"
+
+namespace {
+
+// Host-buffer traversal (both walks): zero-copy when every buffer is mapped
+// pinned memory, else a chunked 3-stream copy/trace pipeline.
+int cast_host(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start, uint8_t* status,
+              int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back,
+              bool sctp) {
   if (int e = check_mesh(m)) return e;
   if (n < 0) return set_error(TB_E_ARG, "negative ray count");
   if (n == 0) return TB_OK;
@@ -1475,6 +1482,11 @@ int tb_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, con
   // compaction, whose refills and epilogue read rays lane by lane over
   // PCIe, 64 Mrays/s).
   const int sched = sched_mode();
+  auto launch = [&](int64_t k, const float* ko, const float* kd, const int32_t* ks, uint8_t* kst, int32_t* kcf,
+                    int32_t* ktet, int32_t* kvis, int32_t* ktri, double* kt, int32_t* kback, cudaStream_t s) {
+    return sctp ? tb_sctp_cast_rays(m, k, ko, kd, ks, kst, kcf, ktet, kvis, ktri, kt, kback, s)
+                : cast_dispatch(m, k, ko, kd, ks, kst, kcf, ktet, kvis, ktri, kt, kback, s, sched);
+  };
   // Zero-copy path: when every buffer is mapped pinned host memory
   // (cudaHostAlloc / torch pin_memory under UVA), the trace kernel reads the
   // rays and writes the hits straight over PCIe -- one launch, no staging
@@ -1486,9 +1498,8 @@ int tb_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, con
   const bool ins_mapped = mapped_ptr(o, &dO) && mapped_ptr(d, &dD) && mapped_ptr(start, &dS);
   if (mode == 0 && outs_mapped && ins_mapped) {
     const cudaStream_t s = ctx->slot[0].s;
-    if (int e = cast_dispatch(m, n, (const float*)dO, (const float*)dD, (const int32_t*)dS, (uint8_t*)dSt,
-                              (int32_t*)dCf, (int32_t*)dTet, (int32_t*)dVis, (int32_t*)dTri, (double*)dT,
-                              (int32_t*)dBack, s, sched))
+    if (int e = launch(n, (const float*)dO, (const float*)dD, (const int32_t*)dS, (uint8_t*)dSt, (int32_t*)dCf,
+                       (int32_t*)dTet, (int32_t*)dVis, (int32_t*)dTri, (double*)dT, (int32_t*)dBack, s))
       return e;
     TB_CUDA(cudaStreamSynchronize(s));
     return TB_OK;
@@ -1511,14 +1522,14 @@ int tb_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, con
     TB_CUDA(cudaMemcpyAsync(sl.st, start + c0, uk * 4, cudaMemcpyHostToDevice, s));
     if (outs_mapped && mode == 2) {
       // inputs by copy engine, hits written by the kernel straight to host
-      if (int e = cast_dispatch(m, k, sl.o, sl.d, sl.st, (uint8_t*)dSt + c0, (int32_t*)dCf + c0,
-                                (int32_t*)dTet + c0, (int32_t*)dVis + c0, dTri ? (int32_t*)dTri + c0 : nullptr,
-                                dT ? (double*)dT + c0 : nullptr, dBack ? (int32_t*)dBack + c0 : nullptr, s, sched))
+      if (int e = launch(k, sl.o, sl.d, sl.st, (uint8_t*)dSt + c0, (int32_t*)dCf + c0, (int32_t*)dTet + c0,
+                         (int32_t*)dVis + c0, dTri ? (int32_t*)dTri + c0 : nullptr, dT ? (double*)dT + c0 : nullptr,
+                         dBack ? (int32_t*)dBack + c0 : nullptr, s))
         return e;
       continue;
     }
-    if (int e = cast_dispatch(m, k, sl.o, sl.d, sl.st, sl.status, sl.cf, sl.tet, sl.vis, triangle ? sl.tri : nullptr,
-                              t ? sl.t : nullptr, tet_back ? sl.back : nullptr, s, sched))
+    if (int e = launch(k, sl.o, sl.d, sl.st, sl.status, sl.cf, sl.tet, sl.vis, triangle ? sl.tri : nullptr,
+                       t ? sl.t : nullptr, tet_back ? sl.back : nullptr, s))
       return e;
     TB_CUDA(cudaMemcpyAsync(status + c0, sl.status, uk, cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaMemcpyAsync(cf + c0, sl.cf, uk * 4, cudaMemcpyDeviceToHost, s));
@@ -1530,6 +1541,22 @@ int tb_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, con
   }
   for (int i = 0; i < PipeCtx::kStreams; ++i) TB_CUDA(cudaStreamSynchronize(ctx->slot[i].s));
   return TB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tb_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
+                      uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle,
+                      double* t, int32_t* tet_back) {
+  return cast_host(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, false);
+}
+
+int tb_sctp_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
+                           uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle,
+                           double* t, int32_t* tet_back) {
+  return cast_host(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, true);
 }
 
 int tb_locate_points_host(tb_mesh* m, int64_t n, const double* q, const int32_t* hints, int32_t* tet,

@@ -66,30 +66,13 @@ def cast_rays_full(mesh, o32, d32, start, *, layout: str | None = None, sctp: bo
     back = np.full(n, -1, dtype=np.int32)
     if n:
         dm = device_mesh(mesh, layout=layout)
-        if sctp:
-            _sctp_host(dm, n, o, d, st, status, cf, tet, visited, triangle, t, back)
-        else:
-            check(
-                lib.tb_cast_rays_host(dm.handle, n, addr(o), addr(d), addr(st), addr(status), addr(cf), addr(tet),
-                                      addr(visited), addr(triangle), addr(t), addr(back)),
-                "tb_cast_rays_host",
-            )
+        fn = lib.tb_sctp_cast_rays_host if sctp else lib.tb_cast_rays_host
+        check(
+            fn(dm.handle, n, addr(o), addr(d), addr(st), addr(status), addr(cf), addr(tet), addr(visited),
+               addr(triangle), addr(t), addr(back)),
+            "tb_sctp_cast_rays_host" if sctp else "tb_cast_rays_host",
+        )
     return status, cf, tet, visited, triangle, t, back
-
-
-def _sctp_host(dm, n, o, d, st, status, cf, tet, visited, triangle, t, back):
-    import torch
-
-    dev = torch.device("cuda", dm.device)
-    to = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
-    go, gd, gs = to(o), to(d), to(st)
-    outs = [torch.empty(n, dtype=x, device=dev) for x in (torch.uint8, torch.int32, torch.int32, torch.int32,
-                                                          torch.int32, torch.float64, torch.int32)]
-    stream = torch.cuda.current_stream(dev)
-    check(lib.tb_sctp_cast_rays(dm.handle, n, addr(go), addr(gd), addr(gs), *[addr(x) for x in outs],
-                                stream.cuda_stream), "tb_sctp_cast_rays")
-    for host, dev_t in zip((status, cf, tet, visited, triangle, t, back), outs):
-        host[...] = dev_t.cpu().numpy()
 
 
 def cast_rays(mesh, o32, d32, start, visits_sink=None):

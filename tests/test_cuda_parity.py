@@ -446,3 +446,26 @@ def test_host_path_coherent_and_incoherent(golden, K, O, schedule, mode):
               "tb_cast_rays_host")
         for k, a, b in zip(NAMES7, outs, exp):
             assert np.array_equal(a.numpy(), b), (k, "pinned")
+
+
+@pytest.mark.parametrize("layout", ("tet20", "tet80"))
+def test_sctp_host_zero_copy(golden, K, O, layout):
+    """tb_sctp_cast_rays_host with mapped pinned buffers (the kernel reads
+    rays / writes hits over PCIe) equals the C oracle's ScTP walk."""
+    import torch
+
+    from paper_2103_02309_b200._lib import addr, check, lib
+    from paper_2103_02309_b200.device import device_mesh
+
+    base = golden_mesh(golden, "model", "tet20")
+    o, d, st = _rays(base, "model")
+    exp = O.cast_rays_full(base, o, d, st, layout=layout, sctp=True)
+    dm = device_mesh(base, layout=layout)
+    n = len(st)
+    pin = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in (o, d, st)]
+    outs = [torch.empty(n, dtype=dt).pin_memory() for dt in (torch.uint8, torch.int32, torch.int32, torch.int32,
+                                                              torch.int32, torch.float64, torch.int32)]
+    check(lib.tb_sctp_cast_rays_host(dm.handle, n, *(addr(x) for x in pin), *(addr(x) for x in outs)),
+          "tb_sctp_cast_rays_host")
+    for k, a, b in zip(NAMES7, outs, exp):
+        assert np.array_equal(a.numpy(), b), k
