@@ -75,6 +75,8 @@ struct tb_mesh {
 namespace {
 
 constexpr int kBlock = 128;
+// cast_kernel block size (r01 A/B: 32 / 64 / 256 threads were 1-7 % slower)
+constexpr int kCastBlock = 128;
 
 struct DeviceGuard {
   int prev = -1;
@@ -317,7 +319,7 @@ __device__ __forceinline__ bool long_walk(const MeshView& m, const float4* __res
 constexpr int kUnroll = 4;
 
 template <int L, bool kClamp>
-__global__ void __launch_bounds__(kBlock) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
+__global__ void __launch_bounds__(kCastBlock) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
                                                       const float* __restrict__ d,
                                                       const int32_t* __restrict__ start,
                                                       uint8_t* __restrict__ status, int32_t* __restrict__ cf,
@@ -954,9 +956,9 @@ struct CastL {
   template <typename... A>
   static void launch(unsigned g, cudaStream_t s, bool safe, A... a) {
     if (safe && L != 80)
-      cast_kernel<L, false><<<g, kBlock, 0, s>>>(a...);
+      cast_kernel<L, false><<<g, kCastBlock, 0, s>>>(a...);
     else
-      cast_kernel<L, true><<<g, kBlock, 0, s>>>(a...);
+      cast_kernel<L, true><<<g, kCastBlock, 0, s>>>(a...);
   }
 };
 template <int L>
@@ -1080,7 +1082,7 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
     e = launch_layout<CastPersistL>(m->layout, grid_for(n, kBlock), s, v, n, o, d, start, status, cf, tet, visited,
                                     triangle, t, tet_back);
   } else {
-    e = launch_layout<CastL>(m->layout, grid_for(n, kBlock), s, m->safe, v, n, o, d, start, status, cf, tet,
+    e = launch_layout<CastL>(m->layout, grid_for(n, kCastBlock), s, m->safe, v, n, o, d, start, status, cf, tet,
                              visited, triangle, t, tet_back);
   }
   if (e) return e;
