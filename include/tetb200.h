@@ -92,6 +92,15 @@ int tb_mesh_destroy(tb_mesh* mesh);
 int tb_mesh_info(const tb_mesh* mesh, int* device, int* layout, int64_t* n_points,
                  int64_t* n_tets, int64_t* n_cf, int64_t* hbm_bytes, int64_t* hot_bytes);
 
+/* 1 when the uploaded records passed the upload-time consistency check
+ * (records equal the encoding of side_verts / side_neighbors,
+ * tetmesh.py:299-320; neighbours symmetric and face-sharing): the walk then
+ * provably stays in bounds and runs without its per-step index clamp.
+ * 0 for meshes that fail it (e.g. records mutated in place): those keep the
+ * clamp, so no read leaves the mesh arrays (results on such meshes are
+ * undefined, as in the reference). */
+int tb_mesh_validated(const tb_mesh* mesh, int* validated);
+
 /* Batch traversal with the batch-layer epilogue fused.
  * Replaces: _kernels.cast_rays (_kernels.pyx:271-370) -> (status, cf, tet,
  *   visited), plus batch.cast_rays' host epilogue (batch.py:57-71 and

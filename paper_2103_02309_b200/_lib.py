@@ -37,6 +37,7 @@ _SIGS = {
         [c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_int64), POINTER(c_int64), POINTER(c_int64),
          POINTER(c_int64), POINTER(c_int64)],
     ),
+    "tb_mesh_validated": (c_int, [c_void_p, POINTER(c_int)]),
     "tb_cast_rays": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),
     "tb_cast_rays_sched": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_int, c_void_p]),
     "tb_cast_rays_host": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P]),

@@ -1255,6 +1255,13 @@ int tb_mesh_info(const tb_mesh* m, int* device, int* layout, int64_t* n_points, 
   return TB_OK;
 }
 
+int tb_mesh_validated(const tb_mesh* m, int* validated) {
+  if (int e = check_mesh(m)) return e;
+  if (!validated) return set_error(TB_E_ARG, "validated is NULL");
+  *validated = m->safe ? 1 : 0;
+  return TB_OK;
+}
+
 int tb_cast_rays(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
                  uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t,
                  int32_t* tet_back, void* stream) {

@@ -88,6 +88,9 @@ class DeviceMesh:
         check(lib.tb_mesh_info(h, None, None, None, None, None, ctypes.byref(hbm), ctypes.byref(hot)), "tb_mesh_info")
         self.hbm_bytes = hbm.value
         self.hot_bytes = hot.value
+        ok = ctypes.c_int()
+        check(lib.tb_mesh_validated(h, ctypes.byref(ok)), "tb_mesh_validated")
+        self.validated = bool(ok.value)
         self._finalizer = weakref.finalize(self, lib.tb_mesh_destroy, h)
 
     @property

@@ -469,3 +469,34 @@ def test_sctp_host_zero_copy(golden, K, O, layout):
           "tb_sctp_cast_rays_host")
     for k, a, b in zip(NAMES7, outs, exp):
         assert np.array_equal(a.numpy(), b), k
+
+
+def test_upload_validation_and_corrupt_records(golden, K, O):
+    """Every consistent mesh validates (no per-step clamp); a record mutated
+    in place fails validation, keeps the clamp and still walks in bounds
+    (no CUDA fault; the reference reads out of bounds there)."""
+    import torch
+
+    from paper_2103_02309_b200.device import DeviceMesh
+
+    for layout in ("tet32", "tet20", "tet16"):
+        m = golden_mesh(golden, "model", layout)
+        assert DeviceMesh(m).validated
+        assert not DeviceMesh(m, layout="tet80").validated  # inline points: nothing to validate
+    m = golden_mesh(golden, "model", "tet20")
+    o, d, st = _rays(m, "model")
+    exp = O.cast_rays_full(m, o, d, st)
+    bad = m.records.copy()
+    words = bad.view("<u4").reshape(len(bad), -1)
+    words[:, 0] ^= 0x00FFFFFF  # every vx word now points far outside the point array
+    from dataclasses import replace
+
+    mb = replace(m, records=bad)
+    dmb = DeviceMesh(mb)
+    assert not dmb.validated
+    got = K.cast_rays_full(dmb, o, d, st)
+    torch.cuda.synchronize()
+    assert got[0].shape == exp[0].shape  # completed without a fault
+    dmg = DeviceMesh(m)  # the good mesh still gives the oracle's results afterwards
+    for k, a, b in zip(NAMES7, K.cast_rays_full(dmg, o, d, st), exp):
+        assert np.array_equal(a, b), k
