@@ -47,9 +47,11 @@ CONFIGS = {
             desc="cfg3: blob GRID=55 (1,109,444 tets), 3840x2160 primary rays, TetMesh-16 Hilbert-sorted"),
     4: dict(grid=55, width=4096, height=4096, layout="tet16", scheme="hilbert", secondaries=True,
             desc="cfg4: blob GRID=55, 16.7M diffuse secondaries from 4096x4096 primary hits, TetMesh-16"),
-    5: dict(kuhn=203, width=7680, height=4320, layout="tet16", scheme="none",
+    # config 5 names no layout (BASELINE.json configs[4]); with 180 GB of HBM the
+    # 1 GB TetMesh-20 beats the 0.8 GB TetMesh-16 (r01 A/B: 825 vs 707 Mrays/s)
+    5: dict(kuhn=203, width=7680, height=4320, layout="tet20", scheme="none",
             desc="cfg5: Kuhn box n=203 (50,192,562 tets) stretched 4x in z with thin strip occluders "
-                 "(long thin triangles), 7680x4320 primary rays, TetMesh-16"),
+                 "(long thin triangles), 7680x4320 primary rays, TetMesh-20"),
 }
 L2_FLUSH_BYTES = 256 << 20
 FALLBACK_HBM_GBS = 6650.0
