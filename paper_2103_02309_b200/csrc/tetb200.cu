@@ -318,8 +318,17 @@ __device__ __forceinline__ bool long_walk(const MeshView& m, const float4* __res
 // Primary traversal kernel: one lane per ray, _kernels.pyx:343-369.
 constexpr int kUnroll = 4;
 
-template <int L, bool kClamp>
-__global__ void __launch_bounds__(kCastBlock) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
+// kHostRays: the ray arrays are mapped pinned host memory (zero-copy e2e
+// path) -- load them with the warp-cooperative 16 B row loads so every input
+// byte crosses PCIe once.  Device-resident rays use three plain coalesced
+// loads per array instead (fewer instructions: no shuffles; r01 A/B +3 %),
+// issued together with the start-tet load.  (An L2 prefetch of the next
+// wave's rays measured neutral-to-negative and was dropped.)  The
+// __launch_bounds__ minimum of 10 blocks keeps the walk at 48 registers
+// (10 blocks / 40 warps per SM) -- without it the branch-free basis grew the
+// kernel to 53 registers and 9 blocks (r01 A/B: config 5 -2.7 %).
+template <int L, bool kClamp, bool kHostRays>
+__global__ void __launch_bounds__(kCastBlock, 10) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
                                                       const float* __restrict__ d,
                                                       const int32_t* __restrict__ start,
                                                       uint8_t* __restrict__ status, int32_t* __restrict__ cf,
@@ -328,10 +337,18 @@ __global__ void __launch_bounds__(kCastBlock) cast_kernel(MeshView m, int64_t n,
                                                       int32_t* __restrict__ tet_back) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   float o0, o1, o2, d0, d1, d2;
-  load_xyz_warp(o, r, n, o0, o1, o2);  // whole warp participates (shuffles)
-  load_xyz_warp(d, r, n, d0, d1, d2);
-  if (r >= n) return;
-  uint32_t cur = (uint32_t)__ldg(start + r);
+  uint32_t cur;
+  if constexpr (kHostRays) {
+    load_xyz_warp(o, r, n, o0, o1, o2);  // whole warp participates (shuffles)
+    load_xyz_warp(d, r, n, d0, d1, d2);
+    if (r >= n) return;
+    cur = (uint32_t)__ldg(start + r);
+  } else {
+    if (r >= n) return;
+    cur = (uint32_t)__ldg(start + r);
+    o0 = __ldg(o + 3 * r); o1 = __ldg(o + 3 * r + 1); o2 = __ldg(o + 3 * r + 2);
+    d0 = __ldg(d + 3 * r); d1 = __ldg(d + 3 * r + 1); d2 = __ldg(d + 3 * r + 2);
+  }
   Basis b;
   uint32_t idx[3];
   float p[6];
@@ -954,11 +971,18 @@ int launch_layout(int layout, unsigned grid, cudaStream_t s, Args... args) {
 template <int L>
 struct CastL {
   template <typename... A>
-  static void launch(unsigned g, cudaStream_t s, bool safe, A... a) {
-    if (safe && L != 80)
-      cast_kernel<L, false><<<g, kCastBlock, 0, s>>>(a...);
-    else
-      cast_kernel<L, true><<<g, kCastBlock, 0, s>>>(a...);
+  static void launch(unsigned g, cudaStream_t s, bool safe, bool host_rays, A... a) {
+    if (host_rays) {
+      if (safe && L != 80)
+        cast_kernel<L, false, true><<<g, kCastBlock, 0, s>>>(a...);
+      else
+        cast_kernel<L, true, true><<<g, kCastBlock, 0, s>>>(a...);
+    } else {
+      if (safe && L != 80)
+        cast_kernel<L, false, false><<<g, kCastBlock, 0, s>>>(a...);
+      else
+        cast_kernel<L, true, false><<<g, kCastBlock, 0, s>>>(a...);
+    }
   }
 };
 template <int L>
@@ -1069,7 +1093,7 @@ int check_mesh(const tb_mesh* m) {
 // Launch the traversal with an explicit schedule (see sched_mode).
 int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start, uint8_t* status,
                   int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back,
-                  cudaStream_t s, int mode) {
+                  cudaStream_t s, int mode, bool host_rays = false) {
   DeviceGuard g(m->device);
   const MeshView v = m->view();
   int e = TB_OK;
@@ -1082,8 +1106,8 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
     e = launch_layout<CastPersistL>(m->layout, grid_for(n, kBlock), s, v, n, o, d, start, status, cf, tet, visited,
                                     triangle, t, tet_back);
   } else {
-    e = launch_layout<CastL>(m->layout, grid_for(n, kCastBlock), s, m->safe, v, n, o, d, start, status, cf, tet,
-                             visited, triangle, t, tet_back);
+    e = launch_layout<CastL>(m->layout, grid_for(n, kCastBlock), s, m->safe, host_rays, v, n, o, d, start, status,
+                             cf, tet, visited, triangle, t, tet_back);
   }
   if (e) return e;
   TB_CUDA(cudaGetLastError());
@@ -1492,9 +1516,10 @@ int cast_host(tb_mesh* m, int64_t n, const float* o, const float* d, const int32
   // PCIe, 64 Mrays/s).
   const int sched = sched_mode();
   auto launch = [&](int64_t k, const float* ko, const float* kd, const int32_t* ks, uint8_t* kst, int32_t* kcf,
-                    int32_t* ktet, int32_t* kvis, int32_t* ktri, double* kt, int32_t* kback, cudaStream_t s) {
+                    int32_t* ktet, int32_t* kvis, int32_t* ktri, double* kt, int32_t* kback, cudaStream_t s,
+                    bool host_rays) {
     return sctp ? tb_sctp_cast_rays(m, k, ko, kd, ks, kst, kcf, ktet, kvis, ktri, kt, kback, s)
-                : cast_dispatch(m, k, ko, kd, ks, kst, kcf, ktet, kvis, ktri, kt, kback, s, sched);
+                : cast_dispatch(m, k, ko, kd, ks, kst, kcf, ktet, kvis, ktri, kt, kback, s, sched, host_rays);
   };
   // Zero-copy path: when every buffer is mapped pinned host memory
   // (cudaHostAlloc / torch pin_memory under UVA), the trace kernel reads the
@@ -1508,7 +1533,7 @@ int cast_host(tb_mesh* m, int64_t n, const float* o, const float* d, const int32
   if (mode == 0 && outs_mapped && ins_mapped) {
     const cudaStream_t s = ctx->slot[0].s;
     if (int e = launch(n, (const float*)dO, (const float*)dD, (const int32_t*)dS, (uint8_t*)dSt, (int32_t*)dCf,
-                       (int32_t*)dTet, (int32_t*)dVis, (int32_t*)dTri, (double*)dT, (int32_t*)dBack, s))
+                       (int32_t*)dTet, (int32_t*)dVis, (int32_t*)dTri, (double*)dT, (int32_t*)dBack, s, true))
       return e;
     TB_CUDA(cudaStreamSynchronize(s));
     return TB_OK;
@@ -1533,12 +1558,12 @@ int cast_host(tb_mesh* m, int64_t n, const float* o, const float* d, const int32
       // inputs by copy engine, hits written by the kernel straight to host
       if (int e = launch(k, sl.o, sl.d, sl.st, (uint8_t*)dSt + c0, (int32_t*)dCf + c0, (int32_t*)dTet + c0,
                          (int32_t*)dVis + c0, dTri ? (int32_t*)dTri + c0 : nullptr, dT ? (double*)dT + c0 : nullptr,
-                         dBack ? (int32_t*)dBack + c0 : nullptr, s))
+                         dBack ? (int32_t*)dBack + c0 : nullptr, s, false))
         return e;
       continue;
     }
     if (int e = launch(k, sl.o, sl.d, sl.st, sl.status, sl.cf, sl.tet, sl.vis, triangle ? sl.tri : nullptr,
-                       t ? sl.t : nullptr, tet_back ? sl.back : nullptr, s))
+                       t ? sl.t : nullptr, tet_back ? sl.back : nullptr, s, false))
       return e;
     TB_CUDA(cudaMemcpyAsync(status + c0, sl.status, uk, cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaMemcpyAsync(cf + c0, sl.cf, uk * 4, cudaMemcpyDeviceToHost, s));

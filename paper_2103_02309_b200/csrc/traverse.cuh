@@ -79,42 +79,45 @@ struct Basis {
 
 __device__ __forceinline__ void build_basis(float o0, float o1, float o2, float d0, float d1,
                                             float d2, Basis& b) {
+  // Written with per-axis predicates and value selects (no axis indices):
+  // the index-then-pick form compiled to ~25 branch islands (BSSY/BRA/BSYNC)
+  // in every ray's init.  Same IEEE operations in the same order.
   const float a0 = fabsf(d0), a1 = fabsf(d1), a2 = fabsf(d2);
-  int mn = 0;
-  if (a1 < a0) {
-    mn = 1;
-    if (a2 < a1) mn = 2;
-  } else if (a2 < a0) {
-    mn = 2;
-  }
-  int r0, r1;
-  if (mn == 0) {
-    r0 = 1; r1 = 2;
-  } else if (mn == 1) {
-    r0 = 0; r1 = 2;
-  } else {
-    r0 = 0; r1 = 1;
-  }
-  const float ar0 = (r0 == 1) ? a1 : a0;
-  const float ar1 = (r1 == 2) ? a2 : a1;
-  const int mx = (ar0 >= ar1) ? r0 : r1;
-  const int ot = 3 - mn - mx;
-  b.mn = mn; b.mx = mx; b.ot = ot;
-  const float umax = -__fdiv_rn(pick3(d0, d1, d2, ot), pick3(d0, d1, d2, mx));
+  // min axis: argmin |d|, lowest index on ties (_kernels.pyx:43-52)
+  const bool c10 = a1 < a0, c21 = a2 < a1, c20 = a2 < a0;
+  const bool mn2 = c10 ? c21 : c20;
+  const bool mn1 = c10 && !c21;
+  const bool mn0 = !mn1 && !mn2;
+  // the other two axes in index order r0 < r1; max among them, '>=' keeps r0
+  const float ar0 = mn0 ? a1 : a0;
+  const float ar1 = mn2 ? a1 : a2;
+  const bool x0 = ar0 >= ar1;  // mx = r0 (else r1); ot = the other
+  const int r0 = mn0 ? 1 : 0, r1 = mn2 ? 1 : 2;
+  b.mn = mn0 ? 0 : (mn1 ? 1 : 2);
+  b.mx = x0 ? r0 : r1;
+  b.ot = x0 ? r1 : r0;
+  const float dr0 = mn0 ? d1 : d0, dr1 = mn2 ? d1 : d2;
+  const float dmx = x0 ? dr0 : dr1, dot = x0 ? dr1 : dr0;
+  const float umax = -__fdiv_rn(dot, dmx);
   b.umax = umax;
-  float u0 = 0.0f, u1 = 0.0f, u2 = 0.0f;
-  if (ot == 0) u0 = 1.0f; else if (ot == 1) u1 = 1.0f; else u2 = 1.0f;
-  if (mx == 0) u0 = umax; else if (mx == 1) u1 = umax; else u2 = umax;
+  // u = e_ot + umax e_mx in xyz (u[mn] = 0), t = d x u (_kernels.pyx:64-75)
+  const bool ot0 = b.ot == 0, ot1 = b.ot == 1, mx0 = b.mx == 0, mx1 = b.mx == 1;
+  const float u0 = ot0 ? 1.0f : (mx0 ? umax : 0.0f);
+  const float u1 = ot1 ? 1.0f : (mx1 ? umax : 0.0f);
+  const float u2 = (!ot0 && !ot1) ? 1.0f : ((!mx0 && !mx1) ? umax : 0.0f);
   const float t0 = __fsub_rn(__fmul_rn(d1, u2), __fmul_rn(d2, u1));
   const float t1 = __fsub_rn(__fmul_rn(d2, u0), __fmul_rn(d0, u2));
   const float t2 = __fsub_rn(__fmul_rn(d0, u1), __fmul_rn(d1, u0));
-  const float tmn = pick3(t0, t1, t2, mn);
+  const float tmn = mn0 ? t0 : (mn1 ? t1 : t2);
+  const float tr0 = mn0 ? t1 : t0, tr1 = mn2 ? t1 : t2;
+  const float tmx = x0 ? tr0 : tr1, tot = x0 ? tr1 : tr0;
   const float sgn = (tmn > 0.0f) ? 1.0f : -1.0f;
   const float tabs = (tmn > 0.0f) ? tmn : -tmn;
   b.sgn = sgn;
-  b.vmax = __fdiv_rn(pick3(t0, t1, t2, mx), tabs);
-  b.voth = __fdiv_rn(pick3(t0, t1, t2, ot), tabs);
-  const float omx = pick3(o0, o1, o2, mx), oot = pick3(o0, o1, o2, ot), omn = pick3(o0, o1, o2, mn);
+  b.vmax = __fdiv_rn(tmx, tabs);
+  b.voth = __fdiv_rn(tot, tabs);
+  const float or0 = mn0 ? o1 : o0, or1 = mn2 ? o1 : o2;
+  const float omx = x0 ? or0 : or1, oot = x0 ? or1 : or0, omn = mn0 ? o0 : (mn1 ? o1 : o2);
   b.pox = __fadd_rn(__fmul_rn(umax, omx), oot);
   b.poy = __fadd_rn(__fadd_rn(__fmul_rn(b.vmax, omx), __fmul_rn(b.voth, oot)), __fmul_rn(sgn, omn));
 }
