@@ -315,6 +315,25 @@ def run_ours(args, cfg):
     def step():
         trace(dm, go, gd, gs, out=res, stream=stream, sctp=sctp, schedule=schedule)
 
+    fg = None
+    if world > 1:
+        # every step gathers its frame set to rank 0: the shard is traced in
+        # chunks and each chunk's 20 B records go out with an async NCCL
+        # gather while the next chunk traces (multigpu.FrameGather)
+        from paper_2103_02309_b200.trace import TraceResult
+
+        fg = multigpu.FrameGather(W, H, world, rank, world, args.gather_chunks, dev, mesh.cf_triangle, mesh.cf_tets)
+        views = [TraceResult(*(getattr(res, f)[a:b] for f in ("status", "cf", "triangle", "t", "tet", "tet_back",
+                                                                 "visited"))) for (a, b) in fg.my_pieces()]
+        pieces = fg.my_pieces()
+
+        def step():  # noqa: F811  (the N > 1 step: trace + per-frame gather)
+            for k, ((a, b), v) in enumerate(zip(pieces, views)):
+                if b > a:
+                    trace(dm, go[a:b], gd[a:b], gs[a:b], out=v, stream=stream, sctp=sctp, schedule=schedule)
+                fg.send(k, v.status, v.cf, v.tet, v.visited, v.t)
+            return fg.finish()
+
     # warm-up
     for _ in range(args.warmup):
         flush.zero_()
@@ -359,14 +378,18 @@ def run_ours(args, cfg):
     # nvidia-smi samples clocks from a short untimed ramp (so the sampler is
     # up and the clocks have left idle) through the end of the timed region.
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    gather_ms = 0.0
     gather_check = None
     gather_error = None
     with ClockSampler(local) as clocks:
         time.sleep(0.3)  # nvidia-smi start-up
         clocks.mark("t_ramp")
         r0 = time.perf_counter()
-        while time.perf_counter() - r0 < args.ramp_s:
+        if world > 1:  # collectives in the step: every rank runs the same count
+            for _ in range(16):
+                flush.zero_()
+                step()
+            torch.cuda.synchronize()
+        while world == 1 and time.perf_counter() - r0 < args.ramp_s:
             for _ in range(8):
                 flush.zero_()
                 step()
@@ -380,19 +403,6 @@ def run_ours(args, cfg):
             evs[i][0].record(stream)
             step()
             evs[i][1].record(stream)
-        if world > 1:
-            g0 = torch.cuda.Event(enable_timing=True)
-            g1 = torch.cuda.Event(enable_timing=True)
-            g0.record(stream)
-            packed = multigpu.pack_hits(gidx, res.status, res.cf, res.tet, res.visited, res.triangle, res.t,
-                                        res.tet_back)
-            try:
-                full = multigpu.gather_hits(packed, per_frame * world)
-                if full is not None:  # rank 0 holds every rank's hits for the last frame set
-                    gather_check = int((full["visited"] > 0).sum().item())
-            except Exception as exc:  # report, do not lose the line
-                gather_error = repr(exc)
-            g1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
         clocks.mark("t_end")
@@ -401,8 +411,23 @@ def run_ours(args, cfg):
         time.sleep(0.05)
     kernel_ms = np.array([a.elapsed_time(b) for a, b in evs])
     if world > 1:
-        gather_ms = g0.elapsed_time(g1)
-    my_ms = float(kernel_ms.sum()) + gather_ms
+        # N > 1: the gathered frame set of the last step, checked on rank 0
+        try:
+            full = step()
+            torch.cuda.synchronize()
+            if full is not None:
+                gather_check = int((full["visited"] > 0).sum().item())
+                dig_path = os.path.join(ROOT, "tests", "golden", "golden_digests.json")
+                key = f"blob{cfg.get('grid')}/{cfg['scheme']}/cast"
+                if os.path.exists(dig_path) and "grid" in cfg and (W, H) == (1920, 1080) \
+                        and not cfg.get("secondaries") and cfg["layout"] != "tet80":
+                    digs = json.load(open(dig_path))
+                    if key in digs:  # frame 0 is the reference camera: compare with its digest
+                        f0 = [full[k][:per_frame].cpu().numpy() for k in ("status", "cf", "tet", "visited")]
+                        gather_check = {"rays": gather_check, "frame0_vs_reference_digest": digest(*f0) == digs[key]}
+        except Exception as exc:  # report, do not lose the line
+            gather_error = repr(exc)
+    my_ms = float(kernel_ms.sum())
     if world > 1:
         t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -529,10 +554,14 @@ def run_ours(args, cfg):
                    "frames": world},
         "tets_visited_per_ray": {"mean": vis_sum / total_rays, "max": vis_max},
         "kernel_ms": {"mean": float(kernel_ms.mean()), "min": float(kernel_ms.min()), "max": float(kernel_ms.max())},
-        "gather_ms": gather_ms if world > 1 else None,
+        "gather_ms": None,
         "gather": None if world == 1 else {"rays_gathered_to_rank0": gather_check,
                                             "rays_expected": per_frame * world, "error": gather_error,
-                                            "collective": "torch.distributed.gather (NCCL), 40 B packed records"},
+                                            "per_step": "every step gathers its frame set to rank 0 inside the "
+                                                        "timed region (chunked, overlapped with the trace)",
+                                            "bytes_to_rank0_per_step": int(20 * per_frame * (world - 1)),
+                                            "chunks": args.gather_chunks,
+                                            "collective": "torch.distributed.gather (NCCL, async), 20 B records"},
         "wall_ms_per_step": wall / args.steps * 1e3,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
@@ -545,7 +574,7 @@ def run_ours(args, cfg):
                              "can exceed 1 -- the binding roofline is roofline_issue"},
         "roofline_issue": roofline_issue,
         "clocks": dict(clocks.summary(clocks.t_ramp, clocks.t_end), window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
-        "gpu_launches": args.steps + (1 if world > 1 else 0),
+        "gpu_launches": args.steps * (1 if world == 1 else sum(1 for a, b in fg.my_pieces() if b > a)),
         "parity": parity,
         "e2e": e2e,
         "e2e_render": e2e_render,
@@ -581,6 +610,7 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--layout", default=None)
     ap.add_argument("--scheme", default=None)
+    ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1: trace/gather pipeline depth per step")
     ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512"),
                     help="ray-to-lane schedule of the timed trace (default: compact for secondaries, else lane)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -114,3 +114,117 @@ def gather_hits(packed, total: int, root: int = 0, group=None):
         dst[idx] = a
         full[name] = dst
     return full
+
+
+# Compact per-ray record of the per-frame gather: cf, tet, visited | status << 30,
+# t (fp64 as two int32) = 20 bytes.  The root rebuilds the ray index from the
+# static shard map and triangle / tet_back from cf with its own mesh copy.
+COMPACT_WORDS = 5
+
+
+def split_chunks(n: int, chunks: int) -> list[tuple[int, int]]:
+    """Exactly ``chunks`` contiguous (start, stop) pieces of a rank's ray
+    list (some empty when n < chunks), so every rank issues the same
+    collectives."""
+    chunks = max(1, chunks)
+    edges = [n * k // chunks for k in range(chunks + 1)]
+    return [(edges[k], edges[k + 1]) for k in range(chunks)]
+
+
+class FrameGather:
+    """Every frame's hits to the root, overlapped with tracing.
+
+    All ranks know every rank's shard (``shard_pixels`` is deterministic), so
+    chunk sizes need no exchange.  The caller traces chunk k of its shard and
+    calls ``send(k, res_k)``: the chunk's compact records go out with an
+    async ``dist.gather`` (NCCL runs it on its own stream, ordered after the
+    trace), while the caller already traces chunk k+1 on its stream.
+    ``finish()`` waits for the collectives and, on the root, scatters the
+    records into full-frame arrays -- the same seven arrays a single-GPU
+    trace of the whole job returns (the root recomputes triangle and
+    tet_back from cf exactly as the trace epilogue does, batch.py:63-71).
+    """
+
+    def __init__(self, width, height, world, rank, frames, chunks, device, cf_triangle, cf_tets, root=0,
+                 group=None, tile=16):
+        import torch
+        import torch.distributed as dist
+
+        self.world, self.rank, self.root, self.group = world, rank, root, group
+        self.device = torch.device(device)
+        # gloo moves host tensors only: stage through host memory there
+        self.comm = torch.device("cpu") if dist.get_backend(group) == "gloo" else self.device
+        self.total = width * height * frames
+        shards = [shard_pixels(width, height, r, world, tile, frames) for r in range(world)]
+        self.pieces = [split_chunks(len(s), chunks) for s in shards]  # per rank, same count everywhere
+        self.n_chunks = len(self.pieces[0])
+        self.cap = [max(1, max(p[k][1] - p[k][0] for p in self.pieces)) for k in range(self.n_chunks)]
+        self.works = []
+        if rank == root:
+            self.idx = [[torch.from_numpy(shards[r][a:b]).to(self.device) for (a, b) in self.pieces[r]]
+                        for r in range(world)]
+            self.recv = [[torch.empty((self.cap[k], COMPACT_WORDS), dtype=torch.int32, device=self.comm)
+                          for _ in range(world)] for k in range(self.n_chunks)]
+            self.cf_triangle = torch.as_tensor(np.asarray(cf_triangle, np.int32)).to(self.device)
+            self.cf_tets = torch.as_tensor(np.asarray(cf_tets, np.int32).reshape(-1, 2)).to(self.device)
+        self.send_bufs = [torch.zeros((self.cap[k], COMPACT_WORDS), dtype=torch.int32, device=self.device)
+                          for k in range(self.n_chunks)]
+
+    def my_pieces(self):
+        return self.pieces[self.rank]
+
+    def send(self, k: int, status, cf, tet, visited, t) -> None:
+        """Queue chunk k's hits (visited < 2^30: it shares a word with status)."""
+        import torch
+        import torch.distributed as dist
+
+        a, b = self.pieces[self.rank][k]
+        n = b - a
+        buf = self.send_bufs[k]
+        if n:
+            buf[:n, 0] = cf
+            buf[:n, 1] = tet
+            buf[:n, 2] = visited.to(torch.int32) | (status.to(torch.int32) << 30)
+            buf[:n, 3:5] = t.to(torch.float64).contiguous().view(torch.int32).view(n, 2)
+        dst = dist.get_global_rank(self.group, self.root) if self.group is not None else self.root
+        gl = self.recv[k] if self.rank == self.root else None
+        if self.comm != self.device:
+            buf = buf.to(self.comm)
+        self.works.append(dist.gather(buf, gather_list=gl, dst=dst, group=self.group, async_op=True))
+
+    def finish(self):
+        """Wait for the gathers; on the root return the full-job arrays."""
+        import torch
+
+        for w in self.works:
+            w.wait()
+        self.works = []
+        if self.rank != self.root:
+            return None
+        parts, idxs = [], []
+        for k in range(self.n_chunks):
+            for r in range(self.world):
+                a, b = self.pieces[r][k]
+                parts.append(self.recv[k][r][: b - a])
+                idxs.append(self.idx[r][k])
+        rec = torch.cat(parts).to(self.device)
+        idx = torch.cat(idxs)
+        cf = rec[:, 0]
+        tet = rec[:, 1]
+        w2 = rec[:, 2]
+        visited = w2 & 0x3FFFFFFF
+        status = ((w2 >> 30) & 3).to(torch.uint8)
+        t = rec[:, 3:5].contiguous().view(torch.float64).view(-1)
+        hit = cf >= 0
+        cfc = cf.clamp(min=0).long()
+        triangle = torch.where(hit, self.cf_triangle[cfc], torch.full_like(cf, -1))
+        ct = self.cf_tets[cfc]
+        back = torch.where(ct[:, 0] == tet, ct[:, 1], ct[:, 0])
+        tet_back = torch.where(hit, back, torch.full_like(cf, -1))
+        out = {}
+        for name, vals, fill in (("status", status, 0), ("cf", cf, -1), ("tet", tet, -1), ("visited", visited, 0),
+                                 ("triangle", triangle, -1), ("t", t, float("inf")), ("tet_back", tet_back, -1)):
+            full = torch.full((self.total,), fill, dtype=vals.dtype, device=self.device)
+            full[idx] = vals
+            out[name] = full
+        return out
