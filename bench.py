@@ -215,8 +215,10 @@ def run_reference_arm(args, cfg):
         "impl": "reference", "metric": "Mrays/s", "value": value, "unit": "Mrays/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "rays_per_step": len(o), "layout": cfg["layout"],
-                   "scheme": cfg["scheme"]},
+        "config": {"workload": cfg["desc"], "rays_per_step": len(o), "layout": mesh.layout,
+                   "scheme": cfg["scheme"],
+                   **({"note": "the reference has no TetMesh-80 layout and no ScTP walk: its 2-D walk on "
+                               "the Tet32 mesh of the same scene and rays"} if cfg["layout"] == "tet80" else {})},
         "tets_visited_per_ray": {"mean": vis / len(o)},
         "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": threads, "kind": kind,
                          "sample": f"full frame ({len(o)} rays) per step: compiled _kernels.cast_rays + "
