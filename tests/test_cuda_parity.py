@@ -500,3 +500,28 @@ def test_upload_validation_and_corrupt_records(golden, K, O):
     dmg = DeviceMesh(m)  # the good mesh still gives the oracle's results afterwards
     for k, a, b in zip(NAMES7, K.cast_rays_full(dmg, o, d, st), exp):
         assert np.array_equal(a, b), k
+
+
+def test_concurrent_calls_from_host_threads(golden, K, O):
+    """The reference renderer calls cast_rays concurrently on one mesh from
+    its tile pool (render.py:538-541): 8 host threads x 6 calls each through
+    the host entry points (pageable buffers -> per-thread staging streams)
+    must give the oracle's results."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2103_02309_b200.device import device_mesh
+    from paper_2103_02309_b200.scenes import interior_rays
+
+    m = golden_mesh(golden, "model", "tet16")
+    device_mesh(m)  # upload once up front, as render() does on first use
+    batches = [interior_rays(m, 3000 + 257 * i, 40 + i) for i in range(48)]
+    exp = [O.cast_rays_full(m, *b) for b in batches]
+
+    def run(i):
+        o, d, st = batches[i]
+        got = K.cast_rays_full(m, o, d, st)
+        return all(np.array_equal(a, b) for a, b in zip(got, exp[i]))
+
+    with ThreadPoolExecutor(8) as ex:
+        ok = list(ex.map(run, range(len(batches))))
+    assert all(ok)
