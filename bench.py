@@ -308,11 +308,11 @@ def run_ours(args, cfg):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     gidx = torch.from_numpy(idx).to(dev)
 
-    # ray schedule: diffuse secondaries (config 4) are incoherent -> block
-    # compaction; primaries run one ray per lane.  TETB200_SCHED (sweeps)
-    # overrides through the process-wide "auto" setting.
-    schedule = args.schedule or ("auto" if os.environ.get("TETB200_SCHED") else
-                                 ("compact" if cfg.get("secondaries") else "lane"))
+    # ray schedule: one ray per lane everywhere -- since the PTX step it also
+    # beats block compaction on the incoherent config-4 secondaries (r01:
+    # 2.38 vs 2.30 Grays/s; profiles/r01_experiments.md).  --schedule or
+    # TETB200_SCHED (sweeps, via the process-wide "auto" setting) override.
+    schedule = args.schedule or ("auto" if os.environ.get("TETB200_SCHED") else "lane")
 
     def step():
         trace(dm, go, gd, gs, out=res, stream=stream, sctp=sctp, schedule=schedule)
@@ -480,6 +480,57 @@ def run_ours(args, cfg):
                "path": f"{'tb_sctp_cast_rays_host' if sctp else 'tb_cast_rays_host'} (C ABI) on pinned host "
                        "buffers: zero-copy trace over PCIe (TETB200_E2E=1: 3-stream chunked H2D/trace/D2H)"}
 
+    # incoherent secondaries of this frame (BASELINE's metric names primary
+    # AND incoherent secondary rays): diffuse bounces from this rank's
+    # primary hits (render.py:353-359 semantics, seed 4), traced on the
+    # device with the compacting schedule, same timing protocol; checked on
+    # a strided sample against the oracle.
+    secondary = None
+    if not args.no_secondary and not cfg.get("secondaries") and not sctp and world == 1:
+        from paper_2103_02309_b200.scenes import diffuse_secondaries
+        from paper_2103_02309_b200.trace import TraceResult as _TR
+
+        so, sd, sst = diffuse_secondaries(o, d, res.t.cpu().numpy(), res.triangle.cpu().numpy(),
+                                          res.tet.cpu().numpy(), mesh.triangle_coords(), seed=4)
+        ns = len(sst)
+        if ns:
+            g2 = [torch.from_numpy(a).to(dev) for a in (so, sd, sst)]
+            r2 = empty_result(ns, dev)
+            sec = {}
+            for sched2 in ("compact", "lane"):
+                for _ in range(args.warmup):
+                    flush.zero_()
+                    trace(dm, *g2, out=r2, stream=stream, schedule=sched2)
+                ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                       for _ in range(args.steps)]
+                torch.cuda.synchronize()
+                for a, b in ev2:
+                    flush.zero_()
+                    a.record(stream)
+                    trace(dm, *g2, out=r2, stream=stream, schedule=sched2)
+                    b.record(stream)
+                torch.cuda.synchronize()
+                sec[sched2] = float(np.mean([a.elapsed_time(b) for a, b in ev2]))
+            v2 = r2.visited.cpu().numpy()
+            par2 = None
+            if not args.no_parity:
+                from oracle import pyoracle
+
+                stride = max(1, ns // args.parity_sample)
+                sl2 = slice(0, ns, stride)
+                exp2 = pyoracle.cast_rays_full(mesh, so[sl2], sd[sl2], sst[sl2], layout=dm.layout)
+                got2 = [x.cpu().numpy()[sl2] for x in (r2.status, r2.cf, r2.tet, r2.visited, r2.triangle, r2.t,
+                                                        r2.tet_back)]
+                mism2 = int(sum(np.count_nonzero(a != b) for a, b in zip(got2, exp2)))
+                par2 = {"vs": f"C oracle on every {stride}th ray", "rays_checked": int(len(exp2[0])),
+                        "bit_exact": mism2 == 0}
+            secondary = {"value": ns / sec["lane"] / 1e3, "unit": "Mrays/s", "rays": ns,
+                         "kernel_ms": sec["lane"], "schedule": "lane",
+                         "block_compaction": {"value": ns / sec["compact"] / 1e3, "kernel_ms": sec["compact"]},
+                         "tets_visited_per_ray": {"mean": float(v2.mean()), "max": int(v2.max())},
+                         "rays_from": "diffuse hemisphere bounces of this frame's primary hits (seed 4)",
+                         "parity": par2}
+
     # render-style end to end: camera rays generated in HBM (no ray upload),
     # trace, all 7 hit arrays copied back to pinned host memory, per step
     e2e_render = None
@@ -580,6 +631,7 @@ def run_ours(args, cfg):
         "parity": parity,
         "e2e": e2e,
         "e2e_render": e2e_render,
+        "secondary": secondary,
     }
     if not args.no_cpu_baseline and world == 1:
         from concurrent.futures import ThreadPoolExecutor  # noqa: F401
@@ -612,6 +664,7 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--layout", default=None)
     ap.add_argument("--scheme", default=None)
+    ap.add_argument("--no-secondary", action="store_true", help="skip the secondary-ray measurement")
     ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1: trace/gather pipeline depth per step")
     ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512"),
                     help="ray-to-lane schedule of the timed trace (default: compact for secondaries, else lane)")

@@ -557,9 +557,29 @@ __global__ void __launch_bounds__(BT) cast_compact_kernel(
     if (has) {
       const float4* __restrict__ P = m.pts + (size_t)perm * (size_t)m.n_points;
       bool done = false, guard = false;
+      int budget = steps_per_round;
+      // 4x unrolled part, as in cast_kernel (exits add their own count)
+      while (budget >= 4 && ref < n_tets && vis + 4 <= (int)fast_limit) {
+        uint32_t nxt = ref;
+        ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+        cur = nxt;
+        if (ref >= n_tets) { vis += 1; break; }
+        nxt = ref;
+        ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+        cur = nxt;
+        if (ref >= n_tets) { vis += 2; break; }
+        nxt = ref;
+        ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+        cur = nxt;
+        if (ref >= n_tets) { vis += 3; break; }
+        nxt = ref;
+        ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+        cur = nxt;
+        vis += 4;
+        budget -= 4;
+      }
 #pragma unroll 1
-      for (int s = 0; s < steps_per_round; ++s) {
-        if (ref >= n_tets) { done = true; break; }
+      for (; budget > 0 && ref < n_tets; --budget) {
         const uint32_t nxt = ref;
         ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
         cur = nxt;

@@ -93,7 +93,7 @@ def main():
             torch.cuda.synchronize()
             o, d, st = diffuse_secondaries(o, d, prim.t.cpu().numpy(), prim.triangle.cpu().numpy(),
                                            prim.tet.cpu().numpy(), mesh.triangle_coords(), seed=4)
-            sched = 3
+            sched = int(os.environ.get("AB_SCHED", "3"))
         go, gd, gs = (torch.from_numpy(x).to(dev) for x in (o, d, st))
         n = len(st)
         handles = [upload(lib, mesh, cfg["layout"]) for lib in libs]
