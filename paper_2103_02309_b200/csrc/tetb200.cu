@@ -864,7 +864,7 @@ __global__ void __launch_bounds__(kBlock) hull_clip_kernel(MeshView m, int64_t n
 }
 
 // Occlusion walks, _kernels.pyx:527-614.
-template <int L>
+template <int L, bool kClamp>
 __global__ void __launch_bounds__(kBlock) shadow_kernel(MeshView m, int64_t n, const double* __restrict__ p,
                                                         const double* __restrict__ light, int light_stride,
                                                         const int32_t* __restrict__ p_tet,
@@ -898,8 +898,30 @@ __global__ void __launch_bounds__(kBlock) shadow_kernel(MeshView m, int64_t n, c
   const int j = init_ray(m, o32[0], o32[1], o32[2], d32[0], d32[1], d32[2], (int)cur, b, idx, pw);
   uint32_t ref = pick4u(__ldg(&m.sn[cur]), j);
   const uint32_t n_tets = (uint32_t)m.n_tets;
+  const uint32_t lt_u = (uint32_t)ltet;  // -1 (light outside) never equals a tet
   const double one_m_eps = __dsub_rn(1.0, eps);
+  const float4* __restrict__ P = ray_points(m, b);
   while (true) {
+    // fast path: plain references that are not the light's tet, 4x unrolled
+    // while the guard cannot trip (same steps as the general loop below)
+    while (ref < n_tets && ref != lt_u && vis + 4 <= (int)n_tets) {
+      uint32_t nxt = ref;
+      ref = advance<L, kClamp>(m, P, b, idx, pw, nxt, cur);
+      cur = nxt;
+      if (ref >= n_tets || ref == lt_u) { vis += 1; break; }
+      nxt = ref;
+      ref = advance<L, kClamp>(m, P, b, idx, pw, nxt, cur);
+      cur = nxt;
+      if (ref >= n_tets || ref == lt_u) { vis += 2; break; }
+      nxt = ref;
+      ref = advance<L, kClamp>(m, P, b, idx, pw, nxt, cur);
+      cur = nxt;
+      if (ref >= n_tets || ref == lt_u) { vis += 3; break; }
+      nxt = ref;
+      ref = advance<L, kClamp>(m, P, b, idx, pw, nxt, cur);
+      cur = nxt;
+      vis += 4;
+    }
     uint32_t nxt, entry;
     if (ref == kBoundary) break;
     if (ref & kConstrained) {
@@ -919,7 +941,7 @@ __global__ void __launch_bounds__(kBlock) shadow_kernel(MeshView m, int64_t n, c
     }
     if ((int32_t)nxt == ltet) break;
     if (nxt >= n_tets) break;
-    ref = advance<L>(m, ray_points(m, b), b, idx, pw, nxt, entry);
+    ref = advance<L, kClamp>(m, P, b, idx, pw, nxt, entry);
     cur = nxt;
     ++vis;
     if ((uint32_t)vis > n_tets) break;
@@ -1097,7 +1119,12 @@ struct LocateL {
 template <int L>
 struct ShadowL {
   template <typename... A>
-  static void launch(unsigned g, cudaStream_t s, A... a) { shadow_kernel<L><<<g, kBlock, 0, s>>>(a...); }
+  static void launch(unsigned g, cudaStream_t s, bool safe, A... a) {
+    if (safe && L != 80)
+      shadow_kernel<L, false><<<g, kBlock, 0, s>>>(a...);
+    else
+      shadow_kernel<L, true><<<g, kBlock, 0, s>>>(a...);
+  }
 };
 template <int L>
 struct SctpL {
@@ -1410,7 +1437,7 @@ int tb_shadow_rays(tb_mesh* m, int64_t n, const double* p, const double* light, 
     return set_error(TB_E_ARG, "bad light strides %d/%d", light_stride, light_tet_stride);
   DeviceGuard g(m->device);
   const cudaStream_t s = (cudaStream_t)stream;
-  if (int e = launch_layout<ShadowL>(m->layout, grid_for(n, kBlock), s, m->view(), n, p, light, light_stride,
+  if (int e = launch_layout<ShadowL>(m->layout, grid_for(n, kBlock), s, m->safe, m->view(), n, p, light, light_stride,
                                      p_tet, light_tet, light_tet_stride, eps, occluded, visited))
     return e;
   TB_CUDA(cudaGetLastError());
