@@ -1503,18 +1503,50 @@ int e2e_mode() {
   return v ? atoi(v) : 0;
 }
 
+void free_pipe_ctx(PipeCtx* c, int device) {
+  if (!c) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  for (PipeCtx::Slot& sl : c->slot) {
+    if (sl.s) {
+      cudaStreamSynchronize(sl.s);
+      cudaStreamDestroy(sl.s);
+    }
+    if (sl.base) cudaFree(sl.base);
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+  cudaGetLastError();  // teardown errors (e.g. runtime already unloading) are not reportable here
+  delete c;
+}
+
+// Per host thread and device: the chunked host path's 3 streams and HBM
+// staging (~44 MB), created on first use and released when the thread exits
+// (renderer tile pools come and go).
+struct PipeCtxSet {
+  PipeCtx* ctxs[64] = {nullptr};
+  ~PipeCtxSet() {
+    for (int dv = 0; dv < 64; ++dv) free_pipe_ctx(ctxs[dv], dv);
+  }
+};
+
 int pipe_ctx(int device, PipeCtx** out) {
-  static thread_local PipeCtx* ctxs[64] = {nullptr};
+  static thread_local PipeCtxSet set;
   if (device < 0 || device >= 64) return set_error(TB_E_ARG, "device %d out of range", device);
-  if (ctxs[device] == nullptr) {
+  if (set.ctxs[device] == nullptr) {
     PipeCtx* c = new PipeCtx();
     const size_t k = (size_t)PipeCtx::kChunk;
     for (int i = 0; i < PipeCtx::kStreams; ++i) {
       PipeCtx::Slot& sl = c->slot[i];
-      TB_CUDA(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
-      HostCall hc;  // reuse the bump allocator arithmetic
+      cudaError_t e = cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking);
       const size_t total = HostCall::al(k * 12) * 2 + HostCall::al(k * 4) * 6 + HostCall::al(k) + HostCall::al(k * 8);
-      TB_CUDA(cudaMalloc((void**)&sl.base, total));
+      if (e == cudaSuccess) e = cudaMalloc((void**)&sl.base, total);
+      if (e != cudaSuccess) {
+        free_pipe_ctx(c, device);
+        return set_error(e == cudaErrorMemoryAllocation ? TB_E_OOM : TB_E_CUDA, "host-path staging: %s",
+                         cudaGetErrorString(e));
+      }
+      HostCall hc;  // reuse the bump allocator arithmetic
       hc.base = sl.base;
       sl.o = hc.take<float>(k * 3);
       sl.d = hc.take<float>(k * 3);
@@ -1528,9 +1560,9 @@ int pipe_ctx(int device, PipeCtx** out) {
       sl.back = hc.take<int32_t>(k);
       hc.base = nullptr;  // owned by the slot, not freed by ~HostCall
     }
-    ctxs[device] = c;
+    set.ctxs[device] = c;
   }
-  *out = ctxs[device];
+  *out = set.ctxs[device];
   return TB_OK;
 }
 
@@ -1593,33 +1625,45 @@ int cast_host(tb_mesh* m, int64_t n, const float* o, const float* d, const int32
     const int64_t c = atoll(v);
     if (c > 0 && c < chunk) chunk = c;
   }
+  // on any failure, drain the slot streams before returning so no queued copy
+  // still touches the caller's buffers afterwards
+  auto drain = [&](int code) {
+    for (int i = 0; i < PipeCtx::kStreams; ++i) cudaStreamSynchronize(ctx->slot[i].s);
+    return code;
+  };
+#define TB_CUDA_DRAIN(call)                                                                             \
+  do {                                                                                                  \
+    cudaError_t e_ = (call);                                                                            \
+    if (e_ != cudaSuccess) return drain(set_error(TB_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_))); \
+  } while (0)
   for (int64_t c0 = 0, c = 0; c0 < n; c0 += chunk, ++c) {
     const int64_t k = (n - c0 < chunk) ? (n - c0) : chunk;
     const size_t uk = (size_t)k;
     PipeCtx::Slot& sl = ctx->slot[c % PipeCtx::kStreams];
     const cudaStream_t s = sl.s;
-    TB_CUDA(cudaMemcpyAsync(sl.o, o + 3 * c0, uk * 12, cudaMemcpyHostToDevice, s));
-    TB_CUDA(cudaMemcpyAsync(sl.d, d + 3 * c0, uk * 12, cudaMemcpyHostToDevice, s));
-    TB_CUDA(cudaMemcpyAsync(sl.st, start + c0, uk * 4, cudaMemcpyHostToDevice, s));
+    TB_CUDA_DRAIN(cudaMemcpyAsync(sl.o, o + 3 * c0, uk * 12, cudaMemcpyHostToDevice, s));
+    TB_CUDA_DRAIN(cudaMemcpyAsync(sl.d, d + 3 * c0, uk * 12, cudaMemcpyHostToDevice, s));
+    TB_CUDA_DRAIN(cudaMemcpyAsync(sl.st, start + c0, uk * 4, cudaMemcpyHostToDevice, s));
     if (outs_mapped && mode == 2) {
       // inputs by copy engine, hits written by the kernel straight to host
       if (int e = launch(k, sl.o, sl.d, sl.st, (uint8_t*)dSt + c0, (int32_t*)dCf + c0, (int32_t*)dTet + c0,
                          (int32_t*)dVis + c0, dTri ? (int32_t*)dTri + c0 : nullptr, dT ? (double*)dT + c0 : nullptr,
                          dBack ? (int32_t*)dBack + c0 : nullptr, s, false))
-        return e;
+        return drain(e);
       continue;
     }
     if (int e = launch(k, sl.o, sl.d, sl.st, sl.status, sl.cf, sl.tet, sl.vis, triangle ? sl.tri : nullptr,
                        t ? sl.t : nullptr, tet_back ? sl.back : nullptr, s, false))
-      return e;
-    TB_CUDA(cudaMemcpyAsync(status + c0, sl.status, uk, cudaMemcpyDeviceToHost, s));
-    TB_CUDA(cudaMemcpyAsync(cf + c0, sl.cf, uk * 4, cudaMemcpyDeviceToHost, s));
-    TB_CUDA(cudaMemcpyAsync(tet + c0, sl.tet, uk * 4, cudaMemcpyDeviceToHost, s));
-    TB_CUDA(cudaMemcpyAsync(visited + c0, sl.vis, uk * 4, cudaMemcpyDeviceToHost, s));
-    if (triangle) TB_CUDA(cudaMemcpyAsync(triangle + c0, sl.tri, uk * 4, cudaMemcpyDeviceToHost, s));
-    if (t) TB_CUDA(cudaMemcpyAsync(t + c0, sl.t, uk * 8, cudaMemcpyDeviceToHost, s));
-    if (tet_back) TB_CUDA(cudaMemcpyAsync(tet_back + c0, sl.back, uk * 4, cudaMemcpyDeviceToHost, s));
+      return drain(e);
+    TB_CUDA_DRAIN(cudaMemcpyAsync(status + c0, sl.status, uk, cudaMemcpyDeviceToHost, s));
+    TB_CUDA_DRAIN(cudaMemcpyAsync(cf + c0, sl.cf, uk * 4, cudaMemcpyDeviceToHost, s));
+    TB_CUDA_DRAIN(cudaMemcpyAsync(tet + c0, sl.tet, uk * 4, cudaMemcpyDeviceToHost, s));
+    TB_CUDA_DRAIN(cudaMemcpyAsync(visited + c0, sl.vis, uk * 4, cudaMemcpyDeviceToHost, s));
+    if (triangle) TB_CUDA_DRAIN(cudaMemcpyAsync(triangle + c0, sl.tri, uk * 4, cudaMemcpyDeviceToHost, s));
+    if (t) TB_CUDA_DRAIN(cudaMemcpyAsync(t + c0, sl.t, uk * 8, cudaMemcpyDeviceToHost, s));
+    if (tet_back) TB_CUDA_DRAIN(cudaMemcpyAsync(tet_back + c0, sl.back, uk * 4, cudaMemcpyDeviceToHost, s));
   }
+#undef TB_CUDA_DRAIN
   for (int i = 0; i < PipeCtx::kStreams; ++i) TB_CUDA(cudaStreamSynchronize(ctx->slot[i].s));
   return TB_OK;
 }

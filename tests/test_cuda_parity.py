@@ -525,3 +525,30 @@ def test_concurrent_calls_from_host_threads(golden, K, O):
     with ThreadPoolExecutor(8) as ex:
         ok = list(ex.map(run, range(len(batches))))
     assert all(ok)
+
+
+def test_host_path_staging_released_at_thread_exit(golden, K):
+    """Each host thread's staging for the chunked host path (~44 MB of HBM)
+    is released when the thread exits -- a renderer's churning tile pool must
+    not leak device memory."""
+    import threading
+
+    import torch
+
+    from paper_2103_02309_b200.device import device_mesh
+    from paper_2103_02309_b200.scenes import interior_rays
+
+    m = golden_mesh(golden, "model", "tet20")
+    device_mesh(m)
+    o, d, st = interior_rays(m, 5000, 9)
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(3):
+        ts = [threading.Thread(target=K.cast_rays_full, args=(m, o, d, st)) for _ in range(8)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 64 << 20, (free0 - free1) / 2**20  # 24 threads x 44 MB would be ~1 GB
