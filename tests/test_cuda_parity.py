@@ -552,3 +552,36 @@ def test_host_path_staging_released_at_thread_exit(golden, K):
     torch.cuda.synchronize()
     free1, _ = torch.cuda.mem_get_info()
     assert free0 - free1 < 64 << 20, (free0 - free1) / 2**20  # 24 threads x 44 MB would be ~1 GB
+
+
+@pytest.mark.parametrize("scheme", ("none", "hilbert"))
+def test_config2_full_frame_vs_reference(digests, K, scheme):
+    """BASELINE config 2 at full size (blob GRID=55, 1.1 M tets, the whole
+    1920x1080 frame) equals the reference's own digests: scene bytes, camera
+    tet, all 2,073,600 rays' status/cf/tet/visited and the fp64 epilogue --
+    for every layout (the layout-equivalence invariant), through
+    both the host path and the device API."""
+    import torch
+
+    from conftest import mesh_digest
+    from paper_2103_02309_b200.scenes import BLOB_CAMERA, blob_scene, camera_rays
+    from paper_2103_02309_b200.tetmesh import relayout
+    from paper_2103_02309_b200.trace import trace
+
+    sc = blob_scene(55, layout="tet20", scheme=scheme, check=False)
+    assert mesh_digest(sc.mesh) == digests[f"blob55/{scheme}/mesh"]
+    o, d = camera_rays(BLOB_CAMERA["position"], BLOB_CAMERA["look_at"], BLOB_CAMERA["up"], BLOB_CAMERA["fov"],
+                       1920, 1080)
+    assert digest(o, d) == digests["blob55/rays"]
+    cam, _ = K.locate_points(sc.mesh, np.array([BLOB_CAMERA["position"]]), np.array([sc.mesh.source_tet], np.int32))
+    assert int(cam[0]) == digests[f"blob55/{scheme}/cam_tet"]
+    st = np.full(len(o), cam[0], np.int32)
+    for layout in ("tet20", "tet16", "tet32"):
+        m = relayout(sc.mesh, layout)
+        out = K.cast_rays_full(m, o, d, st)
+        assert digest(*out[:4]) == digests[f"blob55/{scheme}/cast"], layout
+        assert digest(*out[4:]) == digests[f"blob55/{scheme}/epilogue"], layout
+    dev = torch.device("cuda", 0)
+    res = trace(sc.mesh, *(torch.from_numpy(a).to(dev) for a in (o, d, st)))
+    got = [x.cpu().numpy() for x in (res.status, res.cf, res.tet, res.visited)]
+    assert digest(*got) == digests[f"blob55/{scheme}/cast"]
