@@ -474,11 +474,11 @@ __device__ __forceinline__ uint32_t decide<16>(const Record<16>& rec, uint32_t (
   return nref;
 }
 
-// Alg. 3 (Tet32): nref = n_i where v_i == idxf (i = 0..2), else n3.
+// Alg. 3 (Tet32; also TetMesh-80, whose sorted ids and sorted-slot refs are
+// the same words): nref = n_i where v_i == idxf (i = 0..2), else n3.
 // %13-%15 = v0..v2, %16-%19 = n0..n3.
-template <>
-__device__ __forceinline__ uint32_t decide<32>(const Record<32>& rec, uint32_t (&idx)[3], float (&p)[6], float qx,
-                                               float qy, uint32_t i3, uint32_t) {
+__device__ __forceinline__ uint32_t decide_alg3(uint32_t (&idx)[3], float (&p)[6], float qx, float qy, uint32_t i3,
+                                                const uint4& v, const uint4& n) {
   uint32_t nref;
   asm(TB_STEP_HEAD
       "mov.b32 %0, %19;\n\t"
@@ -489,9 +489,20 @@ __device__ __forceinline__ uint32_t decide<32>(const Record<32>& rec, uint32_t (
       "setp.eq.u32 q0, %15, fi;\n\t"
       "@q0 mov.b32 %0, %18;\n\t" TB_STEP_TAIL
       : TB_STEP_OUTS
-      : "f"(qx), "f"(qy), "r"(i3), "r"(rec.a.x), "r"(rec.a.y), "r"(rec.a.z), "r"(rec.n.x), "r"(rec.n.y),
-        "r"(rec.n.z), "r"(rec.n.w));
+      : "f"(qx), "f"(qy), "r"(i3), "r"(v.x), "r"(v.y), "r"(v.z), "r"(n.x), "r"(n.y), "r"(n.z), "r"(n.w));
   return nref;
+}
+
+template <>
+__device__ __forceinline__ uint32_t decide<32>(const Record<32>& rec, uint32_t (&idx)[3], float (&p)[6], float qx,
+                                               float qy, uint32_t i3, uint32_t) {
+  return decide_alg3(idx, p, qx, qy, i3, rec.a, rec.n);
+}
+
+template <>
+__device__ __forceinline__ uint32_t decide<80>(const Record<80>& rec, uint32_t (&idx)[3], float (&p)[6], float qx,
+                                               float qy, uint32_t i3, uint32_t) {
+  return decide_alg3(idx, p, qx, qy, i3, rec.v, rec.n);
 }
 
 // One traversal step into tet `nxt`, _kernels.pyx:238-259.  Updates the
@@ -513,27 +524,15 @@ __device__ __forceinline__ uint32_t advance(const MeshView& m, const float4* __r
     project_perm(b, q, qx, qy);
     return decide<L>(rec, idx, p, qx, qy, i3, prev);
   } else {
-  const float4 q = rec.vertex(rec.slot_of(i3));
-  project(b, q.x, q.y, q.z, qx, qy);
-  // Algorithm 1 (_kernels.pyx:94-102): f = c0 ? (c2 ? 1 : 0) : (c1 ? 2 : 0)
-  const bool c0 = __fmul_rn(qx, p[1]) < __fmul_rn(qy, p[0]);
-  const bool c2 = __fmul_rn(qx, p[5]) >= __fmul_rn(qy, p[4]);
-  const bool c1 = __fmul_rn(qx, p[3]) < __fmul_rn(qy, p[2]);
-  const bool f1 = c0 && c2;
-  const bool f2 = !c0 && c1;
-  const bool f0 = !(f1 || f2);
-  const uint32_t idxf = f1 ? idx[1] : (f2 ? idx[2] : idx[0]);
-  const uint32_t nref = rec.next_ref(idx, i3, idxf, prev);
-  idx[0] = f0 ? i3 : idx[0];
-  idx[1] = f1 ? i3 : idx[1];
-  idx[2] = f2 ? i3 : idx[2];
-  p[0] = f0 ? qx : p[0];
-  p[1] = f0 ? qy : p[1];
-  p[2] = f1 ? qx : p[2];
-  p[3] = f1 ? qy : p[3];
-  p[4] = f2 ? qx : p[4];
-  p[5] = f2 ? qy : p[5];
-  return nref;
+    // TetMesh-80: the new vertex's slot in the sorted ids, then its inline
+    // coordinates loaded straight in projection order (q[mx], q[ot], q[mn])
+    // -- no per-step axis selects; the decision is Tet32's (same words).
+    // A corrupt record cannot leave the 80-byte record (k is 0..3).
+    const int k = (rec.v.x == i3) ? 0 : ((rec.v.y == i3) ? 1 : ((rec.v.z == i3) ? 2 : 3));
+    const float* f = reinterpret_cast<const float*>(rec.base + 2) + 3 * k;
+    const float4 q = make_float4(__ldg(f + b.mx), __ldg(f + b.ot), __ldg(f + b.mn), 0.0f);
+    project_perm(b, q, qx, qy);
+    return decide<80>(rec, idx, p, qx, qy, i3, prev);
   }
 }
 
