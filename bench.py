@@ -318,12 +318,28 @@ def run_ours(args, cfg):
         trace(dm, go, gd, gs, out=res, stream=stream, sctp=sctp, schedule=schedule)
 
     fg = None
-    if world > 1:
+    pg = None
+    gather_mode = None
+    if world > 1 and args.gather == "p2p":
+        # every step assembles its frame set on rank 0 inside the trace: each
+        # rank's kernel stores every finished ray into rank 0's full-frame
+        # arrays (CUDA IPC, P2P over NVLink) -- no collective moves the hits
+        try:
+            pg = multigpu.PeerFrameGather(W, H, world, rank, world, dev)
+            gather_mode = "p2p"
+
+            def step():  # noqa: F811  (the N > 1 step: fused trace + frame assembly)
+                return pg.step(dm, go, gd, gs, stream)
+        except Exception as exc:  # no peer access / IPC: fall back to the NCCL gather
+            log(f"[bench] p2p frame assembly unavailable ({exc!r}); using the NCCL gather")
+            pg = None
+    if world > 1 and pg is None:
         # every step gathers its frame set to rank 0: the shard is traced in
         # chunks and each chunk's 20 B records go out with an async NCCL
         # gather while the next chunk traces (multigpu.FrameGather)
         from paper_2103_02309_b200.trace import TraceResult
 
+        gather_mode = "nccl"
         fg = multigpu.FrameGather(W, H, world, rank, world, args.gather_chunks, dev, mesh.cf_triangle, mesh.cf_tets)
         views = [TraceResult(*(getattr(res, f)[a:b] for f in ("status", "cf", "triangle", "t", "tet", "tet_back",
                                                                  "visited"))) for (a, b) in fg.my_pieces()]
@@ -341,6 +357,13 @@ def run_ours(args, cfg):
         flush.zero_()
         step()
     torch.cuda.synchronize()
+    if pg is not None:
+        # p2p: the hits live in rank 0's frame; rank 0 checks its own rays'
+        # slice below, and the visited statistics come from the whole frame
+        from paper_2103_02309_b200.trace import TraceResult as _TR
+
+        if rank == 0:
+            res = _TR(*(pg.frame[k][gidx] for k in ("status", "cf", "triangle", "t", "tet", "tet_back", "visited")))
 
     # parity at full size: the reference's own digest of this frame (rank 0, N=1)
     parity = None
@@ -374,7 +397,10 @@ def run_ours(args, cfg):
         mism = int(sum(np.count_nonzero(a != b) for a, b in zip(got, exp)))
         parity = {"vs": f"C oracle (oracle/tetoracle.c) on every {stride}th ray", "rays_checked": int(len(exp[0])),
                   "mismatched_values": mism, "bit_exact": mism == 0}
-    visited = res.visited.cpu().numpy()
+    if pg is None:
+        visited = res.visited.cpu().numpy()
+    else:  # the whole job's visited counts on rank 0, none elsewhere
+        visited = pg.frame["visited"].cpu().numpy() if rank == 0 else np.zeros(0, np.int32)
 
     # timed region: K steps between barrier + sync; per-step kernel events.
     # nvidia-smi samples clocks from a short untimed ramp (so the sampler is
@@ -434,7 +460,8 @@ def run_ours(args, cfg):
         t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         max_ms = float(t.item())
-        vt = torch.tensor([int(visited.sum()), int(visited.max()), n], dtype=torch.int64, device=dev)
+        vt = torch.tensor([int(visited.sum()), int(visited.max(initial=0)), len(visited)], dtype=torch.int64,
+                          device=dev)
         vmax = vt.clone()
         dist.all_reduce(vt, op=dist.ReduceOp.SUM)
         dist.all_reduce(vmax, op=dist.ReduceOp.MAX)
@@ -563,6 +590,8 @@ def run_ours(args, cfg):
                               "pinned host memory (camera tet located once)"}
 
     if rank != 0:
+        if pg is not None:
+            pg.close()
         if world > 1:
             dist.destroy_process_group()
         return
@@ -608,13 +637,20 @@ def run_ours(args, cfg):
         "tets_visited_per_ray": {"mean": vis_sum / total_rays, "max": vis_max},
         "kernel_ms": {"mean": float(kernel_ms.mean()), "min": float(kernel_ms.min()), "max": float(kernel_ms.max())},
         "gather_ms": None,
-        "gather": None if world == 1 else {"rays_gathered_to_rank0": gather_check,
-                                            "rays_expected": per_frame * world, "error": gather_error,
-                                            "per_step": "every step gathers its frame set to rank 0 inside the "
-                                                        "timed region (chunked, overlapped with the trace)",
-                                            "bytes_to_rank0_per_step": int(20 * per_frame * (world - 1)),
-                                            "chunks": args.gather_chunks,
-                                            "collective": "torch.distributed.gather (NCCL, async), 20 B records"},
+        "gather": None if world == 1 else (
+            {"rays_gathered_to_rank0": gather_check, "rays_expected": per_frame * world, "error": gather_error,
+             "mode": "p2p",
+             "per_step": "every step assembles its frame set on rank 0 inside the timed region: each rank's trace "
+                         "epilogue stores every finished ray into rank 0's full-frame arrays (CUDA IPC, P2P over "
+                         "NVLink), then stream sync + barrier",
+             "bytes_to_rank0_per_step": int(29 * per_frame * (world - 1)), "collective": "none (barrier only)"}
+            if gather_mode == "p2p" else
+            {"rays_gathered_to_rank0": gather_check, "rays_expected": per_frame * world, "error": gather_error,
+             "mode": "nccl",
+             "per_step": "every step gathers its frame set to rank 0 inside the timed region (chunked, overlapped "
+                         "with the trace)",
+             "bytes_to_rank0_per_step": int(20 * per_frame * (world - 1)), "chunks": args.gather_chunks,
+             "collective": "torch.distributed.gather (NCCL, async), 20 B records"}),
         "wall_ms_per_step": wall / args.steps * 1e3,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
@@ -627,7 +663,7 @@ def run_ours(args, cfg):
                              "can exceed 1 -- the binding roofline is roofline_issue"},
         "roofline_issue": roofline_issue,
         "clocks": dict(clocks.summary(clocks.t_ramp, clocks.t_end), window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
-        "gpu_launches": args.steps * (1 if world == 1 else sum(1 for a, b in fg.my_pieces() if b > a)),
+        "gpu_launches": args.steps * (1 if fg is None else sum(1 for a, b in fg.my_pieces() if b > a)),
         "parity": parity,
         "e2e": e2e,
         "e2e_render": e2e_render,
@@ -651,6 +687,8 @@ def run_ours(args, cfg):
                                 "sample": f"first {m} rays of the frame, best of {reps}: compiled reference "
                                           "kernels + batch epilogue on a thread pool"}
     print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -665,6 +703,8 @@ def main():
     ap.add_argument("--layout", default=None)
     ap.add_argument("--scheme", default=None)
     ap.add_argument("--no-secondary", action="store_true", help="skip the secondary-ray measurement")
+    ap.add_argument("--gather", choices=("p2p", "nccl"), default="p2p",
+                    help="N > 1 frame assembly: fused P2P stores (default) or the chunked NCCL gather")
     ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1: trace/gather pipeline depth per step")
     ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512"),
                     help="ray-to-lane schedule of the timed trace (default: compact for secondaries, else lane)")

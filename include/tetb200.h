@@ -123,6 +123,29 @@ int tb_cast_rays(tb_mesh* mesh, int64_t n, const float* o, const float* d, const
 int tb_cast_rays_sched(tb_mesh* mesh, int64_t n, const float* o, const float* d, const int32_t* start,
                        uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle,
                        double* t, int32_t* tet_back, int schedule, void* stream);
+/* tb_cast_rays whose ray r writes its seven results to index out_index[r]
+ * (int64, device) of the output arrays: the multi-GPU frame assembly with
+ * no separate collective -- every rank traces its image tiles and its trace
+ * epilogue stores each finished ray straight into the root GPU's full-frame
+ * arrays, mapped into this process with tb_ipc_open (CUDA IPC; P2P stores
+ * over NVLink).  The caller synchronises the stream and then the ranks
+ * (a barrier) before the root reads the frame.  No reference counterpart
+ * (the reference is single-process, render.py:496-541). */
+int tb_cast_rays_scatter(tb_mesh* mesh, int64_t n, const float* o, const float* d,
+                         const int32_t* start, const int64_t* out_index, uint8_t* status,
+                         int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t,
+                         int32_t* tet_back, void* stream);
+
+/* CUDA IPC of device allocations between the ranks of one node: the
+ * 64-byte handle of the allocation holding dev_ptr (which must be the start
+ * of a cudaMalloc'd block, e.g. from tb_device_alloc), its mapping into this
+ * process on `device` (peer access enabled), and the unmapping. */
+int tb_device_alloc(size_t bytes, int device, void** out);
+int tb_device_free(void* ptr);
+int tb_ipc_get_handle(const void* dev_ptr, void* handle_out);
+int tb_ipc_open(const void* handle, int device, void** dev_ptr_out);
+int tb_ipc_close(void* dev_ptr);
+
 int tb_cast_rays_host(tb_mesh* mesh, int64_t n, const float* o, const float* d,
                       const int32_t* start, uint8_t* status, int32_t* cf, int32_t* tet,
                       int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back);

@@ -327,14 +327,19 @@ constexpr int kUnroll = 4;
 // __launch_bounds__ minimum of 10 blocks keeps the walk at 48 registers
 // (10 blocks / 40 warps per SM) -- without it the branch-free basis grew the
 // kernel to 53 registers and 9 blocks (r01 A/B: config 5 -2.7 %).
-template <int L, bool kClamp, bool kHostRays>
+// kScatter: ray r's hits go to slot oidx[r] of the output arrays instead of
+// r -- the multi-GPU frame assembly, where the outputs are the root GPU's
+// full-frame arrays mapped into this process (CUDA IPC over NVLink) and each
+// ray's result is stored there by the epilogue the moment its walk ends.
+template <int L, bool kClamp, bool kHostRays, bool kScatter>
 __global__ void __launch_bounds__(kCastBlock, 10) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
                                                       const float* __restrict__ d,
                                                       const int32_t* __restrict__ start,
                                                       uint8_t* __restrict__ status, int32_t* __restrict__ cf,
                                                       int32_t* __restrict__ tet, int32_t* __restrict__ visited,
                                                       int32_t* __restrict__ triangle, double* __restrict__ t,
-                                                      int32_t* __restrict__ tet_back) {
+                                                      int32_t* __restrict__ tet_back,
+                                                      const int64_t* __restrict__ oidx) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   float o0, o1, o2, d0, d1, d2;
   uint32_t cur;
@@ -398,7 +403,8 @@ __global__ void __launch_bounds__(kCastBlock, 10) cast_kernel(MeshView m, int64_
     }
   }
   if (st != kError) st = (ref == kBoundary) ? kMiss : ((ref & kConstrained) ? kHit : kError);
-  write_result(m, r, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
+  const int64_t w = kScatter ? __ldg(oidx + r) : r;
+  write_result(m, w, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
                tet_back);
 }
 
@@ -1013,17 +1019,23 @@ int launch_layout(int layout, unsigned grid, cudaStream_t s, Args... args) {
 template <int L>
 struct CastL {
   template <typename... A>
-  static void launch(unsigned g, cudaStream_t s, bool safe, bool host_rays, A... a) {
-    if (host_rays) {
-      if (safe && L != 80)
-        cast_kernel<L, false, true><<<g, kCastBlock, 0, s>>>(a...);
+  static void launch(unsigned g, cudaStream_t s, bool safe, bool host_rays, const int64_t* oidx, A... a) {
+    const bool nc = safe && L != 80;  // validated mesh: no per-step index clamp
+    if (oidx != nullptr) {  // scattered outputs (device rays only)
+      if (nc)
+        cast_kernel<L, false, false, true><<<g, kCastBlock, 0, s>>>(a..., oidx);
       else
-        cast_kernel<L, true, true><<<g, kCastBlock, 0, s>>>(a...);
+        cast_kernel<L, true, false, true><<<g, kCastBlock, 0, s>>>(a..., oidx);
+    } else if (host_rays) {
+      if (nc)
+        cast_kernel<L, false, true, false><<<g, kCastBlock, 0, s>>>(a..., oidx);
+      else
+        cast_kernel<L, true, true, false><<<g, kCastBlock, 0, s>>>(a..., oidx);
     } else {
-      if (safe && L != 80)
-        cast_kernel<L, false, false><<<g, kCastBlock, 0, s>>>(a...);
+      if (nc)
+        cast_kernel<L, false, false, false><<<g, kCastBlock, 0, s>>>(a..., oidx);
       else
-        cast_kernel<L, true, false><<<g, kCastBlock, 0, s>>>(a...);
+        cast_kernel<L, true, false, false><<<g, kCastBlock, 0, s>>>(a..., oidx);
     }
   }
 };
@@ -1140,10 +1152,11 @@ int check_mesh(const tb_mesh* m) {
 // Launch the traversal with an explicit schedule (see sched_mode).
 int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start, uint8_t* status,
                   int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back,
-                  cudaStream_t s, int mode, bool host_rays = false) {
+                  cudaStream_t s, int mode, bool host_rays = false, const int64_t* oidx = nullptr) {
   DeviceGuard g(m->device);
   const MeshView v = m->view();
   int e = TB_OK;
+  if (oidx != nullptr) mode = 1;  // scattered outputs: one ray per lane
   if ((mode == 3 || mode == 4) && n < (int64_t)1 << 32) {
     e = mode == 3 ? launch_compact<256>(m->layout, m->safe, n, s, v, n, o, d, start, status, cf, tet, visited,
                                         triangle, t, tet_back)
@@ -1153,8 +1166,8 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
     e = launch_layout<CastPersistL>(m->layout, grid_for(n, kBlock), s, v, n, o, d, start, status, cf, tet, visited,
                                     triangle, t, tet_back);
   } else {
-    e = launch_layout<CastL>(m->layout, grid_for(n, kCastBlock), s, m->safe, host_rays, v, n, o, d, start, status,
-                             cf, tet, visited, triangle, t, tet_back);
+    e = launch_layout<CastL>(m->layout, grid_for(n, kCastBlock), s, m->safe, host_rays, oidx, v, n, o, d, start,
+                             status, cf, tet, visited, triangle, t, tet_back);
   }
   if (e) return e;
   TB_CUDA(cudaGetLastError());
@@ -1345,6 +1358,52 @@ int tb_cast_rays(tb_mesh* m, int64_t n, const float* o, const float* d, const in
   // compaction with tb_set_schedule)
   return cast_dispatch(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, (cudaStream_t)stream,
                        sched_mode());
+}
+
+int tb_cast_rays_scatter(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
+                         const int64_t* out_index, uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited,
+                         int32_t* triangle, double* t, int32_t* tet_back, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  if (n == 0) return TB_OK;
+  if (!o || !d || !start || !out_index || !status || !cf || !tet || !visited)
+    return set_error(TB_E_ARG, "NULL ray buffer");
+  return cast_dispatch(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, (cudaStream_t)stream, 1,
+                       false, out_index);
+}
+
+int tb_device_alloc(size_t bytes, int device, void** out) {
+  if (!out) return set_error(TB_E_ARG, "out is NULL");
+  DeviceGuard g(device);
+  TB_CUDA(cudaMalloc(out, bytes ? bytes : 1));
+  return TB_OK;
+}
+
+int tb_device_free(void* ptr) {
+  if (ptr) TB_CUDA(cudaFree(ptr));
+  return TB_OK;
+}
+
+int tb_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) return set_error(TB_E_ARG, "NULL pointer");
+  cudaIpcMemHandle_t h;
+  TB_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  memcpy(handle_out, &h, sizeof(h));
+  return TB_OK;
+}
+
+int tb_ipc_open(const void* handle, int device, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return set_error(TB_E_ARG, "NULL pointer");
+  DeviceGuard g(device);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  TB_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return TB_OK;
+}
+
+int tb_ipc_close(void* dev_ptr) {
+  if (dev_ptr) TB_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return TB_OK;
 }
 
 int tb_cast_rays_sched(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,

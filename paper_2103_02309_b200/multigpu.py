@@ -228,3 +228,104 @@ class FrameGather:
             full[idx] = vals
             out[name] = full
         return out
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of raw device memory (no copy)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
+
+
+# (name, numpy typestr, bytes per ray) of the seven per-ray outputs, in the
+# order tb_cast_rays_scatter takes them
+_OUTPUTS = (("status", "|u1", 1), ("cf", "<i4", 4), ("tet", "<i4", 4), ("visited", "<i4", 4),
+            ("triangle", "<i4", 4), ("t", "<f8", 8), ("tet_back", "<i4", 4))
+
+
+class PeerFrameGather:
+    """Frame assembly fused into the trace: no collective moves the hits.
+
+    The root allocates the job's seven full-frame arrays in one device block
+    and shares it with the other ranks by CUDA IPC (the 64-byte handle goes
+    out with one broadcast at setup).  Every rank then traces its tiles with
+    ``tb_cast_rays_scatter``: the kernel's epilogue stores each finished
+    ray's results straight into the root's arrays at the ray's global index
+    -- P2P stores over NVLink that overlap the walk ray by ray, instead of a
+    trace followed by a gather.  ``step`` ends with a stream sync and a
+    barrier, after which the root's ``frame`` holds the whole job (the same
+    arrays a single-GPU trace of all of it returns).
+    """
+
+    def __init__(self, width, height, world, rank, frames, device, root=0, group=None, tile=16):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from ._lib import check, lib
+
+        self.world, self.rank, self.root, self.group = world, rank, root, group
+        self.device = torch.device(device)
+        self.total = width * height * frames
+        shard = shard_pixels(width, height, rank, world, tile, frames)
+        self.idx = torch.from_numpy(shard).to(self.device)
+        self.offsets = []
+        off = 0
+        for _, _, size in _OUTPUTS:
+            self.offsets.append(off)
+            off += (size * self.total + 255) // 256 * 256
+        self.bytes = off
+        self.base = None
+        self.remote = None
+        dev_idx = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        handle = None
+        if rank == root:
+            p = ctypes.c_void_p()
+            check(lib.tb_device_alloc(self.bytes, dev_idx, ctypes.byref(p)), "tb_device_alloc")
+            self.base = p.value
+            buf = (ctypes.c_char * 64)()
+            check(lib.tb_ipc_get_handle(self.base, buf), "tb_ipc_get_handle")
+            handle = bytes(buf)
+        obj = [handle]
+        src = dist.get_global_rank(group, root) if group is not None else root
+        dist.broadcast_object_list(obj, src=src, group=group)
+        if rank != root:
+            p = ctypes.c_void_p()
+            check(lib.tb_ipc_open(obj[0], dev_idx, ctypes.byref(p)), "tb_ipc_open")
+            self.remote = p.value
+        dest = self.base if rank == root else self.remote
+        self.ptrs = [dest + o for o in self.offsets]
+        self.frame = None
+        if rank == root:
+            self.frame = {name: torch.as_tensor(_CudaArray(self.base + o, self.total, ts), device=self.device)
+                          for (name, ts, _), o in zip(_OUTPUTS, self.offsets)}
+
+    def step(self, dm, origins, dirs, start, stream=None):
+        """Trace this rank's rays into the root's frame; returns the frame on
+        the root (torch tensors over the shared block), None elsewhere."""
+        import torch
+        import torch.distributed as dist
+
+        from ._lib import addr, check, lib
+
+        s = stream or torch.cuda.current_stream(self.device)
+        check(lib.tb_cast_rays_scatter(dm.handle, self.idx.numel(), addr(origins), addr(dirs), addr(start),
+                                       addr(self.idx), *self.ptrs, s.cuda_stream), "tb_cast_rays_scatter")
+        s.synchronize()  # this rank's stores have landed in the root's memory
+        dist.barrier(group=self.group)
+        return self.frame
+
+    def close(self):
+        import torch.distributed as dist
+
+        from ._lib import lib
+
+        if self.remote is not None:
+            lib.tb_ipc_close(self.remote)
+            self.remote = None
+        dist.barrier(group=self.group)  # every mapping is gone before the root frees the block
+        if self.base is not None:
+            self.frame = None
+            lib.tb_device_free(self.base)
+            self.base = None
