@@ -122,4 +122,119 @@ __device__ __forceinline__ uint32_t sctp_advance(const MeshView& m, SctpWindow& 
   return nref;
 }
 
+// ----------------------------------------------------------------------------
+// Edge-cached ScTP step.  The predicate's face values are scalar triple
+// products s = d . (A x B) of origin-relative vertices, one per directed
+// edge of the face.  For the quad's slots x < y let E[x][y] = d.(R_x x R_y);
+// then d.(R_y x R_x) = -E[x][y] *exactly* (fp64 cross and dot are
+// antisymmetric bit for bit in round-to-nearest), so every s the reference
+// computes is +-E of one of the tet's six edges.  Three of them belong to the
+// entry face and were computed in the previous tet (carried in `SctpEdges`);
+// only the three edges to the new vertex V are new: 3 triple products per
+// step instead of up to 9 (plus 9-27 fp64 subtractions) in sctp_exit.
+//
+// Face k (opposite window vertex w_k, k = 0..2, i.e. slots j = 0..3 minus the
+// entry slot, visited in the reference's order) has vertices {w_p, w_q, V},
+// p < q.  With X = e_pq, tp = d.(R_p x R_V), tq = d.(R_q x R_V), its ordered
+// values (s0, s1, s2) are one of (-tp, X, tq), (-tq, -X, tp), (tp, -tq, -X),
+// (X, tq, -tp) -- as multisets all +-{-tp, X, tq}, the sign being + exactly
+// when swap == (V lies between w_p and w_q in id order).  The reference's
+// decision uses the values only through min, max and comparisons with 0, so
+// it is evaluated on the multiset; signed zeros and the order of equal values
+// cannot change any comparison.  NaNs would make the order matter: any NaN
+// among the step's values takes the exact per-face path (sctp_exit) instead.
+struct SctpEdges {
+  double e01, e02, e12;  // entry face, window order (ascending ids)
+};
+
+__device__ __forceinline__ double triple(const D3& d, const D3& a, const D3& b) { return ddot3(d, dcross3(a, b)); }
+
+__device__ __forceinline__ D3 rel(const float4& P, const D3& o) {
+  return {__dsub_rn((double)P.x, o.x), __dsub_rn((double)P.y, o.y), __dsub_rn((double)P.z, o.z)};
+}
+
+// Edges of a fresh window (init, NaN fallback).
+__device__ __forceinline__ void window_edges(const SctpWindow& w, const D3& o, const D3& d, SctpEdges& e) {
+  const D3 R0 = rel(w.P[0], o), R1 = rel(w.P[1], o), R2 = rel(w.P[2], o);
+  e.e01 = triple(d, R0, R1);
+  e.e02 = triple(d, R0, R2);
+  e.e12 = triple(d, R1, R2);
+}
+
+template <int L>
+__device__ __forceinline__ uint32_t sctp_advance_cached(const MeshView& m, SctpWindow& w, SctpEdges& e,
+                                                        const double (&O)[3], const double (&Dd)[3], uint32_t nxt,
+                                                        uint32_t prev) {
+  Record<L> rec;
+  rec.load(m, nxt);
+  uint32_t i3 = w.id[0] ^ w.id[1] ^ w.id[2] ^ rec.vxw();
+  if (L != 80) i3 = min(i3, (uint32_t)m.n_points - 1u);
+  const float4 q = fetch_vertex<L>(m, rec, i3);
+  const bool rho = __ldg(&m.orient[nxt]) != 0;
+  // a_k: window vertex k precedes V in id order (pos = a0 + a1 + a2)
+  const bool a0 = w.id[0] < i3, a1 = w.id[1] < i3, a2 = w.id[2] < i3;
+  const D3 o = {O[0], O[1], O[2]}, d = {Dd[0], Dd[1], Dd[2]};
+  const D3 RV = rel(q, o);
+  const double t0 = triple(d, rel(w.P[0], o), RV);
+  const double t1 = triple(d, rel(w.P[1], o), RV);
+  const double t2 = triple(d, rel(w.P[2], o), RV);
+  if (isnan(t0) || isnan(t1) || isnan(t2) || isnan(e.e01) || isnan(e.e02) || isnan(e.e12)) {
+    // exact per-face path (the order of the values matters with NaNs)
+    const uint32_t nref = sctp_advance<L>(m, w, O, Dd, nxt, prev);
+    window_edges(w, o, d, e);
+    return nref;
+  }
+  int exit_k = -1, best_k = -1;
+  double best_m = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    // face opposite w_k: p < q the other window vertices
+    const bool ap = (k == 0) ? a1 : a0;
+    const bool aq = (k == 2) ? a1 : a2;
+    const bool ak = (k == 0) ? a0 : ((k == 1) ? a1 : a2);
+    const double X = (k == 0) ? e.e12 : ((k == 1) ? e.e02 : e.e01);
+    const double tp = (k == 0) ? t1 : t0;
+    const double tq = (k == 2) ? t1 : t2;
+    const int j = ak ? k : k + 1;  // the face's slot in the sorted quad
+    const bool swap = ((j & 1) == 0) != rho;
+    const bool middle = ap && !aq;
+    const bool pos_sign = swap == middle;
+    const double v0 = -tp;
+    const double lo = fmin(fmin(v0, X), tq), hi = fmax(fmax(v0, X), tq);
+    const double mn = pos_sign ? lo : -hi;
+    const bool accept = pos_sign ? (lo >= 0.0 && hi > 0.0) : (hi <= 0.0 && lo < 0.0);
+    if (exit_k < 0) {
+      if (accept) {
+        exit_k = k;
+      } else if (mn > best_m) {
+        best_m = mn;
+        best_k = k;
+      }
+    }
+  }
+  if (exit_k < 0) exit_k = best_k >= 0 ? best_k : 0;  // all-NaN cannot happen here; slot rule of sctp_exit
+  const int k = exit_k;
+  const uint32_t idxf = (k == 0) ? w.id[0] : ((k == 1) ? w.id[1] : w.id[2]);
+  const uint32_t nref = rec.next_ref(w.id, i3, idxf, prev);
+  // new window {w_p, w_q, V} in id order, with its edges
+  const bool ap = (k == 0) ? a1 : a0;
+  const bool aq = (k == 2) ? a1 : a2;
+  const uint32_t idp = (k == 0) ? w.id[1] : w.id[0], idq = (k == 2) ? w.id[1] : w.id[2];
+  const float4 Pp = (k == 0) ? w.P[1] : w.P[0], Pq = (k == 2) ? w.P[1] : w.P[2];
+  const double X = (k == 0) ? e.e12 : ((k == 1) ? e.e02 : e.e01);
+  const double tp = (k == 0) ? t1 : t0;
+  const double tq = (k == 2) ? t1 : t2;
+  if (!ap) {  // V first
+    w.id[0] = i3; w.P[0] = q; w.id[1] = idp; w.P[1] = Pp; w.id[2] = idq; w.P[2] = Pq;
+    e.e01 = -tp; e.e02 = -tq; e.e12 = X;
+  } else if (!aq) {  // V between
+    w.id[0] = idp; w.P[0] = Pp; w.id[1] = i3; w.P[1] = q; w.id[2] = idq; w.P[2] = Pq;
+    e.e01 = tp; e.e02 = X; e.e12 = -tq;
+  } else {  // V last
+    w.id[0] = idp; w.P[0] = Pp; w.id[1] = idq; w.P[1] = Pq; w.id[2] = i3; w.P[2] = q;
+    e.e01 = X; e.e02 = tp; e.e12 = tq;
+  }
+  return nref;
+}
+
 }  // namespace tb

@@ -960,7 +960,10 @@ __global__ void __launch_bounds__(kBlock) shadow_kernel(MeshView m, int64_t n, c
 // (traversal.sctp_exit_face, traversal.py:484-511) over the same xor-linked
 // records; the entry face is the one opposite the recovered vertex i3.
 template <int L>
-__global__ void __launch_bounds__(kBlock) sctp_kernel(MeshView m, int64_t n, const float* __restrict__ o,
+#ifndef TB_SCTP_MIN_BLOCKS
+#define TB_SCTP_MIN_BLOCKS 6  // 80 registers (r01: 1 -> 92 regs, 6 -> +5 %, 8 -> spills)
+#endif
+__global__ void __launch_bounds__(kBlock, TB_SCTP_MIN_BLOCKS) sctp_kernel(MeshView m, int64_t n, const float* __restrict__ o,
                                                       const float* __restrict__ d,
                                                       const int32_t* __restrict__ start,
                                                       uint8_t* __restrict__ status, int32_t* __restrict__ cf,
@@ -983,6 +986,8 @@ __global__ void __launch_bounds__(kBlock) sctp_kernel(MeshView m, int64_t n, con
   for (int i = 0; i < 4; ++i) P[i] = ldg_f4(&m.pts[ids[i]]);
   const int j = sctp_exit(P, ids, O, D, -1, __ldg(&m.orient[cur]) != 0);
   w.drop(P, ids, j);
+  SctpEdges e;
+  window_edges(w, {O[0], O[1], O[2]}, {D[0], D[1], D[2]}, e);
   uint32_t ref = pick4u(__ldg(&m.sn[cur]), j);
   uint32_t prev = cur;
   int vis = 1;
@@ -993,7 +998,7 @@ __global__ void __launch_bounds__(kBlock) sctp_kernel(MeshView m, int64_t n, con
     if (ref & kConstrained) { st = kHit; break; }
     const uint32_t nxt = ref & kPayload;
     if (nxt >= n_tets) { st = kError; break; }
-    ref = sctp_advance<L>(m, w, O, D, nxt, prev);
+    ref = sctp_advance_cached<L>(m, w, e, O, D, nxt, prev);
     prev = nxt;
     cur = nxt;
     ++vis;
