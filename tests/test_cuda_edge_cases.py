@@ -116,3 +116,30 @@ def test_large_batch_ragged_sizes(REF):
         exp = REF.cast_rays(m, o, d, st)
         for a, b in zip(got, exp):
             assert np.array_equal(a, b), n
+
+
+@pytest.mark.parametrize("layout", ("tet20", "tet80"))
+def test_sctp_degenerate_and_extreme_rays_vs_c_oracle(layout):
+    """The edge-cached ScTP step decides faces from min / max of cached
+    values and must fall back to the exact per-face order whenever a value
+    is NaN: zero / NaN / inf / tiny / huge directions and far origins give
+    the C oracle's ScTP results bit for bit."""
+    from oracle import pyoracle
+    from paper_2103_02309_b200 import kernels as K
+    from paper_2103_02309_b200.ingestion import build_box_fixture
+    from paper_2103_02309_b200.scenes import interior_rays
+    from paper_2103_02309_b200.tetmesh import encode
+
+    raw, soup = build_box_fixture(4, occluders=[(0, 2, (1, 1), (3, 3))])
+    m = encode(raw, "tet20", soup)
+    o = np.full((8, 3), 1.3, np.float32)
+    d = np.array([[0, 0, 0], [np.nan, 1, 0], [np.inf, 0, 0], [0, 0, 1e-30], [1e30, 1, 1], [0, -0.0, 1],
+                  [1e-38, 1e-38, 1e-38], [-np.inf, np.inf, 1]], np.float32)
+    st = np.full(len(o), int(K.locate_points(m, o[:1].astype(np.float64), np.array([0], np.int32))[0][0]), np.int32)
+    ro, rd, rst = interior_rays(m, 4000, 77)
+    rd[::7] *= np.float32(1e-20)  # tiny directions: products underflow toward zero / subnormals
+    oo, dd, ss = (np.concatenate(a) for a in ((o, ro), (d, rd), (st, rst)))
+    got = K.cast_rays_full(m, oo, dd, ss, layout=layout, sctp=True)
+    exp = pyoracle.cast_rays_full(m, oo, dd, ss, layout=layout, sctp=True)
+    for k, a, b in zip(("status", "cf", "tet", "visited", "triangle", "t", "tet_back"), got, exp):
+        assert np.array_equal(a, b, equal_nan=(k == "t")), k
