@@ -12,12 +12,17 @@ PKG := paper_2103_02309_b200
 LIB := $(PKG)/libtetb200.so
 ORACLE := oracle/libtetoracle.so
 CSRC := $(PKG)/csrc/tetb200.cu
+HSRC := $(PKG)/csrc/host_mesh.cpp
 CHDR := $(PKG)/csrc/traverse.cuh $(PKG)/csrc/sctp.cuh include/tetb200.h
+CXX ?= g++
+# host mesh building: exact IEEE arithmetic like numpy (no contraction)
+CXXFLAGS := -O3 -std=c++17 -fPIC -ffp-contract=off -fno-fast-math -Wall
 
 all: $(LIB) $(ORACLE)
 
-$(LIB): $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)
+$(LIB): $(CSRC) $(HSRC) $(CHDR)
+	$(CXX) $(CXXFLAGS) -c -o $(PKG)/csrc/host_mesh.o $(HSRC)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC) $(PKG)/csrc/host_mesh.o
 
 $(ORACLE): oracle/tetoracle.c oracle/tetoracle.h
 	$(CC) -O3 -ffp-contract=off -fno-fast-math -fPIC -shared -pthread -Wall -o $@ oracle/tetoracle.c -lm

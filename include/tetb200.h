@@ -226,6 +226,32 @@ int tb_sctp_cast_rays_host(tb_mesh* mesh, int64_t n, const float* o, const float
 int tb_set_schedule(int mode, int steps_per_round);
 int tb_get_schedule(int* mode, int* steps_per_round);
 
+/* Host-side mesh building (plain C++, no GPU; csrc/host_mesh.cpp) -- the
+ * native backing of the Python mesh layer, bit-identical to the reference's
+ * numpy code paths it replaces.
+ *   tb_hilbert_keys      3-D Hilbert keys of (n,3) int64 grid cells, order
+ *                        1..20 (hilbert.py:14-58).
+ *   tb_hilbert_quantize  (n,3) float64 points -> grid cells of [lo, hi]
+ *                        (hilbert.py:66-73).
+ *   tb_tet_centroids     float64 centroid of each (t,4) quad, numpy mean order
+ *                        (tetmesh.py:466).
+ *   tb_build_side_tables sorted-slot side tables: row i of the output is row
+ *                        row_of[i] (NULL = i) of (verts, refs), vertex ids
+ *                        mapped through vert_map and plain tet references
+ *                        through tet_map (NULL = identity), slots stably
+ *                        sorted by vertex id (tetmesh.py:350-352, :482-491).
+ *   tb_pack_records      Tet32/20/16 records from the side tables
+ *                        (tetmesh.py:299-320).
+ * All return 0 or TB_E_ARG / TB_E_LAYOUT. */
+int tb_hilbert_keys(const int64_t* cells, int64_t n, int order, uint64_t* keys);
+int tb_hilbert_quantize(const double* pts, int64_t n, const double* lo, const double* hi, int order,
+                        int64_t* cells);
+int tb_tet_centroids(const double* pts, int64_t n_points, const int32_t* quads, int64_t n, double* out);
+int tb_build_side_tables(int64_t n, const int32_t* verts, const uint32_t* refs, const int64_t* row_of,
+                         const int64_t* vert_map, int64_t n_vert_map, const int64_t* tet_map,
+                         int64_t n_tet_map, int32_t* sv_out, uint32_t* sn_out);
+int tb_pack_records(int layout, int64_t n, const int32_t* sv, const uint32_t* sn, uint32_t* words);
+
 /* Pinned host memory helpers for end-to-end callers. */
 int tb_host_alloc(size_t bytes, void** out);
 int tb_host_free(void* ptr);

@@ -58,6 +58,11 @@ _SIGS = {
     "tb_shadow_rays_host": (c_int, [c_void_p, c_int64, P, P, c_int, P, P, c_int, c_double, P, P]),
     "tb_set_schedule": (c_int, [c_int, c_int]),
     "tb_get_schedule": (c_int, [POINTER(c_int), POINTER(c_int)]),
+    "tb_hilbert_keys": (c_int, [P, c_int64, c_int, P]),
+    "tb_hilbert_quantize": (c_int, [P, c_int64, P, P, c_int, P]),
+    "tb_tet_centroids": (c_int, [P, c_int64, P, c_int64, P]),
+    "tb_build_side_tables": (c_int, [c_int64, P, P, P, P, c_int64, P, c_int64, P, P]),
+    "tb_pack_records": (c_int, [c_int, c_int64, P, P, P]),
     "tb_host_alloc": (c_int, [c_size_t, POINTER(c_void_p)]),
     "tb_host_free": (c_int, [c_void_p]),
 }

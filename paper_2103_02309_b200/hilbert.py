@@ -1,76 +1,57 @@
-"""3-D Hilbert keys (J. Skilling, "Programming the Hilbert curve", AIP Conf.
-Proc. 707, 2004: AxesToTranspose + bit interleave).
+"""3-D Hilbert-curve keys for the locality reorder.
 
-Mirror of the reference's key function (/root/reference/pkg/src/tetray/
-hilbert.py:14-73) -- same grid, same key for every cell -- used by
-``tetmesh.reorder`` to sort points and tets along the curve.
+The keys are the reference's (``tetray.hilbert``, hilbert.py:14-73: Skilling's
+transpose construction on a 2**order grid, axis 0 most significant) -- the
+reorder permutation, and with it every tet id the GPU returns, depends on
+them bit for bit.  The arithmetic runs natively (``tb_hilbert_keys`` /
+``tb_hilbert_quantize`` in csrc/host_mesh.cpp, host code, no GPU needed);
+this module checks arguments and shapes.
 """
 
 from __future__ import annotations
 
 import numpy as np
 
+from ._lib import addr, check, lib
 
-def _axes_to_transpose(x: list[np.ndarray], order: int) -> None:
-    """In-place Skilling transform of three uint32 coordinate arrays."""
-    top = np.uint32(1 << (order - 1))
-    q = top
-    while q > 1:
-        mask = np.uint32(q - 1)
-        for i in range(3):
-            flip = (x[i] & q) != 0
-            # where bit q of x[i] is set: invert low bits of x[0];
-            # otherwise exchange the low bits of x[0] and x[i]
-            x[0] = np.where(flip, x[0] ^ mask, x[0])
-            swap = np.where(flip, np.uint32(0), (x[0] ^ x[i]) & mask)
-            x[0] ^= swap
-            x[i] ^= swap
-        q = np.uint32(q >> 1)
-    # Gray code
-    x[1] ^= x[0]
-    x[2] ^= x[1]
-    acc = np.zeros_like(x[0])
-    q = top
-    while q > 1:
-        acc = np.where((x[2] & q) != 0, acc ^ np.uint32(q - 1), acc)
-        q = np.uint32(q >> 1)
-    for i in range(3):
-        x[i] ^= acc
+MAX_ORDER = 20
 
 
-def hilbert_keys(cells: np.ndarray, order: int) -> np.ndarray:
-    """uint64 Hilbert key of each (n, 3) integer grid cell in [0, 2**order)."""
-    cells = np.asarray(cells)
-    if cells.ndim != 2 or cells.shape[1] != 3:
-        raise ValueError("cells must have shape (n, 3)")
-    if order < 1 or order > 20:
-        raise ValueError("order must be in 1..20")
-    lim = 1 << order
-    if cells.min(initial=0) < 0 or cells.max(initial=0) >= lim:
-        raise ValueError(f"grid coordinates must be in [0, {lim})")
-    x = [np.ascontiguousarray(cells[:, i]).astype(np.uint32) for i in range(3)]
-    _axes_to_transpose(x, order)
-    # interleave: bit b of axis 0 is the most significant of each triple
-    key = np.zeros(len(cells), dtype=np.uint64)
-    for b in range(order - 1, -1, -1):
-        triple = (
-            (((x[0] >> np.uint32(b)) & np.uint32(1)).astype(np.uint64) << np.uint64(2))
-            | (((x[1] >> np.uint32(b)) & np.uint32(1)).astype(np.uint64) << np.uint64(1))
-            | ((x[2] >> np.uint32(b)) & np.uint32(1)).astype(np.uint64)
-        )
-        key = (key << np.uint64(3)) | triple
-    return key
+def _cells_array(cells) -> np.ndarray:
+    a = np.asarray(cells)
+    if a.ndim != 2 or a.shape[1] != 3:
+        raise ValueError(f"expected an (n, 3) array of grid cells, got shape {a.shape}")
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def hilbert_keys(cells, order: int) -> np.ndarray:
+    """uint64 key per (n, 3) integer cell of the 2**order grid."""
+    if not 1 <= int(order) <= MAX_ORDER:
+        raise ValueError(f"order {order} outside 1..{MAX_ORDER}")
+    c = _cells_array(cells)
+    side = 1 << int(order)
+    if c.size and (int(c.min()) < 0 or int(c.max()) >= side):
+        raise ValueError(f"cells must lie in [0, {side}) for order {order}")
+    keys = np.empty(len(c), dtype=np.uint64)
+    if len(c):
+        check(lib.tb_hilbert_keys(addr(c), len(c), int(order), addr(keys)), "tb_hilbert_keys")
+    return keys
 
 
 def hilbert_index(cell, order: int) -> int:
-    return int(hilbert_keys(np.asarray(cell, dtype=np.int64)[None, :], order)[0])
+    """Key of a single cell."""
+    return int(hilbert_keys(np.reshape(np.asarray(cell, dtype=np.int64), (1, 3)), order)[0])
 
 
-def quantize(points: np.ndarray, lo, hi, order: int = 10) -> np.ndarray:
-    """Cells of the 2**order grid spanning [lo, hi] (hilbert.py:66-73 semantics)."""
-    points = np.asarray(points, dtype=np.float64)
-    lo = np.asarray(lo, dtype=np.float64)
-    hi = np.asarray(hi, dtype=np.float64)
-    extent = np.where(hi > lo, hi - lo, 1.0)
-    scaled = ((points - lo) / extent) * ((1 << order) - 1)
-    return np.clip(np.floor(scaled).astype(np.int64), 0, (1 << order) - 1)
+def quantize(points, lo, hi, order: int = 10) -> np.ndarray:
+    """(n, 3) cells of the 2**order grid spanning the box [lo, hi]; a flat
+    axis (hi <= lo) maps to extent 1, out-of-box points clamp to the border."""
+    if not 1 <= int(order) <= MAX_ORDER:
+        raise ValueError(f"order {order} outside 1..{MAX_ORDER}")
+    p = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 3))
+    box = [np.ascontiguousarray(np.broadcast_to(np.asarray(b, dtype=np.float64), (3,))) for b in (lo, hi)]
+    cells = np.empty((len(p), 3), dtype=np.int64)
+    if len(p):
+        check(lib.tb_hilbert_quantize(addr(p), len(p), addr(box[0]), addr(box[1]), int(order), addr(cells)),
+              "tb_hilbert_quantize")
+    return cells

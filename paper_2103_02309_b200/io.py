@@ -16,43 +16,39 @@ import numpy as np
 from .tetmesh import LAYOUT_DTYPES, CompactMesh, SceneTriangleSoup
 
 
+# The reference's .npz member names (cli.py:249-290) and where each lives on a
+# CompactMesh: a file written by either side loads on the other.
+_NPZ_ARRAYS = (
+    ("points", lambda m: m.points),
+    ("records", lambda m: m.records_u32()),
+    ("side_verts", lambda m: m.side_verts),
+    ("side_neighbors", lambda m: m.side_neighbors),
+    ("cf_triangle", lambda m: m.cf_triangle),
+    ("cf_tets", lambda m: m.cf_tets),
+    ("cf_verts", lambda m: m.cf_verts),
+    ("soup_vertices", lambda m: m.soup.vertices),
+    ("soup_triangles", lambda m: m.soup.triangles),
+    ("soup_materials", lambda m: m.soup.material_ids),
+)
+
+
 def save_compact(mesh: CompactMesh, path) -> None:
-    np.savez_compressed(
-        path,
-        layout=np.array(mesh.layout),
-        points=mesh.points,
-        records=mesh.records_u32(),
-        side_verts=mesh.side_verts,
-        side_neighbors=mesh.side_neighbors,
-        cf_triangle=mesh.cf_triangle,
-        cf_tets=mesh.cf_tets,
-        cf_verts=mesh.cf_verts,
-        source_tet=np.array(mesh.source_tet),
-        soup_vertices=mesh.soup.vertices,
-        soup_triangles=mesh.soup.triangles,
-        soup_materials=mesh.soup.material_ids,
-    )
+    """Write ``mesh`` in the reference's compressed .npz layout."""
+    members = {name: get(mesh) for name, get in _NPZ_ARRAYS}
+    members["layout"] = np.array(mesh.layout)
+    members["source_tet"] = np.array(mesh.source_tet)
+    np.savez_compressed(path, **members)
 
 
 def load_compact(path) -> CompactMesh:
-    data = np.load(path)
-    layout = str(data["layout"])
-    recs = np.ascontiguousarray(data["records"]).view(LAYOUT_DTYPES[layout]).reshape(-1)
-    soup = SceneTriangleSoup(
-        vertices=data["soup_vertices"], triangles=data["soup_triangles"], material_ids=data["soup_materials"]
-    )
-    return CompactMesh(
-        layout=layout,
-        points=np.ascontiguousarray(data["points"]),
-        records=recs,
-        side_verts=np.ascontiguousarray(data["side_verts"]),
-        side_neighbors=np.ascontiguousarray(data["side_neighbors"]),
-        cf_triangle=np.ascontiguousarray(data["cf_triangle"]),
-        cf_tets=np.ascontiguousarray(data["cf_tets"]),
-        cf_verts=np.ascontiguousarray(data["cf_verts"]),
-        source_tet=int(data["source_tet"]),
-        soup=soup,
-    )
+    """Read a .npz written by ``save_compact`` or the reference CLI."""
+    with np.load(path) as z:
+        arr = {name: np.ascontiguousarray(z[name]) for name, _ in _NPZ_ARRAYS}
+        layout = str(z["layout"])
+        source = int(z["source_tet"])
+    soup = SceneTriangleSoup(arr.pop("soup_vertices"), arr.pop("soup_triangles"), arr.pop("soup_materials"))
+    records = arr.pop("records").view(LAYOUT_DTYPES[layout]).reshape(-1)
+    return CompactMesh(layout=layout, records=records, source_tet=source, soup=soup, **arr)
 
 
 def load_device(path, device: int | None = None, layout: str | None = None):
