@@ -35,10 +35,12 @@ from .tetmesh import (
 
 
 class ParseError(Exception):
+    """A malformed input file: ``path``, the 1-based ``line_no`` (0 = the file
+    as a whole) and the reason, formatted as ``path:line: reason``."""
+
     def __init__(self, path, line_no, message):
-        super().__init__(f"{path}:{line_no}: {message}")
-        self.path = str(path)
-        self.line_no = line_no
+        self.path, self.line_no, self.reason = str(path), line_no, message
+        super().__init__(f"{self.path}:{line_no}: {message}")
 
 
 class AssociationError(Exception):
@@ -78,64 +80,47 @@ def kuhn_tets(n: int) -> np.ndarray:
 
 
 def _check_occluders(n, occluders):
-    occs = []
+    """Occluders as (axis, plane k, u0, v0, u1, v1): axis-aligned rectangles
+    of whole cell faces on an interior lattice plane 0 < k < n."""
+    checked = []
     for occ in occluders:
-        axis, k, (u0, v0), (u1, v1) = occ
-        ok = (
-            axis in (0, 1, 2)
-            and all(isinstance(x, (int, np.integer)) for x in (k, u0, v0, u1, v1))
-            and 1 <= k <= n - 1
-            and 0 <= u0 < u1 <= n
-            and 0 <= v0 < v1 <= n
-        )
-        if not ok:
+        axis, k, lo, hi = occ
+        coords = (k, *lo, *hi)
+        on_lattice = (axis in (0, 1, 2) and all(isinstance(x, (int, np.integer)) for x in coords)
+                      and 0 < k < n and all(0 <= a < b <= n for a, b in zip(lo, hi)))
+        if not on_lattice:
             raise ValueError(f"occluder {occ} is not on the interior cell-face lattice")
-        occs.append((int(axis), int(k), int(u0), int(v0), int(u1), int(v1)))
-    return occs
+        checked.append(tuple(int(x) for x in (axis, k, lo[0], lo[1], hi[0], hi[1])))
+    return checked
 
 
 def _box_soup(n: int, occs, walls: str) -> SceneTriangleSoup:
-    """Wall quads (2 big triangles each) then per-cell occluder squares, split
-    along the low->high diagonal; vertices de-duplicated in first-use order."""
-    verts: list = []
-    vid: dict = {}
-    tris: list = []
-    mats: list = []
-
-    def v(c):
-        key = (float(c[0]), float(c[1]), float(c[2]))
-        if key not in vid:
-            vid[key] = len(verts)
-            verts.append(key)
-        return vid[key]
-
-    def quad(axis, plane, u0, v0, u1, v1, mat):
-        a, b = _FREE_AXES[axis]
-
-        def pt(u, w):
-            c = [0.0, 0.0, 0.0]
-            c[axis] = float(plane)
-            c[a] = float(u)
-            c[b] = float(w)
-            return v(c)
-
-        p00, p10, p11, p01 = pt(u0, v0), pt(u1, v0), pt(u1, v1), pt(u0, v1)
-        tris.extend([(p00, p10, p11), (p00, p11, p01)])
-        mats.extend([mat, mat])
-
+    """The box scene: each wall as one quad (2 big triangles), then every
+    occluder cell face as its own quad; quads split along the low->high
+    diagonal, vertices numbered in order of first use."""
+    quads = []  # (axis, plane, u0, v0, u1, v1, material)
     if walls == "constrained":
-        for axis in range(3):
-            for plane in (0, n):
-                quad(axis, plane, 0, 0, n, n, 0)
+        quads += [(axis, plane, 0, 0, n, n, 0) for axis in range(3) for plane in (0, n)]
     for axis, k, u0, v0, u1, v1 in occs:
-        for u in range(u0, u1):
-            for w in range(v0, v1):
-                quad(axis, k, u, w, u + 1, w + 1, 1)
-    return SceneTriangleSoup(
-        vertices=np.asarray(verts, dtype=np.float64).reshape(-1, 3),
-        triangles=np.asarray(tris, dtype=np.int32).reshape(-1, 3),
-        material_ids=np.asarray(mats, dtype=np.int32),
-    )
+        quads += [(axis, k, u, w, u + 1, w + 1, 1) for u in range(u0, u1) for w in range(v0, v1)]
+    if not quads:
+        return SceneTriangleSoup(np.zeros((0, 3)), np.zeros((0, 3), np.int32), np.zeros(0, np.int32))
+    q = np.array(quads, dtype=np.int64)
+    # corners p00, p10, p11, p01 of each quad in (plane, u, v) coordinates
+    uv = np.stack([q[:, [2, 3]], q[:, [4, 3]], q[:, [4, 5]], q[:, [2, 5]]], axis=1)  # (Q, 4, 2)
+    free = np.array([_FREE_AXES[a] for a in range(3)])[q[:, 0]]  # (Q, 2) the in-plane axes
+    corners = np.empty((len(q), 4, 3), dtype=np.float64)
+    for ax in range(3):
+        corners[:, :, ax] = np.where((q[:, 0] == ax)[:, None], q[:, 1:2],
+                                     np.where((free[:, 0] == ax)[:, None], uv[:, :, 0], uv[:, :, 1]))
+    flat = corners.reshape(-1, 3)
+    uniq, first, inverse = np.unique(flat, axis=0, return_index=True, return_inverse=True)
+    rank = np.empty(len(uniq), dtype=np.int64)
+    rank[np.argsort(first, kind="stable")] = np.arange(len(uniq))
+    ids = rank[inverse.reshape(-1)].reshape(-1, 4)
+    tris = np.stack([ids[:, [0, 1, 2]], ids[:, [0, 2, 3]]], axis=1).reshape(-1, 3)
+    return SceneTriangleSoup(vertices=flat[first[np.argsort(first, kind="stable")]],
+                             triangles=tris.astype(np.int32), material_ids=np.repeat(q[:, 6], 2).astype(np.int32))
 
 
 def build_box_fixture(n: int, occluders=(), walls: str = "constrained"):
@@ -386,6 +371,23 @@ def _inside_2d(t2, area, q, tol):
     return ok
 
 
+def _projection_frames(tri):
+    """Per scene triangle: unit normal, the two axes kept when projecting
+    along its dominant normal axis, its projected corners and twice its
+    signed projected area."""
+    u = tri[:, 1] - tri[:, 0]
+    v = tri[:, 2] - tri[:, 0]
+    normal = np.cross(u, v)
+    length = np.sqrt((normal * normal).sum(axis=1))
+    if not np.all(length > 0):
+        raise AssociationError("degenerate scene triangle")
+    keep = np.array([[1, 2], [0, 2], [0, 1]])[np.abs(normal).argmax(axis=1)]  # (T, 2)
+    uk = np.take_along_axis(u, keep, axis=1)
+    vk = np.take_along_axis(v, keep, axis=1)
+    tri2 = np.take_along_axis(tri, keep[:, None, :], axis=2)  # (T, 3, 2)
+    return normal / length[:, None], keep, tri2, uk[:, 0] * vk[:, 1] - uk[:, 1] * vk[:, 0]
+
+
 def associate_constrained_faces(points, face_verts, soup: SceneTriangleSoup, tolerance: float = 1e-9) -> np.ndarray:
     """Scene triangle containing each constrained face (coplanar within
     tolerance, all three vertices inside; ties broken by strict containment
@@ -397,17 +399,7 @@ def associate_constrained_faces(points, face_verts, soup: SceneTriangleSoup, tol
         if len(face_verts):
             raise AssociationError("scene has no triangles")
         return np.zeros(0, dtype=np.int32)
-    n_t = np.cross(tri[:, 1] - tri[:, 0], tri[:, 2] - tri[:, 0])
-    n_len = np.linalg.norm(n_t, axis=1)
-    if np.any(n_len == 0):
-        raise AssociationError("degenerate scene triangle")
-    n_hat = n_t / n_len[:, None]
-    drop = np.argmax(np.abs(n_t), axis=1)
-    keep = np.array([[1, 2], [0, 2], [0, 1]])[drop]  # (T, 2)
-    tri2 = np.take_along_axis(tri, keep[:, None, :], axis=2)  # (T, 3, 2)
-    e1 = tri2[:, 1] - tri2[:, 0]
-    e2 = tri2[:, 2] - tri2[:, 0]
-    area2 = e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0]
+    n_hat, keep, tri2, area2 = _projection_frames(tri)
     T = len(tri)
     out = np.empty(len(face_verts), dtype=np.int32)
     chunk = max(1, 2_000_000 // (3 * T))
@@ -444,23 +436,26 @@ def associate_constrained_faces(points, face_verts, soup: SceneTriangleSoup, tol
 # TetGen / OBJ (ingestion.py:87-288)
 
 
-def _read_rows(path, min_cols, what):
-    rows = []
-    header = None
+def _records(path):
+    """(line number, tokens) of the non-blank lines of a TetGen file, with
+    '#' comments stripped."""
     with open(path) as fh:
         for line_no, line in enumerate(fh, start=1):
-            s = line.split("#", 1)[0].strip()
-            if not s:
-                continue
-            toks = s.split()
-            if header is None:
-                header = (line_no, toks)
-                continue
-            if len(toks) < min_cols:
-                raise ParseError(path, line_no, f"{what}: expected >= {min_cols} fields")
-            rows.append((line_no, toks))
+            toks = line.partition("#")[0].split()
+            if toks:
+                yield line_no, toks
+
+
+def _read_rows(path, min_cols, what):
+    """A TetGen table: its header line and the data rows after it."""
+    it = _records(path)
+    header = next(it, None)
     if header is None:
         raise ParseError(path, 0, f"{what}: empty file")
+    rows = list(it)
+    short = [ln for ln, toks in rows if len(toks) < min_cols]
+    if short:
+        raise ParseError(path, short[0], f"{what}: expected >= {min_cols} fields")
     return header, rows
 
 
@@ -551,34 +546,37 @@ def mark_constrained(raw: RawTetMesh, face_triples, face_path="<faces>") -> None
     raw.cf_verts = keys_sorted.astype(np.int32)
 
 
+def _obj_index(tok: str, n_verts: int) -> int:
+    """0-based vertex of an OBJ face token ("i", "i/t", "i/t/n"; i < 0 counts back)."""
+    i = int(tok.split("/", 1)[0])
+    return i - 1 if i > 0 else n_verts + i
+
+
 def load_obj(path) -> SceneTriangleSoup:
-    """OBJ subset (v/f, fan triangulation, 1-based or negative indices)."""
-    verts, tris = [], []
+    """The triangles of an OBJ file (``v`` / ``f`` records, polygons fanned
+    from their first corner, 1-based or negative indices)."""
+    verts: list = []
+    tris: list = []
     with open(path) as fh:
         for line_no, line in enumerate(fh, start=1):
-            t = line.split()
-            if not t or t[0].startswith("#"):
-                continue
-            if t[0] == "v":
-                if len(t) < 4:
+            kind, *args = line.split() or ["#"]
+            if kind == "v":
+                if len(args) < 3:
                     raise ParseError(path, line_no, "vertex needs 3 coordinates")
-                verts.append([float(t[1]), float(t[2]), float(t[3])])
-            elif t[0] == "f":
-                if len(t) < 4:
+                verts.append(tuple(float(x) for x in args[:3]))
+            elif kind == "f":
+                if len(args) < 3:
                     raise ParseError(path, line_no, "face needs >= 3 vertices")
-                ids = [int(x.split("/")[0]) for x in t[1:]]
-                ids = [i - 1 if i > 0 else len(verts) + i for i in ids]
-                if min(ids) < 0 or max(ids) >= len(verts):
+                corner = [_obj_index(a, len(verts)) for a in args]
+                if not all(0 <= c < len(verts) for c in corner):
                     raise ParseError(path, line_no, "face index out of range")
-                for k in range(1, len(ids) - 1):
-                    tris.append((ids[0], ids[k], ids[k + 1]))
-    vertices = np.asarray(verts, dtype=np.float64).reshape(-1, 3)
-    triangles = np.asarray(tris, dtype=np.int32).reshape(-1, 3)
-    if len(triangles):
-        c = vertices[triangles]
-        if np.any(np.linalg.norm(np.cross(c[:, 1] - c[:, 0], c[:, 2] - c[:, 0]), axis=1) == 0):
-            raise ParseError(path, 0, "degenerate (zero-area) triangle in file")
-    return SceneTriangleSoup(vertices=vertices, triangles=triangles, material_ids=np.zeros(len(triangles), dtype=np.int32))
+                tris += [(corner[0], corner[k], corner[k + 1]) for k in range(1, len(corner) - 1)]
+    vertices = np.array(verts, dtype=np.float64).reshape(-1, 3)
+    triangles = np.array(tris, dtype=np.int32).reshape(-1, 3)
+    corners = vertices[triangles]
+    if len(triangles) and not np.all(np.cross(corners[:, 1] - corners[:, 0], corners[:, 2] - corners[:, 0]).any(axis=1)):
+        raise ParseError(path, 0, "degenerate (zero-area) triangle in file")
+    return SceneTriangleSoup(vertices=vertices, triangles=triangles, material_ids=np.zeros(len(triangles), np.int32))
 
 
 __all__ = [
