@@ -245,6 +245,48 @@ def algorithmic_bytes(visited: np.ndarray, layout: str) -> int:
     return int(((v - 1) * (L + point)).sum() + 68 * len(v) + 53 * len(v))
 
 
+def l2_gather_roof(dm, stream, flush, layout: str, walk_steps: float, achieved_gbs: float) -> dict:
+    """for meshes that fit in L2, the walk's algorithmic bytes
+    against a measured random-gather roof of the same mesh -- tb_probe_gather
+    issues one step's loads (record + axis-permuted point) at independent
+    pseudo-random indices, 8 per thread in flight, L2 flushed before each
+    rep like the timed steps."""
+    import torch
+
+    from paper_2103_02309_b200._lib import check, lib
+
+    L = {"tet32": 32, "tet20": 20, "tet16": 16}[layout]
+    n_pairs = int(min(max(32 << 20, walk_steps), 256 << 20))
+    sink = torch.zeros(1, dtype=torch.int32, device=flush.device)
+
+    def probe():
+        check(lib.tb_probe_gather(dm.handle, n_pairs, 12345, sink.data_ptr(), stream.cuda_stream), "tb_probe_gather")
+
+    for _ in range(2):
+        probe()
+    ms = []
+    for _ in range(5):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        probe()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    t = float(np.median(ms)) / 1e3
+    peak = n_pairs * (L + 12) / t / 1e9
+    l2 = torch.cuda.get_device_properties(flush.device).L2_cache_size
+    resident = dm.hot_bytes <= l2
+    return {"bound": "l2_gather", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+            "frac": achieved_gbs / peak,
+            "probe": {"kernel": f"gather_probe_kernel<{L}>", "pairs": n_pairs, "bytes_per_pair": L + 12,
+                      "ms": t * 1e3, "working_set_bytes": int(dm.hot_bytes), "l2_bytes": int(l2)},
+            "note": ("peak = random (record, point) gathers over this mesh's hot arrays "
+                     + ("(L2 resident)" if resident else "(larger than L2: an HBM random-gather roof)")
+                     + "; the walk exceeds it when coherent rays share L1/L2 lines (frac > 1) -- its binding "
+                       "roof is roofline_issue")}
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -622,6 +664,9 @@ def run_ours(args, cfg):
                               "sass_per_step": per_step, "sms": sms, "sm_mhz": clk_mhz,
                               "note": "peak = SMs x 4 schedulers x clock x 32 lanes / SASS per walk step; "
                                       "the gap is init/epilogue, SIMT divergence, latency and the tail"}
+    roofline_l2 = None
+    if not sctp and cfg["layout"] != "tet80" and not args.no_l2_probe:
+        roofline_l2 = l2_gather_roof(dm, stream, flush, cfg["layout"], (vis_sum - total_rays) / world, achieved)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -662,6 +707,7 @@ def run_ours(args, cfg):
                              "gathers are served by L1/L2 (ncu: DRAM traffic is a few % of them), so frac "
                              "can exceed 1 -- the binding roofline is roofline_issue"},
         "roofline_issue": roofline_issue,
+        "roofline_l2": roofline_l2,
         "clocks": dict(clocks.summary(clocks.t_ramp, clocks.t_end), window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
         "gpu_launches": args.steps * (1 if fg is None else sum(1 for a, b in fg.my_pieces() if b > a)),
         "parity": parity,
@@ -709,6 +755,7 @@ def main():
     ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512"),
                     help="ray-to-lane schedule of the timed trace (default: compact for secondaries, else lane)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-l2-probe", action="store_true", help="skip the L2 gather-roof probe (roofline_l2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2_073_600)
     ap.add_argument("--ramp-s", type=float, default=0.5, help="untimed load before the timed region (clock ramp)")

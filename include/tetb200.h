@@ -101,6 +101,16 @@ int tb_mesh_info(const tb_mesh* mesh, int* device, int* layout, int64_t* n_point
  * undefined, as in the reference). */
 int tb_mesh_validated(const tb_mesh* mesh, int* validated);
 
+/* Measurement helper (no reference counterpart; SURVEY 8 d asks the roofline
+ * to be reported against a measured L2 gather bandwidth when the hot arrays
+ * fit in L2).  Gathers n_pairs (record, point) pairs of this mesh at
+ * independent pseudo-random indices -- the loads of one walk step, 8 pairs
+ * in flight per thread -- so (layout + 12) * n_pairs / kernel time is the
+ * random-gather roof of this mesh's working set.  Layouts 16/20/32 only.
+ * sink: one device uint32 (practically never written).  Asynchronous on
+ * stream; time it with events on that stream. */
+int tb_probe_gather(tb_mesh* mesh, int64_t n_pairs, uint32_t seed, uint32_t* sink, void* stream);
+
 /* Batch traversal with the batch-layer epilogue fused.
  * Replaces: _kernels.cast_rays (_kernels.pyx:271-370) -> (status, cf, tet,
  *   visited), plus batch.cast_rays' host epilogue (batch.py:57-71 and

@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_size_t, c_void_p
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_size_t, c_uint32, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TETB200_LIB", os.path.join(_HERE, "libtetb200.so"))
@@ -38,6 +38,7 @@ _SIGS = {
          POINTER(c_int64), POINTER(c_int64)],
     ),
     "tb_mesh_validated": (c_int, [c_void_p, POINTER(c_int)]),
+    "tb_probe_gather": (c_int, [c_void_p, c_int64, c_uint32, P, c_void_p]),
     "tb_cast_rays": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),
     "tb_cast_rays_sched": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_int, c_void_p]),
     "tb_cast_rays_scatter": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, P, c_void_p]),

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <string>
@@ -1167,6 +1168,55 @@ struct SctpL {
   static void launch(unsigned g, cudaStream_t s, A... a) { sctp_kernel<L><<<g, kBlock, 0, s>>>(a...); }
 };
 
+// L2 gather roof for the walk's access shape (SURVEY 8 d: "report against a
+// measured L2 gather bandwidth" when the hot arrays fit in L2).  Each pair is
+// one step's worth of gathers at independent pseudo-random indices: the
+// layout's record words (exactly the loads Record<L>::load issues) and one
+// float4 of a random axis-permuted point copy, 8 pairs in flight per thread
+// so the loads are never latency-serialised.  Algorithmic bytes per pair
+// = L + 12, the same per-step figure the bench's roofline counts.
+__device__ __forceinline__ uint32_t probe_hash(uint32_t x) {
+  x ^= x >> 16; x *= 0x7FEB352Du;
+  x ^= x >> 15; x *= 0x846CA68Bu;
+  return x ^ (x >> 16);
+}
+
+__device__ __forceinline__ uint32_t fold4(const uint4& u) { return u.x ^ u.y ^ u.z ^ u.w; }
+
+template <int L>
+__device__ __forceinline__ uint32_t probe_fold(const Record<L>& r) {
+  if constexpr (L == 16) return fold4(r.r);
+  else if constexpr (L == 20) return r.v ^ fold4(r.n);
+  else return fold4(r.a) ^ fold4(r.n);
+}
+
+template <int L>
+__global__ void __launch_bounds__(256) gather_probe_kernel(MeshView m, int64_t n_pairs, uint32_t seed,
+                                                           uint32_t* __restrict__ sink) {
+  constexpr int kInFlight = 8;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nt = (uint32_t)m.n_tets, np6 = (uint32_t)(m.n_points * 6);
+  uint32_t acc = 0;
+  auto pair = [&](int64_t i) {
+    const uint32_t h = probe_hash((uint32_t)i * 2u + seed);
+    Record<L> r;
+    r.load(m, __umulhi(h, nt));
+    const float4 q = __ldg(&m.pts[__umulhi(probe_hash(h ^ 0x5bd1e995u), np6)]);
+    return probe_fold<L>(r) ^ __float_as_uint(q.x) ^ __float_as_uint(q.y) ^ __float_as_uint(q.z);
+  };
+  const int64_t groups = n_pairs / kInFlight;
+  for (int64_t g = tid; g < groups; g += nthreads) {
+    uint32_t v[kInFlight];
+#pragma unroll
+    for (int k = 0; k < kInFlight; ++k) v[k] = pair(g * kInFlight + k);  // all loads issued before any use
+#pragma unroll
+    for (int k = 0; k < kInFlight; ++k) acc ^= v[k];
+  }
+  if (tid < n_pairs - groups * kInFlight) acc ^= pair(groups * kInFlight + tid);
+  if (acc == 0x9E3779B9u) atomicXor(sink, acc);  // keeps the loads live; practically never stores
+}
+
 int check_mesh(const tb_mesh* m) {
   if (m == nullptr) return set_error(TB_E_ARG, "mesh handle is NULL");
   return TB_OK;
@@ -1366,6 +1416,28 @@ int tb_mesh_validated(const tb_mesh* m, int* validated) {
   if (int e = check_mesh(m)) return e;
   if (!validated) return set_error(TB_E_ARG, "validated is NULL");
   *validated = m->safe ? 1 : 0;
+  return TB_OK;
+}
+
+int tb_probe_gather(tb_mesh* m, int64_t n_pairs, uint32_t seed, uint32_t* sink, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n_pairs < 0) return set_error(TB_E_ARG, "negative pair count");
+  if (!sink) return set_error(TB_E_ARG, "sink is NULL");
+  if (n_pairs == 0 || m->n_tets == 0 || m->n_points == 0) return TB_OK;
+  DeviceGuard g(m->device);
+  int sms = 0;
+  TB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device));
+  const unsigned grid = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)sms * 16, (n_pairs + 256 * 8 - 1) / (256 * 8)));
+  const cudaStream_t s = (cudaStream_t)stream;
+  const MeshView v = m->view();
+  switch (m->layout) {
+    case 32: gather_probe_kernel<32><<<grid, 256, 0, s>>>(v, n_pairs, seed, sink); break;
+    case 20: gather_probe_kernel<20><<<grid, 256, 0, s>>>(v, n_pairs, seed, sink); break;
+    case 16: gather_probe_kernel<16><<<grid, 256, 0, s>>>(v, n_pairs, seed, sink); break;
+    default: return set_error(TB_E_LAYOUT, "gather probe: layout %d has no separate point array", m->layout);
+  }
+  TB_CUDA(cudaGetLastError());
   return TB_OK;
 }
 

@@ -98,7 +98,10 @@ class DeviceMesh:
         return LAYOUT_CODES[self.layout]
 
     def close(self) -> None:
+        """Free the device copy now; later calls through this object fail
+        loudly (NULL handle) instead of touching freed memory."""
         self._finalizer()
+        self.handle = ctypes.c_void_p()
 
 
 def _fingerprint(mesh):
@@ -132,19 +135,20 @@ def device_mesh(mesh, device: int | None = None, layout: str | None = None) -> D
 
 
 def _evict(key) -> None:
+    # the host mesh died: forget the cache entry.  The device copy itself is
+    # freed by DeviceMesh's own finalizer once no caller holds it any more
+    # (a caller may keep using a DeviceMesh after its host mesh is gone).
     with _lock:
-        hit = _cache.pop(key, None)
-    if hit is not None:
-        hit[0].close()
+        _cache.pop(key, None)
 
 
 def invalidate(mesh) -> None:
-    """Drop every cached device copy of ``mesh`` (after in-place mutation)."""
+    """Drop every cached device copy of ``mesh`` (after in-place mutation):
+    the next ``device_mesh(mesh)`` uploads again.  DeviceMesh objects already
+    handed out stay valid until released."""
     with _lock:
-        keys = [k for k in _cache if k[0] == id(mesh)]
-        hits = [_cache.pop(k) for k in keys]
-    for dm, _ in hits:
-        dm.close()
+        for k in [k for k in _cache if k[0] == id(mesh)]:
+            _cache.pop(k)
 
 
 __all__ = ["DeviceMesh", "device_mesh", "invalidate", "default_device", "LAYOUT_CODES", "_lib"]

@@ -106,3 +106,67 @@ def test_cast_rays_sched_validates_arguments():
     fake = ctypes.c_void_p(1)  # never dereferenced: the schedule is checked first
     assert lib.tb_cast_rays_sched(fake, 1, *args, 9, None) == -1
     assert b"schedule" in lib.tb_last_error()
+
+
+def test_probe_gather_validates_arguments():
+    from paper_2103_02309_b200._lib import lib
+
+    assert lib.tb_probe_gather(None, 1, 0, None, None) == -1
+    assert b"NULL" in lib.tb_last_error()
+
+
+@pytest.mark.gpu
+def test_probe_gather_runs_per_layout(golden):
+    """tb_probe_gather (the L2 gather roof bench.py reports) runs on every
+    point-array layout and refuses TetMesh-80, which has none."""
+    import torch
+
+    from conftest import golden_mesh
+    from paper_2103_02309_b200._lib import lib
+    from paper_2103_02309_b200.device import device_mesh
+    from paper_2103_02309_b200.tetmesh import relayout
+
+    base = golden_mesh(golden, "box4", "tet32")
+    sink = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for layout in ("tet32", "tet20", "tet16"):
+        dm = device_mesh(relayout(base, layout))
+        assert lib.tb_probe_gather(dm.handle, 100_003, 7, sink.data_ptr(), None) == 0, lib.tb_last_error()
+        assert lib.tb_probe_gather(dm.handle, -1, 7, sink.data_ptr(), None) == -1
+    torch.cuda.synchronize()
+    dm80 = device_mesh(base, layout="tet80")
+    assert lib.tb_probe_gather(dm80.handle, 10, 7, sink.data_ptr(), None) != 0
+    assert b"layout" in lib.tb_last_error()
+
+
+@pytest.mark.gpu
+def test_device_mesh_outlives_its_host_mesh(golden):
+    """A DeviceMesh stays valid after the host mesh it was uploaded from is
+    collected (the cache entry goes, the device copy stays while held)."""
+    import gc
+
+    import numpy as np
+
+    from conftest import golden_mesh
+    from paper_2103_02309_b200.device import device_mesh
+    from paper_2103_02309_b200.tetmesh import relayout
+    from paper_2103_02309_b200.trace import trace
+
+    import torch
+
+    base = golden_mesh(golden, "box4", "tet32")
+    dm = device_mesh(relayout(base, "tet16"))  # the relayouted host mesh dies here
+    gc.collect()
+    n = 64
+    o = torch.full((n, 3), 0.5, dtype=torch.float32, device="cuda") + torch.rand(n, 3, device="cuda")
+    d = torch.randn(n, 3, device="cuda")
+    from paper_2103_02309_b200.trace import locate
+
+    st, _ = locate(dm, o.double(), torch.full((n,), base.source_tet, dtype=torch.int32, device="cuda"))
+    res = trace(dm, o, d, st.clamp(min=0))
+    torch.cuda.synchronize()
+    assert int(res.status.max()) <= 1
+    dm.close()
+    from paper_2103_02309_b200._lib import TetB200Error
+
+    with pytest.raises(TetB200Error):
+        trace(dm, o, d, st.clamp(min=0))
