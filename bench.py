@@ -350,11 +350,14 @@ def run_ours(args, cfg):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     gidx = torch.from_numpy(idx).to(dev)
 
-    # ray schedule: one ray per lane everywhere -- since the PTX step it also
-    # beats block compaction on the incoherent config-4 secondaries (r01:
-    # 2.38 vs 2.30 Grays/s; profiles/r01_experiments.md).  --schedule or
+    # ray schedule: one ray per lane for primaries; incoherent secondaries
+    # (config 4) are binned by direction octant first and walked in binned
+    # order (r01: 2.61 vs 2.38 Grays/s one ray per lane, 2.30 block
+    # compaction; profiles/r01_experiments.md) -- what a renderer's bounce
+    # pass selects with trace(schedule="binned").  --schedule or
     # TETB200_SCHED (sweeps, via the process-wide "auto" setting) override.
-    schedule = args.schedule or ("auto" if os.environ.get("TETB200_SCHED") else "lane")
+    schedule = args.schedule or ("auto" if os.environ.get("TETB200_SCHED") else
+                                 ("binned" if cfg.get("secondaries") else "lane"))
 
     def step():
         trace(dm, go, gd, gs, out=res, stream=stream, sctp=sctp, schedule=schedule)
@@ -552,7 +555,7 @@ def run_ours(args, cfg):
     # incoherent secondaries of this frame (BASELINE's metric names primary
     # AND incoherent secondary rays): diffuse bounces from this rank's
     # primary hits (render.py:353-359 semantics, seed 4), traced on the
-    # device with the compacting schedule, same timing protocol; checked on
+    # device under each schedule, same timing protocol; checked on
     # a strided sample against the oracle.
     secondary = None
     if not args.no_secondary and not cfg.get("secondaries") and not sctp and world == 1:
@@ -566,7 +569,7 @@ def run_ours(args, cfg):
             g2 = [torch.from_numpy(a).to(dev) for a in (so, sd, sst)]
             r2 = empty_result(ns, dev)
             sec = {}
-            for sched2 in ("compact", "lane"):
+            for sched2 in ("compact", "lane", "binned"):
                 for _ in range(args.warmup):
                     flush.zero_()
                     trace(dm, *g2, out=r2, stream=stream, schedule=sched2)
@@ -593,8 +596,10 @@ def run_ours(args, cfg):
                 mism2 = int(sum(np.count_nonzero(a != b) for a, b in zip(got2, exp2)))
                 par2 = {"vs": f"C oracle on every {stride}th ray", "rays_checked": int(len(exp2[0])),
                         "bit_exact": mism2 == 0}
-            secondary = {"value": ns / sec["lane"] / 1e3, "unit": "Mrays/s", "rays": ns,
-                         "kernel_ms": sec["lane"], "schedule": "lane",
+            secondary = {"value": ns / sec["binned"] / 1e3, "unit": "Mrays/s", "rays": ns,
+                         "kernel_ms": sec["binned"], "schedule": "binned",
+                         "note": "direction-octant counting sort + the walk in binned order, both inside the events",
+                         "one_ray_per_lane": {"value": ns / sec["lane"] / 1e3, "kernel_ms": sec["lane"]},
                          "block_compaction": {"value": ns / sec["compact"] / 1e3, "kernel_ms": sec["compact"]},
                          "tets_visited_per_ray": {"mean": float(v2.mean()), "max": int(v2.max())},
                          "rays_from": "diffuse hemisphere bounces of this frame's primary hits (seed 4)",
@@ -702,14 +707,17 @@ def run_ours(args, cfg):
                      "algorithmic_bytes_per_launch": alg,
                      "kernel": (f"sctp_kernel<{cfg['layout'][3:]}>" if sctp else
                                 f"{'cast_compact_kernel' if schedule in ('compact', 'compact512') else 'cast_kernel'}"
-                                f"<{cfg['layout'][3:]}>"),
+                                f"<{cfg['layout'][3:]}>"
+                                + (" after bin_count/bin_scan/bin_scatter (direction binning, inside the events)"
+                                   if schedule == "binned" else "")),
                      "note": "algorithmic gather bytes (SURVEY s8d) over the HBM copy peak; the walk's "
                              "gathers are served by L1/L2 (ncu: DRAM traffic is a few % of them), so frac "
                              "can exceed 1 -- the binding roofline is roofline_issue"},
         "roofline_issue": roofline_issue,
         "roofline_l2": roofline_l2,
         "clocks": dict(clocks.summary(clocks.t_ramp, clocks.t_end), window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
-        "gpu_launches": args.steps * (1 if fg is None else sum(1 for a, b in fg.my_pieces() if b > a)),
+        "gpu_launches": args.steps * (1 if fg is None else sum(1 for a, b in fg.my_pieces() if b > a))
+        * (4 if schedule == "binned" else 1),  # binned: count, scan, scatter, walk
         "parity": parity,
         "e2e": e2e,
         "e2e_render": e2e_render,
@@ -752,7 +760,7 @@ def main():
     ap.add_argument("--gather", choices=("p2p", "nccl"), default="p2p",
                     help="N > 1 frame assembly: fused P2P stores (default) or the chunked NCCL gather")
     ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1: trace/gather pipeline depth per step")
-    ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512"),
+    ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512", "binned"),
                     help="ray-to-lane schedule of the timed trace (default: compact for secondaries, else lane)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-l2-probe", action="store_true", help="skip the L2 gather-roof probe (roofline_l2)")

@@ -230,7 +230,12 @@ int tb_sctp_cast_rays_host(tb_mesh* mesh, int64_t n, const float* o, const float
  *   mode 0 = auto (= one ray per lane), 1 = one ray per lane, 2 = per-lane
  *   persistent refill,
  *   3 / 4 = block compaction (256 / 512 threads per block) for incoherent
- *   batches; steps_per_round = walk steps between compactions (>= 1).
+ *   batches; steps_per_round = walk steps between compactions (>= 1),
+ *   6 = direction binning: a stable counting sort of the rays by direction
+ *   octant into stream-ordered scratch (36 B / ray), then one ray per lane
+ *   over the binned copies with results stored at the original indices --
+ *   for incoherent device-resident batches (n < 2^31; host-ray zero-copy
+ *   calls run one ray per lane).  5 is unused. 
  * Process-wide; overrides TETB200_SCHED / TETB200_ROUND.  A negative
  * argument leaves that setting unchanged. */
 int tb_set_schedule(int mode, int steps_per_round);

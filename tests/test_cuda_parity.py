@@ -347,7 +347,7 @@ def schedule():
 
 
 @pytest.mark.parametrize("mode,rounds", [("lane", 16), ("refill", 16), ("compact", 1), ("compact", 7),
-                                          ("compact", 16), ("compact512", 32)])
+                                          ("compact", 16), ("compact512", 32), ("binned", 16)])
 @pytest.mark.parametrize("layout", LAYOUTS4)
 def test_schedules_identical_results(golden, digests, K, O, schedule, mode, rounds, layout):
     """Every ray-to-lane schedule (one ray per lane, per-lane refill, block
@@ -368,7 +368,7 @@ def test_schedules_identical_results(golden, digests, K, O, schedule, mode, roun
                 assert np.array_equal(a, b[:n]), (k, n)
 
 
-@pytest.mark.parametrize("mode", ("compact", "compact512", "refill"))
+@pytest.mark.parametrize("mode", ("compact", "compact512", "refill", "binned"))
 def test_schedules_cycle_guard(digests, K, O, schedule, mode):
     """Guard rays (status 2, visited = n_tets + 1) through the compacting
     scheduler, on the lattice camera and on the Brent fast-forward mesh."""
@@ -394,7 +394,7 @@ def test_schedules_cycle_guard(digests, K, O, schedule, mode):
         assert np.array_equal(a, b), k
 
 
-@pytest.mark.parametrize("schedule", ("lane", "refill", "compact", "compact512"))
+@pytest.mark.parametrize("schedule", ("lane", "refill", "compact", "compact512", "binned"))
 def test_trace_schedule_argument(golden, K, O, schedule):
     """trace(schedule=...) on device tensors (tb_cast_rays_sched) equals the
     oracle for an incoherent batch larger than one wave of blocks."""

@@ -99,8 +99,11 @@ def main(argv):
     sass = subprocess.run(["cuobjdump", "-sass", str(lib)], capture_output=True, text=True, check=True).stdout
     res = {}
     for name, ins in functions(sass):
-        m = re.search(r"(cast_kernel|cast_compact_kernel|sctp_kernel|shadow_kernel)ILi(\d+)E(?:Li\d+E)?(Lb[01]E)?", name)
+        m = re.search(r"(cast_kernel|cast_compact_kernel|sctp_kernel|shadow_kernel)ILi(\d+)E(?:Li\d+E)?(Lb[01]E)?"
+                      r"((?:Lb[01]E)*)", name)
         if not m:
+            continue
+        if "Lb1E" in m.group(4):  # host-ray / scatter / gather variants: the device-ray kernel is the reference
             continue
         key = f"{m.group(1)}<{m.group(2)}{'' if not m.group(3) else (', clamp' if m.group(3) == 'Lb1E' else ', validated')}>"
         if key in res:
