@@ -280,20 +280,41 @@ class PeerFrameGather:
         self.remote = None
         dev_idx = self.device.index if self.device.index is not None else torch.cuda.current_device()
         handle = None
+        err = None
         if rank == root:
-            p = ctypes.c_void_p()
-            check(lib.tb_device_alloc(self.bytes, dev_idx, ctypes.byref(p)), "tb_device_alloc")
-            self.base = p.value
-            buf = (ctypes.c_char * 64)()
-            check(lib.tb_ipc_get_handle(self.base, buf), "tb_ipc_get_handle")
-            handle = bytes(buf)
+            try:
+                p = ctypes.c_void_p()
+                check(lib.tb_device_alloc(self.bytes, dev_idx, ctypes.byref(p)), "tb_device_alloc")
+                self.base = p.value
+                buf = (ctypes.c_char * 64)()
+                check(lib.tb_ipc_get_handle(self.base, buf), "tb_ipc_get_handle")
+                handle = bytes(buf)
+            except Exception as exc:  # every rank must learn of it (below), not hang in the broadcast
+                err = repr(exc)
         obj = [handle]
         src = dist.get_global_rank(group, root) if group is not None else root
         dist.broadcast_object_list(obj, src=src, group=group)
-        if rank != root:
-            p = ctypes.c_void_p()
-            check(lib.tb_ipc_open(obj[0], dev_idx, ctypes.byref(p)), "tb_ipc_open")
-            self.remote = p.value
+        if rank != root and obj[0] is not None:
+            try:
+                p = ctypes.c_void_p()
+                check(lib.tb_ipc_open(obj[0], dev_idx, ctypes.byref(p)), "tb_ipc_open")
+                self.remote = p.value
+            except Exception as exc:
+                err = repr(exc)
+        # collective verdict: either every rank has the shared block or all
+        # of them give it up together (callers then fall back to FrameGather)
+        verdicts = [None] * dist.get_world_size(group)
+        dist.all_gather_object(verdicts, err, group=group)
+        failed = [v for v in verdicts if v is not None]
+        if failed or obj[0] is None:
+            if self.remote is not None:
+                lib.tb_ipc_close(self.remote)
+                self.remote = None
+            dist.barrier(group=group)
+            if self.base is not None:
+                lib.tb_device_free(self.base)
+                self.base = None
+            raise RuntimeError(f"peer frame assembly unavailable: {failed[0] if failed else 'no IPC handle'}")
         dest = self.base if rank == root else self.remote
         self.ptrs = [dest + o for o in self.offsets]
         self.frame = None

@@ -160,3 +160,31 @@ def test_split_chunks():
     assert multigpu.split_chunks(10, 3) == [(0, 3), (3, 6), (6, 10)]
     assert multigpu.split_chunks(2, 4) == [(0, 0), (0, 1), (1, 1), (1, 2)]
     assert multigpu.split_chunks(0, 2) == [(0, 0), (0, 0)]
+
+
+def _peer_fail_worker(rank, world, port, result_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # no GPU here: the root's device allocation fails; every rank must
+        # raise together (the bench then falls back to FrameGather) instead of
+        # the others waiting forever for an IPC handle
+        try:
+            multigpu.PeerFrameGather(32, 16, world, rank, world, "cpu:0")
+            outcome = "constructed"
+        except RuntimeError as exc:
+            outcome = "raised" if "peer frame assembly unavailable" in str(exc) else f"other: {exc}"
+        flags = [None] * world
+        dist.all_gather_object(flags, outcome)
+        if rank == 0:
+            with open(result_path, "w") as fh:
+                fh.write(",".join(flags))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_peer_gather_failure_is_collective(tmp_path):
+    path = str(tmp_path / "result.txt")
+    mp.start_processes(_peer_fail_worker, args=(2, _free_port(), path), nprocs=2, start_method="spawn", join=True)
+    assert open(path).read() == "raised,raised"
