@@ -1128,7 +1128,7 @@ struct CastPersistL {
 // reads the binned copies and the epilogue stores each result at its
 // original index (cast_kernel's kScatter path), so outputs are unchanged.
 // r01 (config 4, 16.7 M diffuse secondaries): the walk 7.14 -> 6.47 ms.
-constexpr int kBinTile = 2048;    // rays per binning block
+constexpr int kBinTile = 4096;    // rays per binning block
 constexpr int kBinThreads = 256;  // 8 warps; one ray per thread per round
 
 __device__ __forceinline__ int dir_octant(const float* __restrict__ d, int64_t r) {
@@ -1161,26 +1161,40 @@ __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(const float* __r
   if (threadIdx.x < 8) hist[(int64_t)threadIdx.x * n_tiles + blockIdx.x] = cnt[threadIdx.x];
 }
 
-// In-place exclusive scan of hist[0..len) by one block (len = 8 * n_tiles).
+// In-place exclusive scan of hist[0..len) by one block (len = 8 * n_tiles):
+// coalesced 1024-entry chunks, warp-shuffle scans, a running carry.
 __global__ void __launch_bounds__(1024) bin_scan_kernel(int32_t* __restrict__ hist, int64_t len) {
-  __shared__ int64_t part[1024];
-  const int64_t per = (len + 1023) / 1024;
-  const int64_t lo = threadIdx.x * per, hi = lo + per < len ? lo + per : len;
-  int64_t sum = 0;
-  for (int64_t i = lo; i < hi; ++i) sum += hist[i];
-  part[threadIdx.x] = sum;
+  __shared__ int32_t warp_sum[32];
+  __shared__ int32_t carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {  // Hillis-Steele inclusive scan of the partial sums
-    const int64_t v = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+  for (int64_t base = 0; base < len; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const int32_t v = i < len ? hist[i] : 0;
+    int32_t x = v;  // inclusive warp scan
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) warp_sum[warp] = x;
     __syncthreads();
-    part[threadIdx.x] += v;
+    if (warp == 0) {  // scan of the 32 warp totals
+      int32_t w = warp_sum[lane];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += y;
+      }
+      warp_sum[lane] = w;
+    }
     __syncthreads();
-  }
-  int64_t run = part[threadIdx.x] - sum;
-  for (int64_t i = lo; i < hi; ++i) {
-    const int32_t c = hist[i];
-    hist[i] = (int32_t)run;
-    run += c;
+    const int32_t before = carry + (warp ? warp_sum[warp - 1] : 0);
+    if (i < len) hist[i] = before + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_sum[31];
+    __syncthreads();
   }
 }
 
