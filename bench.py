@@ -351,10 +351,10 @@ def run_ours(args, cfg):
     gidx = torch.from_numpy(idx).to(dev)
 
     # ray schedule: one ray per lane for primaries; incoherent secondaries
-    # (config 4) are binned by direction octant first and walked in binned
-    # order (r01: 2.61 vs 2.38 Grays/s one ray per lane, 2.30 block
-    # compaction; profiles/r01_experiments.md) -- what a renderer's bounce
-    # pass selects with trace(schedule="binned").  --schedule or
+    # (config 4) are binned by direction cell first (96 cube-map cells) and
+    # walked in binned order (r01: 3.09 vs 2.37 Grays/s one ray per lane,
+    # 2.30 block compaction; profiles/r01_experiments.md) -- what a
+    # renderer's bounce pass selects with trace(schedule="binned").  --schedule or
     # TETB200_SCHED (sweeps, via the process-wide "auto" setting) override.
     schedule = args.schedule or ("auto" if os.environ.get("TETB200_SCHED") else
                                  ("binned" if cfg.get("secondaries") else "lane"))
@@ -598,7 +598,8 @@ def run_ours(args, cfg):
                         "bit_exact": mism2 == 0}
             secondary = {"value": ns / sec["binned"] / 1e3, "unit": "Mrays/s", "rays": ns,
                          "kernel_ms": sec["binned"], "schedule": "binned",
-                         "note": "direction-octant counting sort + the walk in binned order, both inside the events",
+                         "note": "direction-cell counting sort (96 cube-map cells) + the walk in binned order, "
+                                 "both inside the events",
                          "one_ray_per_lane": {"value": ns / sec["lane"] / 1e3, "kernel_ms": sec["lane"]},
                          "block_compaction": {"value": ns / sec["compact"] / 1e3, "kernel_ms": sec["compact"]},
                          "tets_visited_per_ray": {"mean": float(v2.mean()), "max": int(v2.max())},

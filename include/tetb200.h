@@ -231,9 +231,10 @@ int tb_sctp_cast_rays_host(tb_mesh* mesh, int64_t n, const float* o, const float
  *   persistent refill,
  *   3 / 4 = block compaction (256 / 512 threads per block) for incoherent
  *   batches; steps_per_round = walk steps between compactions (>= 1),
- *   6 = direction binning: a stable counting sort of the rays by direction
- *   octant into stream-ordered scratch (36 B / ray), then one ray per lane
- *   over the binned copies with results stored at the original indices --
+ *   6 = direction binning: a stable counting sort of the ray indices by
+ *   direction cell (cube-map face of the dominant axis x 4 x 4 cells, 96
+ *   bins; stream-ordered scratch, 9 B / ray), then one ray per lane in
+ *   binned order, each ray read and its results stored by index --
  *   for incoherent device-resident batches (n < 2^31; host-ray zero-copy
  *   calls run one ray per lane).  5 is unused. 
  * Process-wide; overrides TETB200_SCHED / TETB200_ROUND.  A negative

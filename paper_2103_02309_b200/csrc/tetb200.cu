@@ -1121,58 +1121,76 @@ struct CastPersistL {
 
 // ----------------------------------------------------------------------------
 // Direction binning for incoherent batches (schedule 6).  A stable counting
-// sort of the rays by direction octant: rays of one octant cross the mesh in
-// roughly parallel directions, so after binning a warp's neighbouring rays
-// (still in the caller's order inside their octant -- image order for
+// sort of the ray indices by direction cell: the dominant axis and its sign
+// pick a cube-map face, a 4 x 4 grid over the face's other two coordinates
+// (divided by the dominant one) the cell -- 96 bins.  Rays of one cell cross
+// the mesh in nearly parallel directions, so after binning a warp's rays
+// (still in the caller's order inside their cell -- image order for
 // secondaries spawned from a frame) share tets and L1 lines.  The walk then
-// reads the binned copies and the epilogue stores each result at its
-// original index (cast_kernel's kScatter path), so outputs are unchanged.
-// r01 (config 4, 16.7 M diffuse secondaries): the walk 7.14 -> 6.47 ms.
-constexpr int kBinTile = 4096;    // rays per binning block
-constexpr int kBinThreads = 256;  // 8 warps; one ray per thread per round
+// reads each ray through the permutation and stores its results at the
+// original index (cast_kernel's kScatter + kGather path): outputs unchanged.
+// r01 (config 4, 16.7 M diffuse secondaries; tools/bin_probe.py): walk
+// 7.14 ms unbinned, 6.47 by octant (8 bins), 6.05 by face, 5.13 by 4 x 4
+// cells per face, 5.47 by 8 x 8.  Any deterministic cell function is exact:
+// only the order of the walks changes.
+constexpr int kBinFace = 4;                          // cells per cube-face edge
+constexpr int kBins = 6 * kBinFace * kBinFace;       // 96
+constexpr int kBinTile = 4096;                       // rays per binning block
+constexpr int kBinThreads = 256;                     // 8 warps; one ray per thread per round
 
-__device__ __forceinline__ int dir_octant(const float* __restrict__ d, int64_t r) {
-  return (__ldg(d + 3 * r) < 0.f) | ((__ldg(d + 3 * r + 1) < 0.f) << 1) | ((__ldg(d + 3 * r + 2) < 0.f) << 2);
+__device__ __forceinline__ int dir_bin(const float* __restrict__ d, int64_t r) {
+  const float x = __ldg(d + 3 * r), y = __ldg(d + 3 * r + 1), z = __ldg(d + 3 * r + 2);
+  const float ax = fabsf(x), ay = fabsf(y), az = fabsf(z);
+  int a;
+  float m, u, v;
+  if (ax >= ay && ax >= az) {
+    a = 0; m = x; u = y; v = z;
+  } else if (ay >= az) {
+    a = 1; m = y; u = x; v = z;
+  } else {
+    a = 2; m = z; u = x; v = y;
+  }
+  const float s = __fdividef(0.5f * kBinFace, fabsf(m));  // NaN / inf directions land in some cell: still exact
+  const int cu = min(max((int)((u + fabsf(m)) * s), 0), kBinFace - 1);
+  const int cv = min(max((int)((v + fabsf(m)) * s), 0), kBinFace - 1);
+  return ((2 * a + (m < 0.f)) * kBinFace + cu) * kBinFace + cv;
 }
 
-// hist[k * n_tiles + tile] = rays of octant k in the tile
+// hist[b * n_tiles + tile] = rays of bin b in the tile; bins[r] = ray r's bin
+// (so the scatter pass reads 1 byte per ray instead of the direction)
 __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(const float* __restrict__ d, int64_t n,
-                                                                int32_t* __restrict__ hist, int n_tiles) {
-  __shared__ int cnt[8];
-  if (threadIdx.x < 8) cnt[threadIdx.x] = 0;
+                                                                int32_t* __restrict__ hist, int n_tiles,
+                                                                uint8_t* __restrict__ bins) {
+  __shared__ int cnt[kBins];
+  for (int b = threadIdx.x; b < kBins; b += kBinThreads) cnt[b] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kBinTile;
-  int local[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int i = threadIdx.x; i < kBinTile; i += kBinThreads) {
+  for (int i = threadIdx.x; i < kBinTile; i += kBinThreads) {  // warp-uniform trip count
     const int64_t r = base + i;
-    if (r < n) {
-      const int k = dir_octant(d, r);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) local[q] += (k == q);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    int v = local[q];
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&cnt[q], v);
+    const int bin = r < n ? dir_bin(d, r) : kBins;
+    if (r < n) bins[r] = (uint8_t)bin;
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);  // one shared-memory atomic per bin per warp
+    if (bin < kBins && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&cnt[bin], __popc(peers));
   }
   __syncthreads();
-  if (threadIdx.x < 8) hist[(int64_t)threadIdx.x * n_tiles + blockIdx.x] = cnt[threadIdx.x];
+  for (int b = threadIdx.x; b < kBins; b += kBinThreads) hist[(int64_t)b * n_tiles + blockIdx.x] = cnt[b];
 }
 
-// In-place exclusive scan of hist[0..len) by one block (len = 8 * n_tiles):
-// coalesced 1024-entry chunks, warp-shuffle scans, a running carry.
-__global__ void __launch_bounds__(1024) bin_scan_kernel(int32_t* __restrict__ hist, int64_t len) {
+// One block per bin: exclusive scan of the bin's per-tile counts in place
+// (coalesced 1024-entry chunks, warp-shuffle scans, running carry); the
+// bin's total goes to totals[bin].
+__global__ void __launch_bounds__(1024) bin_scan_kernel(int32_t* __restrict__ hist, int n_tiles,
+                                                        int32_t* __restrict__ totals) {
   __shared__ int32_t warp_sum[32];
   __shared__ int32_t carry;
+  int32_t* row = hist + (int64_t)blockIdx.x * n_tiles;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int64_t base = 0; base < len; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const int32_t v = i < len ? hist[i] : 0;
-    int32_t x = v;  // inclusive warp scan
+  for (int base = 0; base < n_tiles; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int32_t v = i < n_tiles ? row[i] : 0;
+    int32_t x = v;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const int32_t y = __shfl_up_sync(0xffffffffu, x, off);
@@ -1180,7 +1198,7 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(int32_t* __restrict__ hi
     }
     if (lane == 31) warp_sum[warp] = x;
     __syncthreads();
-    if (warp == 0) {  // scan of the 32 warp totals
+    if (warp == 0) {
       int32_t w = warp_sum[lane];
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
@@ -1190,46 +1208,55 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(int32_t* __restrict__ hi
       warp_sum[lane] = w;
     }
     __syncthreads();
-    const int32_t before = carry + (warp ? warp_sum[warp - 1] : 0);
-    if (i < len) hist[i] = before + x - v;
+    if (i < n_tiles) row[i] = carry + (warp ? warp_sum[warp - 1] : 0) + x - v;
     __syncthreads();
     if (threadIdx.x == 0) carry += warp_sum[31];
     __syncthreads();
   }
+  if (threadIdx.x == 0) totals[blockIdx.x] = carry;
 }
 
-// Stable scatter of the permutation: perm[offs[k * n_tiles + tile] + rank of
-// ray r among the tile's octant-k rays, in caller order] = r.
-__global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const float* __restrict__ d, int64_t n,
-                                                                  const int32_t* __restrict__ offs, int n_tiles,
+// Stable scatter of the permutation: perm[start of bin b + offset of the
+// tile within bin b + rank of ray r among the tile's bin-b rays, in caller
+// order] = r.  Ranks within a warp come from __match_any_sync peers.
+__global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint8_t* __restrict__ bins, int64_t n,
+                                                                  const int32_t* __restrict__ offs,
+                                                                  const int32_t* __restrict__ totals, int n_tiles,
                                                                   int64_t* __restrict__ perm) {
-  __shared__ int warp_cnt[kBinThreads / 32][8];
-  __shared__ int running[8];
+  __shared__ int warp_cnt[kBinThreads / 32][kBins];
+  __shared__ int running[kBins];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x < 8) running[threadIdx.x] = offs[(int64_t)threadIdx.x * n_tiles + blockIdx.x];
+  if (threadIdx.x == 0) {  // bin starts: exclusive prefix of the 96 totals
+    int acc = 0;
+    for (int b = 0; b < kBins; ++b) {
+      running[b] = acc;
+      acc += totals[b];
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kBins; b += kBinThreads) running[b] += offs[(int64_t)b * n_tiles + blockIdx.x];
   const int64_t base = (int64_t)blockIdx.x * kBinTile;
   for (int round = 0; round < kBinTile / kBinThreads; ++round) {
+    if (base + round * kBinThreads >= n) break;  // block-uniform
+    for (int k = threadIdx.x; k < (kBinThreads / 32) * kBins; k += kBinThreads) (&warp_cnt[0][0])[k] = 0;
+    __syncthreads();
     const int64_t r = base + round * kBinThreads + threadIdx.x;
     const bool live = r < n;
-    const int k = live ? dir_octant(d, r) : 8;
-    int my_rank = 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const unsigned msk = __ballot_sync(0xffffffffu, k == q);
-      if (k == q) my_rank = __popc(msk & ((1u << lane) - 1u));
-      if (lane == 0) warp_cnt[warp][q] = __popc(msk);
-    }
+    const int bin = live ? (int)__ldg(bins + r) : kBins;
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (live && rank == 0) warp_cnt[warp][bin] = __popc(peers);
     __syncthreads();
     if (live) {
-      int pos = running[k] + my_rank;
-      for (int w = 0; w < warp; ++w) pos += warp_cnt[w][k];
+      int pos = running[bin] + rank;
+      for (int w = 0; w < warp; ++w) pos += warp_cnt[w][bin];
       perm[pos] = r;
     }
     __syncthreads();
-    if (threadIdx.x < 8) {
+    for (int b = threadIdx.x; b < kBins; b += kBinThreads) {
       int add = 0;
-      for (int w = 0; w < kBinThreads / 32; ++w) add += warp_cnt[w][threadIdx.x];
-      running[threadIdx.x] += add;
+      for (int w = 0; w < kBinThreads / 32; ++w) add += warp_cnt[w][b];
+      running[b] += add;
     }
     __syncthreads();
   }
@@ -1390,17 +1417,19 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
                   : launch_compact<512>(m->layout, m->safe, n, s, v, n, o, d, start, status, cf, tet, visited,
                                         triangle, t, tet_back);
   } else if (mode == 6 && !host_rays && n < ((int64_t)1 << 31)) {
-    // direction binning (stable counting sort of ray indices by octant), then
+    // direction binning (stable counting sort of ray indices by direction cell), then
     // the walk in binned order, reading rays and storing results by index
     const int n_tiles = (int)((n + kBinTile - 1) / kBinTile);
-    const size_t hist_b = ((size_t)n_tiles * 8 * 4 + 255) & ~(size_t)255;
+    const size_t hist_b = ((size_t)n_tiles * kBins * 4 + (size_t)kBins * 4 + 255) & ~(size_t)255;
     char* scratch = nullptr;
-    if (int e2 = scratch_alloc(m->device, hist_b + (size_t)n * 8, s, &scratch)) return e2;
+    if (int e2 = scratch_alloc(m->device, hist_b + (size_t)n * 8 + (size_t)n, s, &scratch)) return e2;
     int32_t* hist = reinterpret_cast<int32_t*>(scratch);
+    int32_t* totals = hist + (size_t)n_tiles * kBins;
     int64_t* perm = reinterpret_cast<int64_t*>(scratch + hist_b);
-    bin_count_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles);
-    bin_scan_kernel<<<1, 1024, 0, s>>>(hist, (int64_t)n_tiles * 8);
-    bin_scatter_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles, perm);
+    uint8_t* bins = reinterpret_cast<uint8_t*>(scratch + hist_b + (size_t)n * 8);
+    bin_count_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles, bins);
+    bin_scan_kernel<<<kBins, 1024, 0, s>>>(hist, n_tiles, totals);
+    bin_scatter_kernel<<<n_tiles, kBinThreads, 0, s>>>(bins, n, hist, totals, n_tiles, perm);
     e = launch_layout<CastBinnedL>(m->layout, grid_for(n, kCastBlock), s, m->safe, perm, v, n, o, d, start, status,
                                    cf, tet, visited, triangle, t, tet_back);
     cudaFreeAsync(scratch, s);

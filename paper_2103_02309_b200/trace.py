@@ -63,9 +63,9 @@ def trace(mesh, origins: torch.Tensor, dirs: torch.Tensor, start: torch.Tensor, 
     ``sctp=True`` runs the fp64 scalar-triple-product fallback walk instead
     of the 2-D modified-basis walk.  ``schedule`` maps rays to lanes (results
     are identical either way): "lane" suits coherent primaries, "binned"
-    (stable counting sort by direction octant, then the walk in binned
-    order) incoherent batches such as diffuse secondaries (r01: +10 % on
-    config 4), "compact" block compaction (kept for comparison); "auto" uses the process-wide setting (default: "lane" -- deciding from
+    (stable counting sort by direction cell -- 96 cube-map cells -- then
+    the walk in binned order) incoherent batches such as diffuse
+    secondaries (r01: +30 % on config 4), "compact" block compaction (kept for comparison); "auto" uses the process-wide setting (default: "lane" -- deciding from
     device-resident start tets would need a host round trip).  Start tets
     are not range-checked here (device inputs stay on the device);
     ``kernels.cast_rays`` checks them.

@@ -60,6 +60,17 @@ def main():
     for shift in (4, 8, 12):
         keys[f"start>>{shift}"] = start >> shift
         keys[f"octant,start>>{shift}"] = (octant << 40) | (start >> shift)
+    # cube-map direction bins: dominant axis and its sign (6 faces) x a k x k
+    # grid over the face's two other coordinates (divided by the dominant one)
+    dd = g[1].double()
+    ax = dd.abs().argmax(dim=1)
+    sgn = (dd.gather(1, ax[:, None])[:, 0] < 0).long()
+    face = ax * 2 + sgn
+    other = torch.tensor([[1, 2], [0, 2], [0, 1]], device=dev)[ax]
+    uv = dd.gather(1, other) / dd.gather(1, ax[:, None]).abs()
+    for k in (1, 2, 4, 8):
+        cell = ((uv + 1) * 0.5 * k).long().clamp(0, k - 1)
+        keys[f"cube{k}"] = (face * k + cell[:, 0]) * k + cell[:, 1]
     ref = None
     for name, key in keys.items():
         if key is None:
