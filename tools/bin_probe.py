@@ -71,8 +71,14 @@ def main():
     for k in (1, 2, 4, 8):
         cell = ((uv + 1) * 0.5 * k).long().clamp(0, k - 1)
         keys[f"cube{k}"] = (face * k + cell[:, 0]) * k + cell[:, 1]
+        if k in (2, 4):
+            for shift in (8, 12, 16):
+                keys[f"cube{k},start>>{shift}"] = (keys[f"cube{k}"] << 40) | (start >> shift)
     ref = None
+    only = os.environ.get("BIN_KEYS")
     for name, key in keys.items():
+        if only and name not in only.split(";") and name != "none":
+            continue
         if key is None:
             perm = torch.arange(n, device=dev)
         else:
