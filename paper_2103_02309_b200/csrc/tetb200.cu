@@ -1262,6 +1262,87 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint8_t*
   }
 }
 
+// Tile-local variant: each block sorts its own `tile` consecutive rays by
+// direction cell (count, 96-bin scan, stable scatter -- one kernel, no
+// global scan), so a ray's binned slot stays inside its tile and the walk's
+// gathered ray reads and scattered result stores touch one tile's span of
+// each array at a time (L2-resident) instead of the whole batch.
+__global__ void __launch_bounds__(1024) bin_local_kernel(const float* __restrict__ d, int64_t n, int tile,
+                                                         int64_t* __restrict__ perm) {
+  __shared__ int running[kBins];
+  __shared__ int warp_cnt[32][kBins];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b = threadIdx.x; b < kBins; b += 1024) running[b] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * tile;
+  for (int i = threadIdx.x; i < tile; i += 1024) {  // block-uniform trip count
+    const int64_t r = base + i;
+    const int bin = r < n ? dir_bin(d, r) : kBins;
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (bin < kBins && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&running[bin], __popc(peers));
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the 96 counts, 3 per lane, offset by the tile start
+    static_assert(kBins == 96, "3 bins per lane");
+    const int c0 = running[3 * lane], c1 = running[3 * lane + 1], c2 = running[3 * lane + 2];
+    int x = c0 + c1 + c2;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    const int ex = x - (c0 + c1 + c2);
+    running[3 * lane] = ex;
+    running[3 * lane + 1] = ex + c0;
+    running[3 * lane + 2] = ex + c0 + c1;
+  }
+  for (int round = 0; round < tile / 1024; ++round) {
+    if (base + (int64_t)round * 1024 >= n) break;  // block-uniform
+    for (int k = threadIdx.x; k < 32 * kBins; k += 1024) (&warp_cnt[0][0])[k] = 0;
+    __syncthreads();
+    const int64_t r = base + (int64_t)round * 1024 + threadIdx.x;
+    const bool live = r < n;
+    const int bin = live ? dir_bin(d, r) : kBins;
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (live && rank == 0) warp_cnt[warp][bin] = __popc(peers);
+    __syncthreads();
+    if (live) {
+      int pos = running[bin] + rank;
+      for (int w = 0; w < warp; ++w) pos += warp_cnt[w][bin];
+      perm[base + pos] = r;
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kBins; b += 1024) {
+      int add = 0;
+      for (int w = 0; w < 32; ++w) add += warp_cnt[w][b];
+      running[b] += add;
+    }
+    __syncthreads();
+  }
+}
+
+// Global vs tile-local binning (r01, bench.py device values): a batch whose
+// rays and results fit in L2 keeps the global sort (config-2 secondaries,
+// 2.07 M rays: global 2269 Mrays/s, local 65536-ray tiles 2007); a larger
+// one sorts within 65536-ray tiles, because a global permutation scatters
+// every ray's reads and result stores over the whole batch and the partial
+// sectors thrash L2 (ncu, config 4 global: 9.4 GB DRAM read + 3.6 GB write
+// per walk) -- config 4: global 3094, local 16 K / 64 K / 256 K / 1 M-ray
+// tiles 3258 / 3277 / 2975 / 2015 (the last two starve the binning kernel of
+// blocks).  TETB200_BIN_TILE overrides (0 = global).
+int bin_tile(int device, int64_t n) {
+  static int env = -2;
+  if (env == -2) {
+    const char* v = getenv("TETB200_BIN_TILE");
+    env = v ? (atoi(v) <= 0 ? 0 : ((atoi(v) + 1023) / 1024) * 1024) : -1;
+  }
+  if (env >= 0) return env;
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+  return n * 57 > (int64_t)l2 ? 65536 : 0;  // 57 B: a ray's inputs (28) and results (29)
+}
+
 // TETB200_SCHED: 0 = auto, 1 = one ray per lane (cast_kernel), 2 = persistent
 // refill (cast_persist_kernel), 3 / 4 = block compaction with 256 / 512
 // threads (cast_compact_kernel).  TETB200_ROUND: steps per compaction round.
@@ -1427,9 +1508,13 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
     int32_t* totals = hist + (size_t)n_tiles * kBins;
     int64_t* perm = reinterpret_cast<int64_t*>(scratch + hist_b);
     uint8_t* bins = reinterpret_cast<uint8_t*>(scratch + hist_b + (size_t)n * 8);
-    bin_count_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles, bins);
-    bin_scan_kernel<<<kBins, 1024, 0, s>>>(hist, n_tiles, totals);
-    bin_scatter_kernel<<<n_tiles, kBinThreads, 0, s>>>(bins, n, hist, totals, n_tiles, perm);
+    if (const int lt = bin_tile(m->device, n)) {
+      bin_local_kernel<<<grid_for(n, lt), 1024, 0, s>>>(d, n, lt, perm);
+    } else {
+      bin_count_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles, bins);
+      bin_scan_kernel<<<kBins, 1024, 0, s>>>(hist, n_tiles, totals);
+      bin_scatter_kernel<<<n_tiles, kBinThreads, 0, s>>>(bins, n, hist, totals, n_tiles, perm);
+    }
     e = launch_layout<CastBinnedL>(m->layout, grid_for(n, kCastBlock), s, m->safe, perm, v, n, o, d, start, status,
                                    cf, tet, visited, triangle, t, tet_back);
     cudaFreeAsync(scratch, s);

@@ -104,6 +104,35 @@ def test_degenerate_directions_vs_c_oracle():
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("schedule", ("lane", "binned"))
+def test_degenerate_directions_device_schedules(schedule):
+    """The same degenerate rays, mixed into a batch spanning several binning
+    tiles, through trace(schedule=...): the binned schedule's direction cell
+    of a zero / NaN / inf direction is arbitrary but its results must still
+    equal the C restatement ray for ray."""
+    import torch
+
+    from oracle import pyoracle
+    from paper_2103_02309_b200 import kernels as K
+    from paper_2103_02309_b200.ingestion import build_box_fixture
+    from paper_2103_02309_b200.scenes import interior_rays
+    from paper_2103_02309_b200.tetmesh import encode
+    from paper_2103_02309_b200.trace import trace
+
+    raw, soup = build_box_fixture(4, occluders=[(0, 2, (1, 1), (3, 3))])
+    m = encode(raw, "tet16", soup)
+    o, d, st = interior_rays(m, 9000, 5)
+    bad = np.array([[0, 0, 0], [np.nan, 1, 0], [np.inf, 0, 0], [0, 0, 1e-30], [1e30, 1, 1], [0, -0.0, 1],
+                    [-np.inf, np.nan, 2]], np.float32)
+    d[::1301][: len(bad)] = bad[: len(d[::1301])]
+    dev = torch.device("cuda", 0)
+    res = trace(m, *(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (o, d, st)), schedule=schedule)
+    exp = pyoracle.cast_rays_full(m, o, d, st)
+    got = (res.status, res.cf, res.tet, res.visited, res.triangle, res.t, res.tet_back)
+    for a, b in zip(got, exp):
+        assert np.array_equal(a.cpu().numpy(), b, equal_nan=True)
+
+
 def test_large_batch_ragged_sizes(REF):
     """Sizes that are not multiples of the block / warp / chunk sizes."""
     from paper_2103_02309_b200 import kernels as K

@@ -593,3 +593,26 @@ def test_config2_full_frame_vs_reference(digests, K, scheme):
     res = trace(sc.mesh, *(torch.from_numpy(a).to(dev) for a in (o, d, st)))
     got = [x.cpu().numpy() for x in (res.status, res.cf, res.tet, res.visited)]
     assert digest(*got) == digests[f"blob55/{scheme}/cast"]
+
+
+def test_binned_large_batch_uses_tiles_and_matches_lane(golden):
+    """A batch whose rays and results exceed L2 takes the tile-local binning
+    path (bin_tile: n * 57 B > L2); its results must equal one ray per lane
+    (itself pinned to the oracle above) for every ray, including a ragged
+    last tile."""
+    import torch
+
+    from paper_2103_02309_b200.scenes import interior_rays
+    from paper_2103_02309_b200.trace import trace
+
+    m = golden_mesh(golden, "model", "tet16")
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    n = l2 // 57 + 70_001
+    o, d, st = interior_rays(m, n, 23)
+    dev = torch.device("cuda", 0)
+    g = [torch.from_numpy(a).to(dev) for a in (o, d, st)]
+    a = trace(m, *g, schedule="lane")
+    b = trace(m, *g, schedule="binned")
+    torch.cuda.synchronize()
+    for k in NAMES7:
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
