@@ -352,7 +352,7 @@ def run_ours(args, cfg):
 
     # ray schedule: one ray per lane for primaries; incoherent secondaries
     # (config 4) are binned by direction cell first (96 cube-map cells) and
-    # walked in binned order (r01: 3.27 vs 2.37 Grays/s one ray per lane,
+    # walked in binned order (r01: 3.36 vs 2.37 Grays/s one ray per lane,
     # 2.30 block compaction; profiles/r01_experiments.md) -- what a
     # renderer's bounce pass selects with trace(schedule="binned").  --schedule or
     # TETB200_SCHED (sweeps, via the process-wide "auto" setting) override.

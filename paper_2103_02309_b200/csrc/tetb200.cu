@@ -1158,8 +1158,16 @@ __device__ __forceinline__ int dir_bin(const float* __restrict__ d, int64_t r) {
 
 // hist[b * n_tiles + tile] = rays of bin b in the tile; bins[r] = ray r's bin
 // (so the scatter pass reads 1 byte per ray instead of the direction)
+// Histogram index of (bin b, tile t): global sort (S == 0) bin-major over
+// all tiles; tile-local sort (S = tiles per segment) segment-major, then
+// bin, then the tile within the segment -- so one exclusive scan per segment
+// yields absolute positions inside the segment's own range of rays.
+__device__ __forceinline__ int64_t hist_at(int b, int t, int n_tiles, int S) {
+  return S ? ((int64_t)(t / S) * kBins + b) * S + (t % S) : (int64_t)b * n_tiles + t;
+}
+
 __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(const float* __restrict__ d, int64_t n,
-                                                                int32_t* __restrict__ hist, int n_tiles,
+                                                                int32_t* __restrict__ hist, int n_tiles, int S,
                                                                 uint8_t* __restrict__ bins) {
   __shared__ int cnt[kBins];
   for (int b = threadIdx.x; b < kBins; b += kBinThreads) cnt[b] = 0;
@@ -1173,7 +1181,46 @@ __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(const float* __r
     if (bin < kBins && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&cnt[bin], __popc(peers));
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < kBins; b += kBinThreads) hist[(int64_t)b * n_tiles + blockIdx.x] = cnt[b];
+  for (int b = threadIdx.x; b < kBins; b += kBinThreads) hist[hist_at(b, blockIdx.x, n_tiles, S)] = cnt[b];
+}
+
+// Tile-local mode: one block per segment, exclusive scan of its kBins * S
+// counts in place, offset by the segment's first ray.
+__global__ void __launch_bounds__(1024) bin_seg_scan_kernel(int32_t* __restrict__ hist, int S) {
+  __shared__ int32_t warp_sum[32];
+  __shared__ int32_t carry;
+  const int len = kBins * S;
+  int32_t* row = hist + (int64_t)blockIdx.x * len;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int32_t seg_base = blockIdx.x * S * kBinTile;
+  for (int base = 0; base < len; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int32_t v = i < len ? row[i] : 0;
+    int32_t x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) warp_sum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t w = warp_sum[lane];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, w, off);
+        if (lane >= off) w += y;
+      }
+      warp_sum[lane] = w;
+    }
+    __syncthreads();
+    if (i < len) row[i] = seg_base + carry + (warp ? warp_sum[warp - 1] : 0) + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_sum[31];
+    __syncthreads();
+  }
 }
 
 // One block per bin: exclusive scan of the bin's per-tile counts in place
@@ -1222,19 +1269,19 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(int32_t* __restrict__ hi
 __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint8_t* __restrict__ bins, int64_t n,
                                                                   const int32_t* __restrict__ offs,
                                                                   const int32_t* __restrict__ totals, int n_tiles,
-                                                                  int64_t* __restrict__ perm) {
+                                                                  int S, int64_t* __restrict__ perm) {
   __shared__ int warp_cnt[kBinThreads / 32][kBins];
   __shared__ int running[kBins];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {  // bin starts: exclusive prefix of the 96 totals
+  if (threadIdx.x == 0) {  // global sort: bin starts = exclusive prefix of the 96 totals
     int acc = 0;
     for (int b = 0; b < kBins; ++b) {
       running[b] = acc;
-      acc += totals[b];
+      acc += S ? 0 : totals[b];
     }
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < kBins; b += kBinThreads) running[b] += offs[(int64_t)b * n_tiles + blockIdx.x];
+  for (int b = threadIdx.x; b < kBins; b += kBinThreads) running[b] += offs[hist_at(b, blockIdx.x, n_tiles, S)];
   const int64_t base = (int64_t)blockIdx.x * kBinTile;
   for (int round = 0; round < kBinTile / kBinThreads; ++round) {
     if (base + round * kBinThreads >= n) break;  // block-uniform
@@ -1262,85 +1309,23 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint8_t*
   }
 }
 
-// Tile-local variant: each block sorts its own `tile` consecutive rays by
-// direction cell (count, 96-bin scan, stable scatter -- one kernel, no
-// global scan), so a ray's binned slot stays inside its tile and the walk's
-// gathered ray reads and scattered result stores touch one tile's span of
-// each array at a time (L2-resident) instead of the whole batch.
-__global__ void __launch_bounds__(1024) bin_local_kernel(const float* __restrict__ d, int64_t n, int tile,
-                                                         int64_t* __restrict__ perm) {
-  __shared__ int running[kBins];
-  __shared__ int warp_cnt[32][kBins];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int b = threadIdx.x; b < kBins; b += 1024) running[b] = 0;
-  __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * tile;
-  for (int i = threadIdx.x; i < tile; i += 1024) {  // block-uniform trip count
-    const int64_t r = base + i;
-    const int bin = r < n ? dir_bin(d, r) : kBins;
-    const unsigned peers = __match_any_sync(0xffffffffu, bin);
-    if (bin < kBins && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&running[bin], __popc(peers));
-  }
-  __syncthreads();
-  if (warp == 0) {  // exclusive scan of the 96 counts, 3 per lane, offset by the tile start
-    static_assert(kBins == 96, "3 bins per lane");
-    const int c0 = running[3 * lane], c1 = running[3 * lane + 1], c2 = running[3 * lane + 2];
-    int x = c0 + c1 + c2;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, off);
-      if (lane >= off) x += y;
-    }
-    const int ex = x - (c0 + c1 + c2);
-    running[3 * lane] = ex;
-    running[3 * lane + 1] = ex + c0;
-    running[3 * lane + 2] = ex + c0 + c1;
-  }
-  for (int round = 0; round < tile / 1024; ++round) {
-    if (base + (int64_t)round * 1024 >= n) break;  // block-uniform
-    for (int k = threadIdx.x; k < 32 * kBins; k += 1024) (&warp_cnt[0][0])[k] = 0;
-    __syncthreads();
-    const int64_t r = base + (int64_t)round * 1024 + threadIdx.x;
-    const bool live = r < n;
-    const int bin = live ? dir_bin(d, r) : kBins;
-    const unsigned peers = __match_any_sync(0xffffffffu, bin);
-    const int rank = __popc(peers & ((1u << lane) - 1u));
-    if (live && rank == 0) warp_cnt[warp][bin] = __popc(peers);
-    __syncthreads();
-    if (live) {
-      int pos = running[bin] + rank;
-      for (int w = 0; w < warp; ++w) pos += warp_cnt[w][bin];
-      perm[base + pos] = r;
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < kBins; b += 1024) {
-      int add = 0;
-      for (int w = 0; w < 32; ++w) add += warp_cnt[w][b];
-      running[b] += add;
-    }
-    __syncthreads();
-  }
-}
-
-// Global vs tile-local binning (r01, bench.py device values): a batch whose
-// rays and results fit in L2 keeps the global sort (config-2 secondaries,
-// 2.07 M rays: global 2269 Mrays/s, local 65536-ray tiles 2007); a larger
-// one sorts within 65536-ray tiles, because a global permutation scatters
-// every ray's reads and result stores over the whole batch and the partial
-// sectors thrash L2 (ncu, config 4 global: 9.4 GB DRAM read + 3.6 GB write
-// per walk) -- config 4: global 3094, local 16 K / 64 K / 256 K / 1 M-ray
-// tiles 3258 / 3277 / 2975 / 2015 (the last two starve the binning kernel of
-// blocks).  TETB200_BIN_TILE overrides (0 = global).
-int bin_tile(int device, int64_t n) {
+// Sorting segments (r01, bench.py device values): binning sorts within
+// segments of 262144 consecutive rays rather than over the whole batch.  A
+// global permutation scatters every ray's gathered reads and result stores
+// over the whole batch, and the partial sectors thrash L2 (ncu, config 4
+// global: 9.4 GB DRAM read + 3.6 GB write per walk, L2 hit 25 %); within a
+// segment those spans stay L2-resident while coherence is kept.  Config 4
+// (16.7 M rays): global 3097 Mrays/s; segments of 64 K / 128 K / 256 K /
+// 512 K / 1 M / 2 M rays 3335 / 3347 / 3359 / 3373 / 3367 / 3330.  Config-2
+// secondaries (2.07 M): global 2265, 256 K segments 2398.  TETB200_BIN_TILE
+// overrides (0 = one global sort).
+int bin_tile() {
   static int env = -2;
   if (env == -2) {
     const char* v = getenv("TETB200_BIN_TILE");
-    env = v ? (atoi(v) <= 0 ? 0 : ((atoi(v) + 1023) / 1024) * 1024) : -1;
+    env = v ? (atoi(v) <= 0 ? 0 : ((atoi(v) + kBinTile - 1) / kBinTile) * kBinTile) : -1;  // whole tiles
   }
-  if (env >= 0) return env;
-  int l2 = 0;
-  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
-  return n * 57 > (int64_t)l2 ? 65536 : 0;  // 57 B: a ray's inputs (28) and results (29)
+  return env >= 0 ? env : 262144;
 }
 
 // TETB200_SCHED: 0 = auto, 1 = one ray per lane (cast_kernel), 2 = persistent
@@ -1501,20 +1486,26 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
     // direction binning (stable counting sort of ray indices by direction cell), then
     // the walk in binned order, reading rays and storing results by index
     const int n_tiles = (int)((n + kBinTile - 1) / kBinTile);
-    const size_t hist_b = ((size_t)n_tiles * kBins * 4 + (size_t)kBins * 4 + 255) & ~(size_t)255;
+    const int S = bin_tile() / kBinTile;  // tiles per sorting segment, 0 = one global sort
+    const int n_segs = S ? (n_tiles + S - 1) / S : 1;
+    // hist: kBins counts per tile (padded to whole segments in tile-local mode), then the 96 totals
+    const size_t hist_n = (size_t)(S ? n_segs * S : n_tiles) * kBins;
+    const size_t hist_b = ((hist_n + kBins) * 4 + 255) & ~(size_t)255;
     char* scratch = nullptr;
     if (int e2 = scratch_alloc(m->device, hist_b + (size_t)n * 8 + (size_t)n, s, &scratch)) return e2;
     int32_t* hist = reinterpret_cast<int32_t*>(scratch);
-    int32_t* totals = hist + (size_t)n_tiles * kBins;
+    int32_t* totals = hist + hist_n;
     int64_t* perm = reinterpret_cast<int64_t*>(scratch + hist_b);
     uint8_t* bins = reinterpret_cast<uint8_t*>(scratch + hist_b + (size_t)n * 8);
-    if (const int lt = bin_tile(m->device, n)) {
-      bin_local_kernel<<<grid_for(n, lt), 1024, 0, s>>>(d, n, lt, perm);
+    if (S) {
+      TB_CUDA(cudaMemsetAsync(hist, 0, hist_n * 4, s));  // the ragged segment's missing tiles count 0
+      bin_count_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles, S, bins);
+      bin_seg_scan_kernel<<<n_segs, 1024, 0, s>>>(hist, S);
     } else {
-      bin_count_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles, bins);
+      bin_count_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles, 0, bins);
       bin_scan_kernel<<<kBins, 1024, 0, s>>>(hist, n_tiles, totals);
-      bin_scatter_kernel<<<n_tiles, kBinThreads, 0, s>>>(bins, n, hist, totals, n_tiles, perm);
     }
+    bin_scatter_kernel<<<n_tiles, kBinThreads, 0, s>>>(bins, n, hist, totals, n_tiles, S, perm);
     e = launch_layout<CastBinnedL>(m->layout, grid_for(n, kCastBlock), s, m->safe, perm, v, n, o, d, start, status,
                                    cf, tet, visited, triangle, t, tet_back);
     cudaFreeAsync(scratch, s);

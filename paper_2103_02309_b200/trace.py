@@ -65,7 +65,7 @@ def trace(mesh, origins: torch.Tensor, dirs: torch.Tensor, start: torch.Tensor, 
     are identical either way): "lane" suits coherent primaries, "binned"
     (stable counting sort by direction cell -- 96 cube-map cells -- then
     the walk in binned order) incoherent batches such as diffuse
-    secondaries (r01: +38 % on config 4), "compact" block compaction
+    secondaries (r01: +41 % on config 4), "compact" block compaction
     (kept for comparison); "auto" uses the process-wide setting (default:
     "lane" -- deciding from device-resident start tets would need a host
     round trip).  Start tets

@@ -595,11 +595,10 @@ def test_config2_full_frame_vs_reference(digests, K, scheme):
     assert digest(*got) == digests[f"blob55/{scheme}/cast"]
 
 
-def test_binned_large_batch_uses_tiles_and_matches_lane(golden):
-    """A batch whose rays and results exceed L2 takes the tile-local binning
-    path (bin_tile: n * 57 B > L2); its results must equal one ray per lane
-    (itself pinned to the oracle above) for every ray, including a ragged
-    last tile."""
+def test_binned_many_segments_matches_lane(golden):
+    """A batch of ~9 binning segments (262144 rays each) with a ragged last
+    segment and tile: the binned results must equal one ray per lane
+    (itself pinned to the oracle above) for every ray."""
     import torch
 
     from paper_2103_02309_b200.scenes import interior_rays
