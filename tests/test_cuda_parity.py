@@ -413,11 +413,12 @@ def test_trace_schedule_argument(golden, K, O, schedule):
         assert np.array_equal(a.cpu().numpy(), b), k
 
 
-@pytest.mark.parametrize("mode", ("auto", "compact"))
+@pytest.mark.parametrize("mode", ("auto", "compact", "binned"))
 def test_host_path_coherent_and_incoherent(golden, K, O, schedule, mode):
     """tb_cast_rays_host on a camera batch (one start tet) and an incoherent
     batch: both equal the oracle, with pinned (zero-copy) and pageable
-    buffers, under the default and the compacting schedule."""
+    buffers, under the default, the compacting and the binned schedule
+    (the staged path bins each chunk)."""
     from paper_2103_02309_b200.scenes import camera_rays, interior_rays
 
     schedule(mode, 32)
