@@ -78,6 +78,9 @@ namespace {
 constexpr int kBlock = 128;
 // cast_kernel block size (r01 A/B: 32 / 64 / 256 threads were 1-7 % slower)
 constexpr int kCastBlock = 128;
+#ifndef TB_CAST_MIN_BLOCKS
+#define TB_CAST_MIN_BLOCKS 10  // cast_kernel residency target: 48 registers (r01 A/B)
+#endif
 
 struct DeviceGuard {
   int prev = -1;
@@ -336,7 +339,7 @@ constexpr int kUnroll = 4;
 // direction-binned schedule walks the rays in binned order straight from the
 // caller's arrays, so the binning pass writes only the 8-byte permutation.
 template <int L, bool kClamp, bool kHostRays, bool kScatter, bool kGather = false>
-__global__ void __launch_bounds__(kCastBlock, 10) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
+__global__ void __launch_bounds__(kCastBlock, TB_CAST_MIN_BLOCKS) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
                                                       const float* __restrict__ d,
                                                       const int32_t* __restrict__ start,
                                                       uint8_t* __restrict__ status, int32_t* __restrict__ cf,
