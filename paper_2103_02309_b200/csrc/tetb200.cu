@@ -1136,8 +1136,12 @@ struct CastPersistL {
 // 7.14 ms unbinned, 6.47 by octant (8 bins), 6.05 by face, 5.13 by 4 x 4
 // cells per face, 5.47 by 8 x 8.  Any deterministic cell function is exact:
 // only the order of the walks changes.
-constexpr int kBinFace = 4;                          // cells per cube-face edge
+#ifndef TB_BIN_FACE
+#define TB_BIN_FACE 4
+#endif
+constexpr int kBinFace = TB_BIN_FACE;                // cells per cube-face edge
 constexpr int kBins = 6 * kBinFace * kBinFace;       // 96
+static_assert(kBins <= 255, "bin ids are stored as bytes (kBins itself marks a dead lane)");
 constexpr int kBinTile = 4096;                       // rays per binning block
 constexpr int kBinThreads = 256;                     // 8 warps; one ray per thread per round
 
