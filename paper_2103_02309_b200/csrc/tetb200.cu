@@ -1505,7 +1505,10 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
     int64_t* perm = reinterpret_cast<int64_t*>(scratch + hist_b);
     uint8_t* bins = reinterpret_cast<uint8_t*>(scratch + hist_b + (size_t)n * 8);
     if (S) {
-      TB_CUDA(cudaMemsetAsync(hist, 0, hist_n * 4, s));  // the ragged segment's missing tiles count 0
+      if (cudaError_t me = cudaMemsetAsync(hist, 0, hist_n * 4, s)) {  // the ragged segment's missing tiles count 0
+        cudaFreeAsync(scratch, s);
+        return set_error(TB_E_CUDA, "binning scratch memset: %s", cudaGetErrorString(me));
+      }
       bin_count_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles, S, bins);
       bin_seg_scan_kernel<<<n_segs, 1024, 0, s>>>(hist, S);
     } else {
