@@ -709,7 +709,7 @@ def run_ours(args, cfg):
                      "kernel": (f"sctp_kernel<{cfg['layout'][3:]}>" if sctp else
                                 f"{'cast_compact_kernel' if schedule in ('compact', 'compact512') else 'cast_kernel'}"
                                 f"<{cfg['layout'][3:]}>"
-                                + (" after bin_count/bin_scan/bin_scatter (direction binning, inside the events)"
+                                + (" after bin_count/bin_seg_scan/bin_scatter (direction binning, inside the events)"
                                    if schedule == "binned" else "")),
                      "note": "algorithmic gather bytes (SURVEY s8d) over the HBM copy peak; the walk's "
                              "gathers are served by L1/L2 (ncu: DRAM traffic is a few % of them), so frac "
