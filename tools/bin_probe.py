@@ -10,6 +10,10 @@ Outputs are scattered back (tb_cast_rays_scatter) and must equal the
 unsorted run bit for bit.
 
     python tools/bin_probe.py [--size 4096] [--layout tet16]
+    BIN_KEYS="cube4;cube4,start>>8" python tools/bin_probe.py   # only these keys (+ the unsorted run)
+
+Keys also include cube-map direction cells (dominant axis and sign x a k x k grid, k = 1, 2,
+4, 8) alone and combined with start-tet buckets.
 """
 
 from __future__ import annotations
