@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""Schedules for incoherent secondaries: one ray per lane vs block
-compaction (256 / 512 threads, several round lengths), per layout and
+"""Schedules for incoherent secondaries: one ray per lane vs direction
+binning vs block compaction (256 / 512 threads, several round lengths), per layout and
 primary-frame size, on the blob GRID=55 scene.  Device time per launch
 (CUDA events, L2 flushed), median of --reps; outputs compared across
 schedules bit for bit.
@@ -54,7 +54,7 @@ def main():
             g = [torch.from_numpy(a).to(dev) for a in (so, sd, sst)]
             n = len(sst)
             ref = None
-            for sched, rounds in (("lane", 32), ("compact", 16), ("compact", 32), ("compact", 64),
+            for sched, rounds in (("lane", 32), ("binned", 32), ("compact", 16), ("compact", 32), ("compact", 64),
                                   ("compact512", 32)):
                 _lib.set_schedule(None, rounds)
                 out = empty_result(n, dev)
