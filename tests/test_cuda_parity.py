@@ -616,3 +616,22 @@ def test_binned_many_segments_matches_lane(golden):
     torch.cuda.synchronize()
     for k in NAMES7:
         assert torch.equal(getattr(a, k), getattr(b, k)), k
+
+
+@pytest.mark.parametrize("schedule", ("lane", "binned", "compact"))
+def test_schedules_without_epilogue(golden, O, schedule):
+    """trace(epilogue=False): triangle / t / tet_back are not computed (NULL in
+    the C call) under every schedule; status / cf / tet / visited still equal
+    the oracle."""
+    import torch
+
+    from paper_2103_02309_b200.scenes import interior_rays
+    from paper_2103_02309_b200.trace import trace
+
+    m = golden_mesh(golden, "model", "tet20")
+    o, d, st = interior_rays(m, 50_000, 31)
+    dev = torch.device("cuda", 0)
+    res = trace(m, *(torch.from_numpy(a).to(dev) for a in (o, d, st)), epilogue=False, schedule=schedule)
+    exp = O.cast_rays_full(m, o, d, st)
+    for k, a, b in zip(NAMES7[:4], (res.status, res.cf, res.tet, res.visited), exp[:4]):
+        assert np.array_equal(a.cpu().numpy(), b), k
