@@ -114,6 +114,28 @@ def main():
     out("shadow_kernel<20> (hit point -> point light)", ms, m, "Mrays_s",
         {"visited_mean": float(sv.double().mean()), "occluded_frac": float(occ.double().mean())})
 
+    # f2 probe: the same shadow rays sorted by direction cell of (light - p)
+    # (torch sort outside the timed region) -- what binning could buy here
+    dd = light - p
+    ax = dd.abs().argmax(dim=1)
+    face = ax * 2 + (dd.gather(1, ax[:, None])[:, 0] < 0).long()
+    other = torch.tensor([[1, 2], [0, 2], [0, 1]], device=dev)[ax]
+    uv = dd.gather(1, other) / dd.gather(1, ax[:, None]).abs()
+    cell = ((uv + 1) * 2).long().clamp(0, 3)
+    perm = torch.sort((face * 4 + cell[:, 0]) * 4 + cell[:, 1], stable=True).indices
+    ps, pts_ = p[perm].contiguous(), ptet[perm].contiguous()
+    occ2 = torch.empty(m, dtype=torch.uint8, device=dev)
+    sv2 = torch.empty(m, dtype=torch.int32, device=dev)
+
+    def shadow_sorted():
+        check(lib.tb_shadow_rays(dm.handle, m, addr(ps), addr(light), 0, addr(pts_), addr(lt), 0, 1e-4, addr(occ2),
+                                 addr(sv2), s), "tb_shadow_rays")
+
+    ms = timed(shadow_sorted, args.reps, flush)
+    same = bool(torch.equal(occ2, occ[perm]) and torch.equal(sv2, sv[perm]))
+    out("shadow_kernel<20> (same rays sorted by direction cell, sort untimed)", ms, m, "Mrays_s",
+        {"equal_after_unpermute": same})
+
     # f4: visit recording (CSR second pass over the frame)
     offs = torch.zeros(n + 1, dtype=torch.int64, device=dev)
     offs[1:] = torch.cumsum(res.visited.long(), 0)
