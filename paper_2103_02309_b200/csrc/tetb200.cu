@@ -1163,8 +1163,6 @@ __device__ __forceinline__ int dir_bin(const float* __restrict__ d, int64_t r) {
   return ((2 * a + (m < 0.f)) * kBinFace + cu) * kBinFace + cv;
 }
 
-// hist[b * n_tiles + tile] = rays of bin b in the tile; bins[r] = ray r's bin
-// (so the scatter pass reads 1 byte per ray instead of the direction)
 // Histogram index of (bin b, tile t): global sort (S == 0) bin-major over
 // all tiles; tile-local sort (S = tiles per segment) segment-major, then
 // bin, then the tile within the segment -- so one exclusive scan per segment
@@ -1173,6 +1171,8 @@ __device__ __forceinline__ int64_t hist_at(int b, int t, int n_tiles, int S) {
   return S ? ((int64_t)(t / S) * kBins + b) * S + (t % S) : (int64_t)b * n_tiles + t;
 }
 
+// hist[hist_at(b, tile)] = rays of bin b in the tile; bins[r] = ray r's bin
+// (so the scatter pass reads 1 byte per ray instead of the direction).
 __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(const float* __restrict__ d, int64_t n,
                                                                 int32_t* __restrict__ hist, int n_tiles, int S,
                                                                 uint8_t* __restrict__ bins) {
@@ -1191,7 +1191,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(const float* __r
   for (int b = threadIdx.x; b < kBins; b += kBinThreads) hist[hist_at(b, blockIdx.x, n_tiles, S)] = cnt[b];
 }
 
-// Tile-local mode: one block per segment, exclusive scan of its kBins * S
+// Segmented mode: one block per segment, exclusive scan of its kBins * S
 // counts in place, offset by the segment's first ray.
 __global__ void __launch_bounds__(1024) bin_seg_scan_kernel(int32_t* __restrict__ hist, int S) {
   __shared__ int32_t warp_sum[32];
@@ -1230,7 +1230,7 @@ __global__ void __launch_bounds__(1024) bin_seg_scan_kernel(int32_t* __restrict_
   }
 }
 
-// One block per bin: exclusive scan of the bin's per-tile counts in place
+// Global mode (TETB200_BIN_TILE=0): one block per bin, exclusive scan of the bin's per-tile counts in place
 // (coalesced 1024-entry chunks, warp-shuffle scans, running carry); the
 // bin's total goes to totals[bin].
 __global__ void __launch_bounds__(1024) bin_scan_kernel(int32_t* __restrict__ hist, int n_tiles,
