@@ -173,7 +173,7 @@ def cpu_reference_trace(mesh, o, d, st, threads: int):
     if K is None:
         K, kind = pyoracle, "port"
     n = len(st)
-    chunks = max(threads * 16, 1)
+    chunks = max(1, min(threads * 16, n // 4096))  # >= 4096 rays per chunk: pool overhead stays small
     bounds = np.linspace(0, n, chunks + 1).astype(np.int64)
 
     def work(i):
