@@ -242,7 +242,7 @@ def run_reference_arm(args, cfg):
         "tets_visited_per_ray": {"mean": vis / len(o)},
         "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": threads, "kind": kind,
                          "sample": f"full frame ({len(o)} rays) per step: compiled _kernels.cast_rays + "
-                                   "batch epilogue, ThreadPoolExecutor over 16 chunks/thread"},
+                                   "batch epilogue, ThreadPoolExecutor over min(16 per thread, n / 4096) chunks"},
         "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
