@@ -101,6 +101,24 @@ int tb_mesh_info(const tb_mesh* mesh, int* device, int* layout, int64_t* n_point
  * undefined, as in the reference). */
 int tb_mesh_validated(const tb_mesh* mesh, int* validated);
 
+/* Single-process multi-GPU trace (SURVEY 8 b's proposed tb_trace_multi; no
+ * reference counterpart -- the reference renderer's tile pool,
+ * render.py:496-541, is one process on CPU threads).  meshes[0..n_meshes)
+ * are replicas of one mesh (same layout and size), each resident on its own
+ * device (replicas may share a device).  The frame's width x height rays
+ * (o, d, start: device pointers on meshes[0]'s device, pixel-major) are split
+ * into 16 x 16-pixel tiles in render.py order, tile k to meshes[k % n].
+ * Every device walks its tiles reading the rays from meshes[0]'s device and
+ * stores each result into the output arrays there (also on meshes[0]'s
+ * device, same layout as tb_cast_rays; triangle / t / tet_back may be NULL):
+ * P2P loads and stores over NVLink, no staging copies, no collective.
+ * Asynchronous on `stream` (a stream of meshes[0]'s device): the other
+ * devices wait for the rays on it and `stream` waits for their results.
+ * Fails (TB_E_CUDA) when a device cannot access meshes[0]'s device. */
+int tb_trace_multi(int n_meshes, tb_mesh* const* meshes, int64_t width, int64_t height, const float* o,
+                   const float* d, const int32_t* start, uint8_t* status, int32_t* cf, int32_t* tet,
+                   int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back, void* stream);
+
 /* Measurement helper (no reference counterpart; SURVEY 8 d asks the roofline
  * to be reported against a measured L2 gather bandwidth when the hot arrays
  * fit in L2).  Gathers n_pairs (record, point) pairs of this mesh at

@@ -14,7 +14,10 @@
 #include <cstring>
 #include <algorithm>
 #include <atomic>
+#include <map>
 #include <mutex>
+#include <tuple>
+#include <vector>
 #include <string>
 
 #include "../../include/tetb200.h"
@@ -1749,6 +1752,135 @@ int tb_cast_rays_scatter(tb_mesh* m, int64_t n, const float* o, const float* d, 
     return set_error(TB_E_ARG, "NULL ray buffer");
   return cast_dispatch(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, (cudaStream_t)stream, 1,
                        false, out_index);
+}
+
+// Single-process multi-GPU trace (SURVEY 8 b's tb_trace_multi).  The frame's
+// 16 x 16-pixel tiles (render.py:496-514 order) go round-robin to the meshes;
+// every mesh's device walks its tiles straight from the frame's ray arrays on
+// meshes[0]'s device and stores each result into the frame's output arrays
+// there (cast_kernel's kGather + kScatter path: P2P loads and stores over
+// NVLink for the other devices, no staging copies, no collective).
+namespace {
+struct ShardKey {
+  int device;
+  int64_t width, height;
+  int parts, part;
+  bool operator<(const ShardKey& o) const {
+    return std::tie(device, width, height, parts, part) < std::tie(o.device, o.width, o.height, o.parts, o.part);
+  }
+};
+std::mutex g_shard_mu;
+std::map<ShardKey, std::pair<int64_t*, int64_t>> g_shards;  // device index arrays, kept for the process
+
+int shard_indices(int device, int64_t W, int64_t H, int parts, int part, const int64_t** idx, int64_t* count) {
+  std::lock_guard<std::mutex> lk(g_shard_mu);
+  const ShardKey key{device, W, H, parts, part};
+  auto it = g_shards.find(key);
+  if (it == g_shards.end()) {
+    std::vector<int64_t> h;
+    const int64_t tx = (W + 15) / 16, ty = (H + 15) / 16;
+    for (int64_t k = part; k < tx * ty; k += parts) {
+      const int64_t x0 = (k % tx) * 16, y0 = (k / tx) * 16;
+      for (int64_t y = y0; y < std::min(H, y0 + 16); ++y)
+        for (int64_t x = x0; x < std::min(W, x0 + 16); ++x) h.push_back(y * W + x);
+    }
+    int64_t* dptr = nullptr;
+    if (!h.empty()) {
+      DeviceGuard g(device);
+      TB_CUDA(cudaMalloc((void**)&dptr, h.size() * sizeof(int64_t)));
+      TB_CUDA(cudaMemcpy(dptr, h.data(), h.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    }
+    it = g_shards.emplace(key, std::make_pair(dptr, (int64_t)h.size())).first;
+  }
+  *idx = it->second.first;
+  *count = it->second.second;
+  return TB_OK;
+}
+
+// one non-blocking stream per (host thread, device) for the non-root devices
+cudaStream_t multi_stream(int device) {
+  static thread_local cudaStream_t streams[64] = {};
+  if (device < 0 || device >= 64) return nullptr;
+  if (!streams[device]) {
+    DeviceGuard g(device);
+    cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking);
+  }
+  return streams[device];
+}
+}  // namespace
+
+int tb_trace_multi(int n_meshes, tb_mesh* const* meshes, int64_t width, int64_t height, const float* o,
+                   const float* d, const int32_t* start, uint8_t* status, int32_t* cf, int32_t* tet,
+                   int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back, void* stream) {
+  if (n_meshes < 1 || n_meshes > 64 || !meshes) return set_error(TB_E_ARG, "n_meshes %d not in 1..64", n_meshes);
+  if (width < 0 || height < 0 || width * height >= ((int64_t)1 << 40)) return set_error(TB_E_ARG, "bad frame size");
+  if (width * height == 0) return TB_OK;
+  if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
+  for (int k = 0; k < n_meshes; ++k) {
+    if (int e = check_mesh(meshes[k])) return e;
+    if (meshes[k]->layout != meshes[0]->layout || meshes[k]->n_tets != meshes[0]->n_tets)
+      return set_error(TB_E_ARG, "mesh %d is not a replica of mesh 0 (layout / size differ)", k);
+  }
+  const int d0 = meshes[0]->device;
+  const cudaStream_t s0 = (cudaStream_t)stream;
+  cudaEvent_t ready = nullptr;
+  {
+    DeviceGuard g(d0);
+    TB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    TB_CUDA(cudaEventRecord(ready, s0));  // the rays are written on the caller's stream
+  }
+  int err = TB_OK;
+  std::vector<cudaEvent_t> done;
+  for (int k = 0; k < n_meshes && err == TB_OK; ++k) {
+    tb_mesh* m = meshes[k];
+    const int64_t* idx = nullptr;
+    int64_t count = 0;
+    if ((err = shard_indices(m->device, width, height, n_meshes, k, &idx, &count)) != TB_OK || count == 0) continue;
+    DeviceGuard g(m->device);
+    if (m->device != d0) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, m->device, d0);
+      if (!can) {
+        err = set_error(TB_E_CUDA, "device %d cannot access device %d's memory (no P2P)", m->device, d0);
+        break;
+      }
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(d0, 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) {
+        err = set_error(TB_E_CUDA, "enable peer access %d -> %d: %s", m->device, d0, cudaGetErrorString(pe));
+        break;
+      }
+      cudaGetLastError();
+    }
+    const cudaStream_t sk = m->device == d0 ? s0 : multi_stream(m->device);
+    if (sk != s0 && cudaStreamWaitEvent(sk, ready, 0) != cudaSuccess) {
+      err = set_error(TB_E_CUDA, "cross-device wait failed");
+      break;
+    }
+    if ((err = launch_layout<CastBinnedL>(m->layout, grid_for(count, kCastBlock), sk, m->safe, idx, m->view(), count, o,
+                                          d, start, status, cf, tet, visited, triangle, t, tet_back)) != TB_OK)
+      break;
+    if (sk != s0) {
+      cudaEvent_t ev = nullptr;
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess || cudaEventRecord(ev, sk) != cudaSuccess) {
+        err = set_error(TB_E_CUDA, "event on device %d failed", m->device);
+        break;
+      }
+      done.push_back(ev);
+    }
+  }
+  {
+    DeviceGuard g(d0);
+    for (cudaEvent_t ev : done) {
+      if (cudaStreamWaitEvent(s0, ev, 0) != cudaSuccess && err == TB_OK) err = set_error(TB_E_CUDA, "join failed");
+      cudaEventDestroy(ev);  // released once the wait has been enqueued
+    }
+    cudaEventDestroy(ready);
+  }
+  if (err == TB_OK) {
+    DeviceGuard g(d0);
+    TB_CUDA(cudaGetLastError());
+  }
+  return err;
 }
 
 int tb_device_alloc(size_t bytes, int device, void** out) {

@@ -350,3 +350,37 @@ class PeerFrameGather:
             self.frame = None
             lib.tb_device_free(self.base)
             self.base = None
+
+
+def trace_multi(meshes, width: int, height: int, origins, dirs, start, *, out=None, stream=None, epilogue=True):
+    """Single-process multi-GPU trace of one frame (``tb_trace_multi``).
+
+    ``meshes``: DeviceMesh replicas, one per GPU (``device_mesh(mesh, device=k)``);
+    ``origins`` / ``dirs`` (W*H, 3) float32 and ``start`` (W*H,) int32 are torch
+    tensors on ``meshes[0]``'s device.  The frame's 16x16 tiles go round-robin
+    to the replicas; each GPU walks its tiles straight from these arrays and
+    stores its results into ``out`` (a TraceResult on the same device) -- the
+    same arrays a single-GPU ``trace`` of the frame returns.
+    """
+    import ctypes
+
+    import torch
+
+    from ._lib import addr, check, lib
+    from .trace import empty_result
+
+    n = int(width) * int(height)
+    if origins.shape != (n, 3) or dirs.shape != (n, 3) or start.shape != (n,):
+        raise ValueError(f"rays must be ({n}, 3) / ({n},) for a {width}x{height} frame")
+    dev = origins.device
+    for x, dt in ((origins, torch.float32), (dirs, torch.float32), (start, torch.int32)):
+        if x.device != dev or x.dtype != dt or not x.is_contiguous():
+            raise ValueError("rays must be contiguous float32 / int32 tensors on one device")
+    res = out if out is not None else empty_result(n, dev)
+    handles = (ctypes.c_void_p * len(meshes))(*[m.handle.value for m in meshes])
+    s = (stream or torch.cuda.current_stream(dev)).cuda_stream
+    check(lib.tb_trace_multi(len(meshes), ctypes.cast(handles, ctypes.c_void_p), int(width), int(height), addr(origins), addr(dirs), addr(start),
+                             addr(res.status), addr(res.cf), addr(res.tet), addr(res.visited),
+                             addr(res.triangle) if epilogue else None, addr(res.t) if epilogue else None,
+                             addr(res.tet_back) if epilogue else None, s), "tb_trace_multi")
+    return res

@@ -74,3 +74,53 @@ def test_p2p_frame_assembly_two_ranks(tmp_path):
     path = str(tmp_path / "result.txt")
     mp.start_processes(_worker, args=(2, _free_port(), path), nprocs=2, start_method="spawn", join=True)
     assert open(path).read() == "ok"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("replicas,layout", [(1, "tet20"), (2, "tet20"), (3, "tet16")])
+def test_trace_multi_equals_single_trace(replicas, layout):
+    """tb_trace_multi with replicas sharing cuda:0 (the single-GPU box; on a
+    node each replica sits on its own GPU): the tile split, the gathered ray
+    reads and the scattered stores give exactly the single-GPU frame."""
+    import numpy as np
+    import torch
+
+    from paper_2103_02309_b200.device import DeviceMesh
+    from paper_2103_02309_b200.multigpu import trace_multi
+    from paper_2103_02309_b200.scenes import BLOB_CAMERA, blob_scene, camera_rays
+    from paper_2103_02309_b200.tetmesh import relayout
+    from paper_2103_02309_b200.trace import locate, trace
+
+    mesh = relayout(blob_scene(8, layout="tet20").mesh, layout)
+    W, H = 101, 67  # ragged edge tiles
+    o, d = camera_rays(BLOB_CAMERA["position"], BLOB_CAMERA["look_at"], BLOB_CAMERA["up"], BLOB_CAMERA["fov"], W, H)
+    dev = torch.device("cuda", 0)
+    dms = [DeviceMesh(mesh, 0) for _ in range(replicas)]
+    cam, _ = locate(dms[0], torch.tensor([BLOB_CAMERA["position"]], dtype=torch.float64, device=dev),
+                    torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))
+    go, gd = torch.from_numpy(o).to(dev), torch.from_numpy(d).to(dev)
+    gs = torch.full((W * H,), int(cam.item()), dtype=torch.int32, device=dev)
+    ref = trace(dms[0], go, gd, gs)
+    got = trace_multi(dms, W, H, go, gd, gs)
+    torch.cuda.synchronize()
+    for k in ("status", "cf", "tet", "visited", "triangle", "t", "tet_back"):
+        assert torch.equal(getattr(got, k), getattr(ref, k)), k
+    assert int(got.visited.min()) >= 1
+
+
+@pytest.mark.gpu
+def test_trace_multi_rejects_non_replicas():
+    import torch
+
+    from paper_2103_02309_b200._lib import TetB200Error
+    from paper_2103_02309_b200.device import DeviceMesh
+    from paper_2103_02309_b200.multigpu import trace_multi
+    from paper_2103_02309_b200.scenes import blob_scene
+    from paper_2103_02309_b200.tetmesh import relayout
+
+    mesh = blob_scene(6, layout="tet20").mesh
+    a, b = DeviceMesh(mesh, 0), DeviceMesh(relayout(mesh, "tet16"), 0)
+    z3 = torch.zeros((16 * 16, 3), dtype=torch.float32, device="cuda")
+    st = torch.zeros(16 * 16, dtype=torch.int32, device="cuda")
+    with pytest.raises(TetB200Error, match="replica"):
+        trace_multi([a, b], 16, 16, z3, z3, st)
