@@ -114,7 +114,9 @@ int tb_mesh_validated(const tb_mesh* mesh, int* validated);
  * P2P loads and stores over NVLink, no staging copies, no collective.
  * Asynchronous on `stream` (a stream of meshes[0]'s device): the other
  * devices wait for the rays on it and `stream` waits for their results.
- * Fails (TB_E_CUDA) when a device cannot access meshes[0]'s device. */
+ * Fails (TB_E_CUDA) when a device cannot access meshes[0]'s device.  The
+ * per-replica tile index arrays (8 B per pixel) are built once per (device,
+ * frame size, replica count) and kept for the process. */
 int tb_trace_multi(int n_meshes, tb_mesh* const* meshes, int64_t width, int64_t height, const float* o,
                    const float* d, const int32_t* start, uint8_t* status, int32_t* cf, int32_t* tet,
                    int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back, void* stream);
