@@ -101,6 +101,12 @@ int tb_mesh_info(const tb_mesh* mesh, int* device, int* layout, int64_t* n_point
  * undefined, as in the reference). */
 int tb_mesh_validated(const tb_mesh* mesh, int* validated);
 
+/* Copy an uploaded mesh to another device (or the same one) peer to peer:
+ * every device array, nothing rebuilt or revalidated (SURVEY 8 e: the mesh
+ * is replicated per GPU; from HBM over NVLink instead of a second host
+ * upload).  The replica is an independent handle (tb_mesh_destroy it). */
+int tb_mesh_replicate(const tb_mesh* src, int device, tb_mesh** out);
+
 /* Single-process multi-GPU trace (SURVEY 8 b's proposed tb_trace_multi; no
  * reference counterpart -- the reference renderer's tile pool,
  * render.py:496-541, is one process on CPU threads).  meshes[0..n_meshes)

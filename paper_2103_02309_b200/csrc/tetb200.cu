@@ -1670,6 +1670,51 @@ int tb_mesh_create(int device, int layout, int64_t n_points, const float* points
   return TB_OK;
 }
 
+// Device-to-device copy of an uploaded mesh (SURVEY 8 e: "mesh replicated --
+// upload from pinned host memory, or broadcast from GPU 0").  Every device
+// array is copied peer to peer (NVLink on a node); nothing is rebuilt or
+// revalidated, so a replica costs one HBM-to-HBM copy of the mesh.
+int tb_mesh_replicate(const tb_mesh* src, int device, tb_mesh** out) {
+  if (int e = check_mesh(src)) return e;
+  if (!out) return set_error(TB_E_ARG, "out is NULL");
+  *out = nullptr;
+  const int64_t np = src->n_points, nt = src->n_tets;
+  const int64_t rec_bytes = src->layout == 16 ? nt * 16 : src->layout == 32 ? nt * 32 : src->layout == 20 ? nt * 16
+                                                                                                            : nt * 80;
+  tb_mesh* m = new tb_mesh();
+  m->device = device;
+  m->layout = src->layout;
+  m->n_points = np; m->n_tets = nt; m->n_cf = src->n_cf; m->n_tri = src->n_tri;
+  m->safe = src->safe;
+  m->hbm_bytes = src->hbm_bytes;
+  m->hot_bytes = src->hot_bytes;
+  int err = TB_OK;
+  auto copy = [&](auto*& dst, const void* from, int64_t bytes) {
+    if (err != TB_OK || from == nullptr || bytes <= 0) return;
+    DeviceGuard g(device);
+    cudaError_t e = cudaMalloc((void**)&dst, (size_t)bytes);
+    if (e == cudaSuccess) e = cudaMemcpyPeer(dst, device, from, src->device, (size_t)bytes);
+    if (e != cudaSuccess)
+      err = set_error(e == cudaErrorMemoryAllocation ? TB_E_OOM : TB_E_CUDA, "replicate to device %d: %s", device,
+                      cudaGetErrorString(e));
+  };
+  copy(m->pts, src->pts, 6 * np * 16);
+  copy(m->rec4, src->rec4, rec_bytes);
+  copy(m->vx, src->vx, src->layout == 20 ? nt * 4 : 0);
+  copy(m->sv, src->sv, nt * 16);
+  copy(m->sn, src->sn, nt * 16);
+  copy(m->orient, src->orient, nt);
+  copy(m->cf_tri, src->cf_tri, src->n_cf * 4);
+  copy(m->cf_tets, src->cf_tets, src->n_cf * 8);
+  copy(m->tri, src->tri, src->n_tri * 72);
+  if (err != TB_OK) {
+    tb_mesh_destroy(m);
+    return err;
+  }
+  *out = m;
+  return TB_OK;
+}
+
 int tb_mesh_destroy(tb_mesh* m) {
   if (m == nullptr) return TB_OK;
   DeviceGuard g(m->device);

@@ -93,6 +93,18 @@ class DeviceMesh:
         self.validated = bool(ok.value)
         self._finalizer = weakref.finalize(self, lib.tb_mesh_destroy, h)
 
+    def replicate(self, device: int) -> "DeviceMesh":
+        """A copy of this device mesh on ``device``, made peer to peer from HBM
+        (``tb_mesh_replicate``; no host upload, no rebuild)."""
+        h = ctypes.c_void_p()
+        check(lib.tb_mesh_replicate(self.handle, int(device), ctypes.byref(h)), "tb_mesh_replicate")
+        rep = object.__new__(DeviceMesh)
+        rep.__dict__.update({k: v for k, v in self.__dict__.items() if k not in ("handle", "_finalizer")})
+        rep.device = int(device)
+        rep.handle = h
+        rep._finalizer = weakref.finalize(rep, lib.tb_mesh_destroy, h)
+        return rep
+
     @property
     def layout_code(self) -> int:
         return LAYOUT_CODES[self.layout]

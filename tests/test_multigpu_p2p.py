@@ -95,7 +95,8 @@ def test_trace_multi_equals_single_trace(replicas, layout):
     W, H = 101, 67  # ragged edge tiles
     o, d = camera_rays(BLOB_CAMERA["position"], BLOB_CAMERA["look_at"], BLOB_CAMERA["up"], BLOB_CAMERA["fov"], W, H)
     dev = torch.device("cuda", 0)
-    dms = [DeviceMesh(mesh, 0) for _ in range(replicas)]
+    dms = [DeviceMesh(mesh, 0)]
+    dms += [dms[0].replicate(0) for _ in range(replicas - 1)]  # peer copies (same device on this box)
     cam, _ = locate(dms[0], torch.tensor([BLOB_CAMERA["position"]], dtype=torch.float64, device=dev),
                     torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))
     go, gd = torch.from_numpy(o).to(dev), torch.from_numpy(d).to(dev)
