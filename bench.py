@@ -390,7 +390,20 @@ def run_ours(args, cfg):
         # rank's kernel stores every finished ray into rank 0's full-frame
         # arrays (CUDA IPC, P2P over NVLink) -- no collective moves the hits
         try:
-            pg = multigpu.PeerFrameGather(W, H, world, rank, world, dev)
+            root_rays = True  # lean assembly: ranks store 13 B per ray, rank 0 derives the epilogue
+            if rank == 0:
+                if cfg.get("secondaries"):
+                    root_rays = None  # secondaries are spawned per rank: the root lacks their rays
+                else:  # the job's rays in global order (frame-major), resident on rank 0 (untimed setup)
+                    frames_rays = [frame_rays(cfg, f)[:2] for f in range(world)]
+                    root_rays = tuple(torch.from_numpy(np.ascontiguousarray(np.concatenate([fr[i] for fr in
+                                                                                             frames_rays])))
+                                      .to(dev) for i in (0, 1))
+            lean_flags = [None] * world
+            dist.all_gather_object(lean_flags, root_rays is not None)
+            if not all(lean_flags):
+                root_rays = None
+            pg = multigpu.PeerFrameGather(W, H, world, rank, world, dev, root_rays=root_rays)
             gather_mode = "p2p"
 
             def step():  # noqa: F811  (the N > 1 step: fused trace + frame assembly)
@@ -714,7 +727,8 @@ def run_ours(args, cfg):
              "per_step": "every step assembles its frame set on rank 0 inside the timed region: each rank's trace "
                          "epilogue stores every finished ray into rank 0's full-frame arrays (CUDA IPC, P2P over "
                          "NVLink), then stream sync + barrier",
-             "bytes_to_rank0_per_step": int(29 * per_frame * (world - 1)), "collective": "none (barrier only)"}
+             "bytes_to_rank0_per_step": int((13 if pg.lean else 29) * per_frame * (world - 1)),
+             "lean": bool(pg.lean), "collective": "none (barrier only)"}
             if gather_mode == "p2p" else
             {"rays_gathered_to_rank0": gather_check, "rays_expected": per_frame * world, "error": gather_error,
              "mode": "nccl",
@@ -737,8 +751,9 @@ def run_ours(args, cfg):
         "roofline_issue": roofline_issue,
         "roofline_l2": roofline_l2,
         "clocks": dict(clocks.summary(clocks.t_ramp, clocks.t_end), window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
-        "gpu_launches": args.steps * (1 if fg is None else sum(1 for a, b in fg.my_pieces() if b > a))
-        * (4 if schedule == "binned" else 1),  # binned: count, scan, scatter, walk
+        "gpu_launches": args.steps * ((1 if fg is None else sum(1 for a, b in fg.my_pieces() if b > a))
+                                      * (4 if schedule == "binned" else 1)  # binned: count, scan, scatter, walk
+                                      + (1 if pg is not None and pg.lean else 0)),  # lean p2p: root epilogue
         "parity": parity,
         "e2e": e2e,
         "e2e_render": e2e_render,

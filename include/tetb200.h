@@ -101,6 +101,15 @@ int tb_mesh_info(const tb_mesh* mesh, int* device, int* layout, int64_t* n_point
  * undefined, as in the reference). */
 int tb_mesh_validated(const tb_mesh* mesh, int* validated);
 
+/* The batch epilogue alone (batch.py:57-71, _kernels_py._mt_t) from stored
+ * results: triangle = cf_triangle[cf], fp64 t, tet_back, for rays whose
+ * status / cf / tet came from a launch without the epilogue (the multi-GPU
+ * frame assembly ships 13 B per ray and the root derives the other 16).
+ * o, d, cf, tet, outputs: device pointers; identical to tb_cast_rays' fused
+ * epilogue bit for bit. */
+int tb_cast_epilogue(tb_mesh* mesh, int64_t n, const float* o, const float* d, const int32_t* cf,
+                     const int32_t* tet, int32_t* triangle, double* t, int32_t* tet_back, void* stream);
+
 /* Copy an uploaded mesh to another device (or the same one) peer to peer:
  * every device array, nothing rebuilt or revalidated (SURVEY 8 e: the mesh
  * is replicated per GPU; from HBM over NVLink instead of a second host

@@ -39,6 +39,7 @@ _SIGS = {
     ),
     "tb_mesh_validated": (c_int, [c_void_p, POINTER(c_int)]),
     "tb_probe_gather": (c_int, [c_void_p, c_int64, c_uint32, P, c_void_p]),
+    "tb_cast_epilogue": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, c_void_p]),
     "tb_mesh_replicate": (c_int, [c_void_p, c_int, POINTER(c_void_p)]),
     "tb_trace_multi": (c_int, [c_int, P, c_int64, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),
     "tb_cast_rays": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),

@@ -279,6 +279,33 @@ __device__ __forceinline__ void write_result(const MeshView& m, int64_t r, uint8
   }
 }
 
+// Batch epilogue alone (batch.py:57-71) from stored cf / tet: the multi-GPU
+// frame assembly ships only status / cf / tet / visited to the root, which
+// derives triangle, t and tet_back here from its own copy of the rays.
+__global__ void __launch_bounds__(256) epilogue_kernel(MeshView m, int64_t n, const float* __restrict__ o,
+                                                       const float* __restrict__ d, const int32_t* __restrict__ cf,
+                                                       const int32_t* __restrict__ tet, int32_t* __restrict__ triangle,
+                                                       double* __restrict__ t, int32_t* __restrict__ tet_back) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int32_t cfi = __ldg(cf + r);
+  int32_t tri = -1, back = -1;
+  double tt = INFINITY;
+  if (cfi >= 0) {
+    tri = __ldg(&m.cf_tri[cfi]);
+    if (t != nullptr)
+      tt = mt_t((double)__ldg(o + 3 * r), (double)__ldg(o + 3 * r + 1), (double)__ldg(o + 3 * r + 2),
+                (double)__ldg(d + 3 * r), (double)__ldg(d + 3 * r + 1), (double)__ldg(d + 3 * r + 2),
+                m.tri + 9 * (int64_t)tri);
+    const int2 ct = __ldg(&m.cf_tets[cfi]);
+    const int32_t cur = __ldg(tet + r);
+    back = (ct.x == cur) ? ct.y : ct.x;
+  }
+  if (triangle != nullptr) triangle[r] = tri;
+  if (t != nullptr) t[r] = tt;
+  if (tet_back != nullptr) tet_back[r] = back;
+}
+
 // ----------------------------------------------------------------------------
 // Cycle guard without the O(n_tets) walk.  The reference stops a ray once it
 // has visited more than n_tets tets (_kernels.pyx:365-368); rays that tie
@@ -1926,6 +1953,19 @@ int tb_trace_multi(int n_meshes, tb_mesh* const* meshes, int64_t width, int64_t 
     TB_CUDA(cudaGetLastError());
   }
   return err;
+}
+
+int tb_cast_epilogue(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* cf, const int32_t* tet,
+                     int32_t* triangle, double* t, int32_t* tet_back, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  if (n == 0) return TB_OK;
+  if (!o || !d || !cf || !tet) return set_error(TB_E_ARG, "NULL buffer");
+  DeviceGuard g(m->device);
+  epilogue_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(m->view(), n, o, d, cf, tet, triangle, t,
+                                                                         tet_back);
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
 }
 
 int tb_device_alloc(size_t bytes, int device, void** out) {

@@ -255,9 +255,16 @@ class PeerFrameGather:
     trace followed by a gather.  ``step`` ends with a stream sync and a
     barrier, after which the root's ``frame`` holds the whole job (the same
     arrays a single-GPU trace of all of it returns).
+
+    ``root_rays``: lean assembly.  Every rank passes it -- the root the job's
+    full (origins, dirs) device tensors in global ray order, the others
+    ``True`` -- and the ranks then store only status / cf / tet / visited
+    (13 B per ray over NVLink instead of 29); after the barrier the root
+    derives triangle / t / tet_back for the whole job with
+    ``tb_cast_epilogue`` (bit-identical to the fused epilogue).
     """
 
-    def __init__(self, width, height, world, rank, frames, device, root=0, group=None, tile=16):
+    def __init__(self, width, height, world, rank, frames, device, root=0, group=None, tile=16, root_rays=None):
         import ctypes
 
         import torch
@@ -266,6 +273,12 @@ class PeerFrameGather:
         from ._lib import check, lib
 
         self.world, self.rank, self.root, self.group = world, rank, root, group
+        # lean assembly (every rank passes root_rays=True, the root the job's
+        # (origins, dirs) tensors): ranks store only status / cf / tet /
+        # visited (13 B per ray instead of 29) and the root derives triangle,
+        # t and tet_back with tb_cast_epilogue from its own copy of the rays
+        self.lean = root_rays is not None
+        self.root_rays = root_rays if (self.lean and rank == root) else None
         self.device = torch.device(device)
         self.total = width * height * frames
         shard = shard_pixels(width, height, rank, world, tile, frames)
@@ -331,10 +344,17 @@ class PeerFrameGather:
         from ._lib import addr, check, lib
 
         s = stream or torch.cuda.current_stream(self.device)
+        # _OUTPUTS order: status, cf, tet, visited, triangle, t, tet_back
+        ptrs = self.ptrs[:4] + [None, None, None] if self.lean else self.ptrs
         check(lib.tb_cast_rays_scatter(dm.handle, self.idx.numel(), addr(origins), addr(dirs), addr(start),
-                                       addr(self.idx), *self.ptrs, s.cuda_stream), "tb_cast_rays_scatter")
+                                       addr(self.idx), *ptrs, s.cuda_stream), "tb_cast_rays_scatter")
         s.synchronize()  # this rank's stores have landed in the root's memory
         dist.barrier(group=self.group)
+        if self.root_rays is not None:
+            ro, rd = self.root_rays
+            check(lib.tb_cast_epilogue(dm.handle, self.total, addr(ro), addr(rd), self.ptrs[1], self.ptrs[2],
+                                       self.ptrs[4], self.ptrs[5], self.ptrs[6], s.cuda_stream), "tb_cast_epilogue")
+            s.synchronize()
         return self.frame
 
     def close(self):

@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, result_path):
+def _worker(rank, world, port, result_path, lean=False):
     import torch
     import torch.distributed as dist
 
@@ -50,7 +50,10 @@ def _worker(rank, world, port, result_path):
             d_all.append(d)
             st_all.append(np.full(len(o), cam[0], np.int32))
         o_all, d_all, st_all = (np.concatenate(a) for a in (o_all, d_all, st_all))
-        pg = multigpu.PeerFrameGather(W, H, world, rank, frames, dev)
+        root_rays = None
+        if lean:
+            root_rays = tuple(torch.from_numpy(a).to(dev) for a in (o_all, d_all)) if rank == 0 else True
+        pg = multigpu.PeerFrameGather(W, H, world, rank, frames, dev, root_rays=root_rays)
         idx = pg.idx.cpu().numpy()
         dm = device_mesh(mesh, device=0)
         g = [torch.from_numpy(a[idx]).to(dev) for a in (o_all, d_all, st_all)]
@@ -68,11 +71,15 @@ def _worker(rank, world, port, result_path):
 
 
 @pytest.mark.timeout(300)
-def test_p2p_frame_assembly_two_ranks(tmp_path):
+@pytest.mark.parametrize("lean", (False, True))
+def test_p2p_frame_assembly_two_ranks(tmp_path, lean):
+    """Two ranks (sharing cuda:0 here) assemble the frame set on rank 0 by P2P
+    stores; lean: 13 B per ray stored, triangle / t / tet_back derived on the
+    root (tb_cast_epilogue).  Either way the frame equals the oracle."""
     import torch.multiprocessing as mp
 
     path = str(tmp_path / "result.txt")
-    mp.start_processes(_worker, args=(2, _free_port(), path), nprocs=2, start_method="spawn", join=True)
+    mp.start_processes(_worker, args=(2, _free_port(), path, lean), nprocs=2, start_method="spawn", join=True)
     assert open(path).read() == "ok"
 
 
