@@ -530,7 +530,10 @@ def run_ours(args, cfg):
                     digs = json.load(open(dig_path))
                     if key in digs:  # frame 0 is the reference camera: compare with its digest
                         f0 = [full[k][:per_frame].cpu().numpy() for k in ("status", "cf", "tet", "visited")]
-                        gather_check = {"rays": gather_check, "frame0_vs_reference_digest": digest(*f0) == digs[key]}
+                        e0 = [full[k][:per_frame].cpu().numpy() for k in ("triangle", "t", "tet_back")]
+                        gather_check = {"rays": gather_check, "frame0_vs_reference_digest": digest(*f0) == digs[key],
+                                        "frame0_epilogue_vs_reference_digest":
+                                            digest(*e0) == digs[key.replace("/cast", "/epilogue")]}
         except Exception as exc:  # report, do not lose the line
             gather_error = repr(exc)
     my_ms = float(kernel_ms.sum())
