@@ -13,7 +13,7 @@ LIB := $(PKG)/libtetb200.so
 ORACLE := oracle/libtetoracle.so
 CSRC := $(PKG)/csrc/tetb200.cu
 HSRC := $(PKG)/csrc/host_mesh.cpp
-CHDR := $(PKG)/csrc/traverse.cuh $(PKG)/csrc/sctp.cuh include/tetb200.h
+CHDR := $(PKG)/csrc/traverse.cuh $(PKG)/csrc/sctp.cuh $(PKG)/csrc/binning.cuh include/tetb200.h
 CXX ?= g++
 # host mesh building: exact IEEE arithmetic like numpy (no contraction)
 CXXFLAGS := -O3 -std=c++17 -fPIC -ffp-contract=off -fno-fast-math -Wall
