@@ -170,3 +170,20 @@ def test_device_mesh_outlives_its_host_mesh(golden):
 
     with pytest.raises(TetB200Error):
         trace(dm, o, d, st.clamp(min=0))
+
+
+def test_multi_gpu_entry_points_validate_arguments():
+    """tb_trace_multi / tb_mesh_replicate / tb_cast_epilogue reject bad
+    arguments before touching a device (runs without a GPU)."""
+    import ctypes
+
+    from paper_2103_02309_b200._lib import lib
+
+    nulls = (None,) * 10
+    assert lib.tb_trace_multi(0, None, 16, 16, *nulls, None) == -1
+    assert b"n_meshes" in lib.tb_last_error()
+    assert lib.tb_trace_multi(65, None, 16, 16, *nulls, None) == -1
+    out = ctypes.c_void_p()
+    assert lib.tb_mesh_replicate(None, 0, ctypes.byref(out)) == -1
+    assert b"NULL" in lib.tb_last_error()
+    assert lib.tb_cast_epilogue(None, 1, *(None,) * 7, None) == -1
