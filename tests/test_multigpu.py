@@ -188,3 +188,12 @@ def test_gloo_world2_peer_gather_failure_is_collective(tmp_path):
     path = str(tmp_path / "result.txt")
     mp.start_processes(_peer_fail_worker, args=(2, _free_port(), path), nprocs=2, start_method="spawn", join=True)
     assert open(path).read() == "raised,raised"
+
+
+def test_trace_multi_checks_shapes_before_any_device_work():
+    """multigpu.trace_multi validates the frame's ray arrays on the host side."""
+    with pytest.raises(ValueError, match="frame"):
+        multigpu.trace_multi([], 4, 4, torch.zeros((15, 3)), torch.zeros((16, 3)), torch.zeros(16, dtype=torch.int32))
+    with pytest.raises(ValueError, match="contiguous"):
+        multigpu.trace_multi([], 4, 4, torch.zeros((16, 3), dtype=torch.float64), torch.zeros((16, 3)),
+                             torch.zeros(16, dtype=torch.int32))
