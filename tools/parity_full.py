@@ -9,6 +9,7 @@ the binned schedule -- and compares all seven output arrays bit for bit.
 Test infrastructure only (the oracle is the checker here, never measured).
 
     python tools/parity_full.py [--configs 3,4,5]
+    python tools/parity_full.py --layouts      # config 2 in every layout, 2-D and ScTP walks
 """
 
 from __future__ import annotations
@@ -79,5 +80,35 @@ def main():
                               "oracle_threads": os.cpu_count()}), flush=True)
 
 
+def layouts_cfg2():
+    """Config 2's full frame in every layout, 2-D and ScTP walks, vs the oracle
+    (TetMesh-80 against the oracle's own TetMesh-80 restatement)."""
+    from paper_2103_02309_b200.tetmesh import relayout
+
+    dev = torch.device("cuda", 0)
+    cfg = CONFIGS[2]
+    base = build_scene(cfg).mesh
+    o, d, pos = frame_rays(cfg, 0)
+    for layout in ("tet32", "tet20", "tet16", "tet80"):
+        mesh = base if layout in (base.layout, "tet80") else relayout(base, layout)
+        dm = device_mesh(mesh, layout=layout if layout == "tet80" else None)
+        cam, _ = locate(dm, torch.tensor(pos[None], dtype=torch.float64, device=dev),
+                        torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))
+        st = np.full(len(o), int(cam.item()), np.int32)
+        for sctp in (False, True):
+            if sctp and layout not in ("tet20", "tet80"):
+                continue
+            res = trace(dm, *(torch.from_numpy(a).to(dev) for a in (o, d, st)), sctp=sctp)
+            torch.cuda.synchronize()
+            exp = pyoracle.cast_rays_full(mesh, o, d, st, layout=dm.layout, sctp=sctp)
+            bad = compare(res, exp)
+            print(json.dumps({"config": 2, "rays": "primaries", "n": len(st), "layout": layout,
+                              "walk": "sctp" if sctp else "2d", "mismatched": bad, "bit_exact": not bad}),
+                  flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    if "--layouts" in sys.argv:
+        layouts_cfg2()
+    else:
+        main()
