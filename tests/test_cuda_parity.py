@@ -635,3 +635,31 @@ def test_schedules_without_epilogue(golden, O, schedule):
     exp = O.cast_rays_full(m, o, d, st)
     for k, a, b in zip(NAMES7[:4], (res.status, res.cf, res.tet, res.visited), exp[:4]):
         assert np.array_equal(a.cpu().numpy(), b), k
+
+
+def test_cast_epilogue_equals_fused_epilogue(golden):
+    """tb_cast_epilogue (the lean multi-GPU assembly's root pass) derives
+    triangle / t / tet_back from stored cf / tet bit for bit like the fused
+    epilogue, for hits and misses, in every host-visible layout."""
+    import torch
+
+    from paper_2103_02309_b200._lib import addr, check, lib
+    from paper_2103_02309_b200.device import device_mesh
+    from paper_2103_02309_b200.scenes import interior_rays
+    from paper_2103_02309_b200.trace import empty_result, trace
+
+    dev = torch.device("cuda", 0)
+    for layout in ("tet32", "tet20", "tet16"):
+        m = golden_mesh(golden, "model", layout)
+        o, d, st = interior_rays(m, 30_000, 44)
+        g = [torch.from_numpy(a).to(dev) for a in (o, d, st)]
+        full = trace(m, *g)
+        lean = trace(m, *g, epilogue=False)
+        out = empty_result(len(st), dev)
+        check(lib.tb_cast_epilogue(device_mesh(m).handle, len(st), addr(g[0]), addr(g[1]), addr(lean.cf),
+                                   addr(lean.tet), addr(out.triangle), addr(out.t), addr(out.tet_back),
+                                   torch.cuda.current_stream(dev).cuda_stream), "tb_cast_epilogue")
+        torch.cuda.synchronize()
+        assert int((full.status == 1).sum()) > 0 and int((full.status == 0).sum()) >= 0
+        for k in ("triangle", "t", "tet_back"):
+            assert torch.equal(getattr(out, k), getattr(full, k)), (layout, k)
