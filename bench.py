@@ -4,23 +4,39 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
     torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
 
+``--gpus N`` without a torchrun environment relaunches itself under
+``torch.distributed.run`` with N ranks (fails loudly when N exceeds the
+visible GPUs).
+
 Workload (BASELINE.json configs[1], the metric's single-GPU config):
 config 2 = the reference's blob generator at GRID=55 (1,109,444 tets,
 byte-identical to gen_model_mesh -> parse_tetgen -> encode, pinned by
 tests/test_host_mirror.py), TetMesh-20, Hilbert-sorted, 1920x1080 primary
 rays from the blob camera, all starting in the located camera tet.
 A "step" traces one frame per GPU.  Weak scaling: at N GPUs the job is N
-frames (camera jittered per frame), 16x16 tiles dealt round-robin to ranks,
-hit buffers gathered to rank 0 with one NCCL collective inside the timed
-region.
+frames (camera moved per frame), 16x16 tiles dealt round-robin to ranks,
+every ray's results stored into rank 0's frame arrays inside the trace
+(P2P over NVLink) -- the frame set is assembled on rank 0 every step.
 
-value  = rays / device time of the trace kernel (CUDA events on the launch
-         stream, inputs resident in HBM, L2 flushed between steps).
-e2e    = the same rays through the C ABI with pinned HOST buffers
-         (tb_cast_rays_host: H2D, kernel, D2H, sync) per step.
-roofline = SURVEY.md s8(d) algorithmic bytes / kernel time vs measured HBM.
-cpu_baseline = the reference's compiled kernels (oracle/_ref) + its batch
-         epilogue on all host cores (rank 0, N=1, bounded sample).
+value    = rays / device time of the trace (CUDA events on the launch stream,
+           inputs resident in HBM, 256 MiB written between steps to flush L2).
+e2e      = the same metric through the C ABI with pinned HOST buffers
+           (N=1: tb_cast_rays_host, rays read / hits written over PCIe; N>1:
+           H2D of each rank's rays + fused trace/assembly + D2H of rank 0's
+           assembled frame), per step.
+roofline = the binding roof of the walk: instruction issue (SASS per step
+           from tools/sass_steps.py x walk steps vs SMs x 4 schedulers x
+           clock x 32 lanes).  The SURVEY s8(d) algorithmic bytes over HBM
+           and over a measured L2 gather roof ride along as roofline_hbm /
+           roofline_l2, ncu DRAM bytes per launch as roofline.traffic.
+secondary_cfg4 = BASELINE config 4 (16.7 M diffuse secondaries from
+           4096x4096 primary hits, Tet16) measured in the same run.
+cpu_baseline / --impl reference = the reference's own public API
+           (tetray.batch.cast_rays on its compiled kernels, installed under
+           oracle/_ref/site) on all host threads.  The reference arm loads
+           its scene with tetray.cli.load_compact from a file the reference's
+           own pipeline wrote (oracle/make_ref_scene.py) and never maps this
+           repo's CUDA library.
 """
 
 from __future__ import annotations
@@ -49,12 +65,13 @@ CONFIGS = {
             desc="cfg4: blob GRID=55, 16.7M diffuse secondaries from 4096x4096 primary hits, TetMesh-16"),
     # config 5 names no layout (BASELINE.json configs[4]); with 180 GB of HBM the
     # 1 GB TetMesh-20 beats the 0.8 GB TetMesh-16 (r01 A/B: 825 vs 707 Mrays/s)
-    5: dict(kuhn=203, width=7680, height=4320, layout="tet20", scheme="none",
+    5: dict(kuhn=203, width=7680, height=4320, layout="tet20", scheme="none", sample_stride=64,
             desc="cfg5: Kuhn box n=203 (50,192,562 tets) stretched 4x in z with thin strip occluders "
                  "(long thin triangles), 7680x4320 primary rays, TetMesh-20"),
 }
 L2_FLUSH_BYTES = 256 << 20
 FALLBACK_HBM_GBS = 6650.0
+LAYOUT_BYTES = {"tet32": 32, "tet20": 20, "tet16": 16, "tet80": 80}
 
 
 def log(*a):
@@ -76,27 +93,34 @@ def measured_peak():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def build_scene(cfg):
-    from paper_2103_02309_b200.scenes import blob_scene, kuhn_strip_scene
+def config_dict(cfg, world: int) -> dict:
+    """The workload description -- identical in both arms (the driver compares them)."""
+    return {"workload": cfg["desc"], "rays_per_gpu": cfg["width"] * cfg["height"], "frames": world,
+            "layout": cfg["layout"], "scheme": cfg["scheme"],
+            "parallelism": f"tile-shard x{world}, mesh replicated" if world > 1 else "single GPU",
+            "l2": "GPU arm writes 256 MiB between timed steps (L2 flush); CPU arm n/a"}
 
-    t0 = time.perf_counter()
-    if "kuhn" in cfg:
-        sc = kuhn_strip_scene(cfg["kuhn"], layout=cfg["layout"], scheme=cfg["scheme"])
-    else:
-        host_layout = "tet32" if cfg["layout"] == "tet80" else cfg["layout"]
-        sc = blob_scene(cfg["grid"], layout=host_layout, scheme=cfg["scheme"], check=False)
-    log(f"[bench] scene {sc.name}: {sc.mesh.n_tets} tets, {sc.mesh.n_points} points, "
-        f"{sc.mesh.n_constrained} constrained faces, built in {time.perf_counter() - t0:.1f}s")
-    return sc
+
+def camera_of(cfg, frame: int = 0):
+    from paper_2103_02309_b200.workload import BLOB_CAMERA, kuhn_camera
+
+    cam = dict(kuhn_camera(cfg["kuhn"]) if "kuhn" in cfg else BLOB_CAMERA)
+    cam["position"] = tuple(np.asarray(cam["position"], dtype=np.float64) + np.array([0.0, 0.02, 0.0]) * frame)
+    return cam
 
 
 def frame_rays(cfg, frame: int):
-    from paper_2103_02309_b200.scenes import BLOB_CAMERA, camera_rays, kuhn_camera
+    from paper_2103_02309_b200.workload import camera_rays
 
-    cam = kuhn_camera(cfg["kuhn"]) if "kuhn" in cfg else BLOB_CAMERA
-    pos = np.asarray(cam["position"], dtype=np.float64) + np.array([0.0, 0.02, 0.0]) * frame
-    o, d = camera_rays(tuple(pos), cam["look_at"], cam["up"], cam["fov"], cfg["width"], cfg["height"])
-    return o, d, pos
+    cam = camera_of(cfg, frame)
+    o, d = camera_rays(cam["position"], cam["look_at"], cam["up"], cam["fov"], cfg["width"], cfg["height"])
+    return o, d, np.asarray(cam["position"], dtype=np.float64)
+
+
+def sample_pixels(cfg) -> np.ndarray | None:
+    """Config 5's reference sample: every 64th pixel."""
+    s = cfg.get("sample_stride")
+    return None if not s else np.arange(0, cfg["width"] * cfg["height"], s, dtype=np.int64)
 
 
 class ClockSampler:
@@ -109,7 +133,7 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list = []
 
     def __enter__(self):
         try:
@@ -160,92 +184,205 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_trace(mesh, o, d, st, threads: int):
-    """The reference's CPU path for one batch: compiled kernels (oracle/_ref,
-    _kernels.pyx:271-370, GIL released) + the batch epilogue (batch.py:57-71),
-    chunked over a thread pool like the reference renderer's tile pool."""
+# ---------------------------------------------------------------------------
+# The reference's CPU path (oracle/_ref/site: the unmodified tetray package)
+
+def ref_package():
+    """The installed reference (oracle/_ref/site, built by oracle/build_ref.sh)."""
+    site = os.path.join(ROOT, "oracle", "_ref", "site")
+    if not os.path.isdir(os.path.join(site, "tetray")):
+        raise RuntimeError(f"{site}/tetray missing: run oracle/build_ref.sh (or __graft_entry__.build())")
+    if site not in sys.path:
+        sys.path.insert(0, site)
+    import tetray
+    from tetray import backend
+
+    if backend.active_backend() != "compiled":
+        raise RuntimeError("the reference's compiled kernels did not import")
+    return tetray
+
+
+def ref_trace(mesh, o, d, st, threads: int, *, outputs: bool = False):
+    """The reference's CPU path for one batch, through its public API:
+    tetray.batch.cast_rays (compiled _kernels.cast_rays, GIL released, +
+    the batch epilogue, batch.py:39-80) over a thread pool of >= 4096-ray
+    chunks, the way its renderer's tile pool calls it (render.py:538-541).
+    Returns the summed visited count (and the 7 arrays when ``outputs``)."""
     from concurrent.futures import ThreadPoolExecutor
 
-    from oracle import pyoracle
+    from tetray import batch
 
-    K = pyoracle.ref_kernels()
-    kind = "reference"
-    if K is None:
-        K, kind = pyoracle, "port"
     n = len(st)
-    chunks = max(1, min(threads * 16, n // 4096))  # >= 4096 rays per chunk: pool overhead stays small
+    chunks = max(1, min(threads * 16, n // 4096))
     bounds = np.linspace(0, n, chunks + 1).astype(np.int64)
+    res = [None] * chunks
 
     def work(i):
         a, b = bounds[i], bounds[i + 1]
         if a == b:
             return 0
-        status, cf, tet, visited = K.cast_rays(mesh, o[a:b], d[a:b], st[a:b])
-        pyoracle.batch_epilogue(mesh, o[a:b], d[a:b], status, cf, tet)
-        return int(visited.sum())
+        h = batch.cast_rays(mesh, o[a:b], d[a:b], st[a:b])
+        if outputs:
+            res[i] = (h.status, h.cf, h.tet_front, h.visited, h.triangle, h.t, h.tet_back)
+        return int(h.visited.sum())
 
     with ThreadPoolExecutor(max_workers=threads) as pool:
         total_vis = sum(pool.map(work, range(chunks)))
-    return kind, total_vis
+    if outputs:
+        parts = [r for r in res if r is not None]
+        return total_vis, [np.concatenate([p[k] for p in parts]) for k in range(7)]
+    return total_vis
 
 
-def cpu_single_thread(mesh, o, d, st, reps: int = 2) -> dict:
-    """the reference's CPU path on ONE thread, its compiled
-    kernels and the host batch epilogue timed separately (best of reps)."""
-    from oracle import pyoracle
+def ref_cast_full(mesh, o, d, st, threads: int):
+    """The 7 result arrays of the reference (parity checker, never measured)."""
+    return ref_trace(mesh, o, d, st, threads, outputs=True)[1]
 
-    K = pyoracle.ref_kernels() or pyoracle
-    best_k = best_e = None
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        status, cf, tet, _ = K.cast_rays(mesh, o, d, st)
-        t1 = time.perf_counter()
-        pyoracle.batch_epilogue(mesh, o, d, status, cf, tet)
-        t2 = time.perf_counter()
-        best_k = t1 - t0 if best_k is None else min(best_k, t1 - t0)
-        best_e = t2 - t1 if best_e is None else min(best_e, t2 - t1)
-    n = len(st)
-    return {"value": n / (best_k + best_e) / 1e6, "unit": "Mrays/s", "cores": 1, "rays": n,
-            "kernel_only": n / best_k / 1e6, "epilogue_share": best_e / (best_k + best_e)}
+
+def ref_scene(cfg):
+    """The config's scene as a reference CompactMesh, never touching this
+    repo's CUDA library: blob scenes from the file the reference's own
+    pipeline wrote (oracle/make_ref_scene.py; built here if missing),
+    re-encoded with the reference's relayout; the Kuhn box (too large for the
+    reference's Python builder) from raw arrays dumped by a child process of
+    the native builder, wrapped in the reference's CompactMesh."""
+    ref_package()
+    from tetray.cli import load_compact
+    from tetray.tetmesh import LAYOUT_DTYPES, CompactMesh, SceneTriangleSoup, relayout
+
+    layout = "tet32" if cfg["layout"] == "tet80" else cfg["layout"]
+    if "grid" in cfg:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import make_ref_scene
+
+        path = make_ref_scene.scene_path(cfg["grid"], "tet20", cfg["scheme"])
+        if not path.exists():
+            log(f"[bench/ref] building {path.name} with the reference pipeline (minutes)")
+            make_ref_scene.build(cfg["grid"], "tet20", cfg["scheme"])
+        return relayout(load_compact(path), layout), "reference pipeline (oracle/make_ref_scene.py) + load_compact"
+    out = os.path.join("/tmp", f"tetb200_kuhn{cfg['kuhn']}_{layout}_{cfg['scheme']}")
+    if not os.path.exists(os.path.join(out, "done")):
+        subprocess.run([sys.executable, os.path.abspath(__file__), "--dump-scene", str(cfg["kuhn"]), "--layout",
+                        layout, "--scheme", cfg["scheme"], "--out", out], check=True)
+    z = {k: np.load(os.path.join(out, k + ".npy")) for k in
+         ("points", "records", "side_verts", "side_neighbors", "cf_triangle", "cf_tets", "cf_verts", "soup_vertices",
+          "soup_triangles", "soup_materials", "source_tet")}
+    mesh = CompactMesh(layout=layout, points=z["points"], records=z["records"].view(LAYOUT_DTYPES[layout]).reshape(-1),
+                       side_verts=z["side_verts"], side_neighbors=z["side_neighbors"], cf_triangle=z["cf_triangle"],
+                       cf_tets=z["cf_tets"], cf_verts=z["cf_verts"], source_tet=int(z["source_tet"]),
+                       soup=SceneTriangleSoup(vertices=z["soup_vertices"], triangles=z["soup_triangles"],
+                                              material_ids=z["soup_materials"]))
+    return mesh, "native builder arrays (child process) wrapped in the reference's CompactMesh"
+
+
+def dump_scene(n: int, layout: str, scheme: str, out: str):
+    """--dump-scene: the config-5 Kuhn mesh as raw .npy arrays for the reference arm."""
+    from paper_2103_02309_b200.scenes import kuhn_strip_scene
+
+    m = kuhn_strip_scene(n, layout=layout, scheme=scheme).mesh
+    os.makedirs(out, exist_ok=True)
+    for k, v in (("points", m.points), ("records", m.records_u32()), ("side_verts", m.side_verts),
+                 ("side_neighbors", m.side_neighbors), ("cf_triangle", m.cf_triangle), ("cf_tets", m.cf_tets),
+                 ("cf_verts", m.cf_verts), ("soup_vertices", m.soup.vertices), ("soup_triangles", m.soup.triangles),
+                 ("soup_materials", m.soup.material_ids), ("source_tet", np.array(m.source_tet))):
+        np.save(os.path.join(out, k + ".npy"), np.ascontiguousarray(v))
+    open(os.path.join(out, "done"), "w").close()
+
+
+def ref_rays(cfg, mesh, frame: int = 0, pixels=None):
+    """Rays of the config through the reference's own camera
+    (render.camera_rays, render.py:169-185) and its locate_points."""
+    from tetray import batch
+    from tetray.render import RenderConfig, camera_rays
+
+    cam = camera_of(cfg, frame)
+    W, H = cfg["width"], cfg["height"]
+    rc = RenderConfig(camera_position=cam["position"], camera_look_at=cam["look_at"], camera_up=cam["up"],
+                      fov=cam["fov"], width=W, height=H)
+    pix = np.arange(W * H, dtype=np.int64) if pixels is None else pixels
+    o, d = camera_rays(rc, (pix % W).astype(np.float64), (pix // W).astype(np.float64))
+    cam_tet, _ = batch.locate_points(mesh, np.asarray(cam["position"], dtype=np.float64)[None])
+    return np.ascontiguousarray(o), np.ascontiguousarray(d), np.full(len(o), int(cam_tet[0]), np.int32)
+
+
+def native_libs_loaded() -> list:
+    """In-tree shared objects mapped into this process (reference-arm hygiene)."""
+    libs = set()
+    try:
+        for line in open("/proc/self/maps"):
+            p = line.split()[-1] if line.strip() else ""
+            if p.endswith(".so") or ".so." in p:
+                if p.startswith(ROOT):
+                    libs.add(os.path.relpath(p, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
 
 
 def run_reference_arm(args, cfg):
     world, rank, _ = dist_env()
+    world = max(world, args.gpus)
     if rank != 0:
         return
-    sc = build_scene(cfg)
-    mesh = sc.mesh
-    from oracle import pyoracle
-
-    o, d, pos = frame_rays(cfg, 0)
-    K = pyoracle.ref_kernels() or pyoracle
-    cam, _ = K.locate_points(mesh, pos[None], np.array([mesh.source_tet], np.int32))
-    st = np.full(len(o), int(cam[0]), dtype=np.int32)
+    t0 = time.perf_counter()
+    tetray = ref_package()
+    mesh, scene_src = ref_scene(cfg)
+    log(f"[bench/ref] scene {mesh.n_tets} tets ({scene_src}) in {time.perf_counter() - t0:.1f}s")
     threads = os.cpu_count() or 1
+    pix = sample_pixels(cfg)
+    o, d, st = ref_rays(cfg, mesh, 0, pix)
+    sample = f"frame 0, {len(o)} rays" + (" (every 64th pixel)" if pix is not None else " (full frame)")
+    if cfg.get("secondaries"):
+        from paper_2103_02309_b200.workload import diffuse_secondaries
+
+        _, prim = ref_trace(mesh, o, d, st, threads, outputs=True)  # untimed: the primaries
+        o, d, st = diffuse_secondaries(o, d, prim[5], prim[4], prim[2], mesh.triangle_coords(), seed=4)
+        m = min(len(st), args.ref_sample)
+        o, d, st = o[:m], d[:m], st[:m]
+        sample = f"first {m} of the frame's diffuse secondaries (seed 4)"
     for _ in range(args.warmup):
-        kind, _ = cpu_reference_trace(mesh, o, d, st, threads)
+        ref_trace(mesh, o, d, st, threads)
     times = []
+    vis = 0
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        kind, vis = cpu_reference_trace(mesh, o, d, st, threads)
-        times.append(time.perf_counter() - t0)
+        s0 = time.perf_counter()
+        vis = ref_trace(mesh, o, d, st, threads)
+        times.append(time.perf_counter() - s0)
     total = sum(times)
-    value = len(o) * args.steps / total / 1e6
+    value = len(st) * args.steps / total / 1e6
     line = {
-        "impl": "reference", "metric": "Mrays/s", "value": value, "unit": "Mrays/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": "Mrays/s", "value": value, "unit": "Mrays/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "rays_per_step": len(o), "layout": mesh.layout,
-                   "scheme": cfg["scheme"],
-                   **({"note": "the reference has no TetMesh-80 layout and no ScTP walk: its 2-D walk on "
-                               "the Tet32 mesh of the same scene and rays"} if cfg["layout"] == "tet80" else {})},
-        "tets_visited_per_ray": {"mean": vis / len(o)},
-        "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": threads, "kind": kind,
-                         "sample": f"full frame ({len(o)} rays) per step: compiled _kernels.cast_rays + "
-                                   "batch epilogue, ThreadPoolExecutor over min(16 per thread, n / 4096) chunks"},
+        "config": config_dict(cfg, world),
+        "tets_visited_per_ray": {"mean": vis / len(st)},
+        "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": threads, "kind": "reference",
+                         "sample": sample + ": tetray.batch.cast_rays (compiled kernels + batch epilogue), "
+                                            "ThreadPoolExecutor over min(16 per thread, n / 4096) chunks"},
         "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference": {"package": os.path.relpath(os.path.dirname(tetray.__file__), ROOT), "scene": scene_src,
+                      "layout_note": ("the reference has no TetMesh-80 and no ScTP walk: its 2-D walk on the "
+                                      "Tet32 mesh of the same scene and rays") if cfg["layout"] == "tet80" else None},
+        "native_so_loaded": native_libs_loaded(),
     }
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# Our arm
+
+def build_scene(cfg):
+    from paper_2103_02309_b200.scenes import blob_scene, kuhn_strip_scene
+
+    t0 = time.perf_counter()
+    if "kuhn" in cfg:
+        sc = kuhn_strip_scene(cfg["kuhn"], layout=cfg["layout"], scheme=cfg["scheme"])
+    else:
+        host_layout = "tet32" if cfg["layout"] == "tet80" else cfg["layout"]
+        sc = blob_scene(cfg["grid"], layout=host_layout, scheme=cfg["scheme"], check=False)
+    log(f"[bench] scene {sc.name}: {sc.mesh.n_tets} tets, {sc.mesh.n_points} points, "
+        f"{sc.mesh.n_constrained} constrained faces, built in {time.perf_counter() - t0:.1f}s")
+    return sc
 
 
 def digest(*arrays) -> str:
@@ -259,10 +396,55 @@ def digest(*arrays) -> str:
 
 def algorithmic_bytes(visited: np.ndarray, layout: str) -> int:
     """sum_rays [(visited-1)(L+12) + 68] + 53 N."""
-    L = {"tet32": 32, "tet20": 20, "tet16": 16, "tet80": 80}[layout]
+    L = LAYOUT_BYTES[layout]
     point = 0 if layout == "tet80" else 12
     v = visited.astype(np.int64)
     return int(((v - 1) * (L + point)).sum() + 68 * len(v) + 53 * len(v))
+
+
+def timed(fn, steps: int, warmup: int, stream, flush):
+    """Device time per call (ms): CUDA events on the launch stream, L2 flushed before each."""
+    import torch
+
+    for _ in range(warmup):
+        flush.zero_()
+        fn()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for a, b in evs:
+        flush.zero_()
+        a.record(stream)
+        fn()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return np.array([a.elapsed_time(b) for a, b in evs])
+
+
+def issue_roof(layout: str, schedule: str, walk_steps: float, kern_s: float, clk_mhz, sms: int):
+    """The walk's binding roof: SASS instructions per walk step (tools/
+    sass_steps.py, committed per build) at full issue on every scheduler."""
+    sp = os.path.join(ROOT, "profiles", "sass_step_counts.json")
+    if not (os.path.exists(sp) and clk_mhz):
+        return None
+    counts = json.load(open(sp))
+    kname = "cast_compact_kernel" if schedule in ("compact", "compact512") else "cast_kernel"
+    entry = counts.get(f"{kname}<{layout[3:]}, validated>") or counts.get(f"{kname}<{layout[3:]}, clamp>")
+    if not entry:
+        return None
+    per_step = (entry.get("unrolled_x4_per_step") or entry["single_step"])["total"]
+    peak_steps = sms * 4 * clk_mhz * 1e6 * 32 / per_step
+    ach = walk_steps / kern_s
+    return {"bound": "issue", "achieved": ach / 1e9, "peak": peak_steps / 1e9, "unit": "G ray-steps/s",
+            "frac": ach / peak_steps, "sass_per_step": per_step, "sms": sms, "sm_mhz": clk_mhz,
+            "note": "peak = SMs x 4 schedulers x SM clock x 32 lanes / SASS instructions per walk step; the gap "
+                    "is init/epilogue, SIMT divergence, issue stalls and the tail"}
+
+
+def traffic_of(key: str):
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        return json.load(open(tp)).get(key)
+    return None
 
 
 def l2_gather_roof(dm, stream, flush, layout: str, walk_steps: float, achieved_gbs: float) -> dict:
@@ -275,36 +457,32 @@ def l2_gather_roof(dm, stream, flush, layout: str, walk_steps: float, achieved_g
 
     from paper_2103_02309_b200._lib import check, lib
 
-    L = {"tet32": 32, "tet20": 20, "tet16": 16}[layout]
+    L = LAYOUT_BYTES[layout]
     n_pairs = int(min(max(32 << 20, walk_steps), 256 << 20))
     sink = torch.zeros(1, dtype=torch.int32, device=flush.device)
 
     def probe():
         check(lib.tb_probe_gather(dm.handle, n_pairs, 12345, sink.data_ptr(), stream.cuda_stream), "tb_probe_gather")
 
-    for _ in range(2):
-        probe()
-    ms = []
-    for _ in range(5):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        probe()
-        b.record(stream)
-        torch.cuda.synchronize()
-        ms.append(a.elapsed_time(b))
-    t = float(np.median(ms)) / 1e3
+    t = float(np.median(timed(probe, 5, 2, stream, flush))) / 1e3
     peak = n_pairs * (L + 12) / t / 1e9
     l2 = torch.cuda.get_device_properties(flush.device).L2_cache_size
-    resident = dm.hot_bytes <= l2
-    return {"bound": "l2_gather", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
-            "frac": achieved_gbs / peak,
+    return {"bound": "l2_gather", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s", "frac": achieved_gbs / peak,
             "probe": {"kernel": f"gather_probe_kernel<{L}>", "pairs": n_pairs, "bytes_per_pair": L + 12,
                       "ms": t * 1e3, "working_set_bytes": int(dm.hot_bytes), "l2_bytes": int(l2)},
-            "note": ("peak = random (record, point) gathers over this mesh's hot arrays "
-                     + ("(L2 resident)" if resident else "(larger than L2: an HBM random-gather roof)")
-                     + "; the walk exceeds it when coherent rays share L1/L2 lines (frac > 1) -- its binding "
-                       "roof is roofline_issue")}
+            "note": "peak = random (record, point) gathers over this mesh's hot arrays; the walk exceeds it when "
+                    "coherent rays share L1/L2 lines (frac > 1) -- its binding roof is `roofline` (issue)"}
+
+
+def parity_vs_reference(mesh, o, d, st, got, stride: int, threads: int, layout: str) -> dict:
+    """A strided sample of rays against the reference itself (oracle/_ref/
+    site: tetray.batch.cast_rays on its compiled kernels) -- the checker."""
+    sl = slice(0, len(st), stride)
+    exp = ref_cast_full(mesh_for_ref(mesh, {"layout": layout}), o[sl], d[sl], st[sl], threads)
+    names = ("status", "cf", "tet", "visited", "triangle", "t", "tet_back")
+    mism = {k: int(np.count_nonzero(g[sl] != e)) for k, g, e in zip(names, got, exp)}
+    return {"vs": f"reference tetray.batch.cast_rays (oracle/_ref) on every {stride}th ray",
+            "rays_checked": int(len(exp[0])), "mismatched_values": mism, "bit_exact": not any(mism.values())}
 
 
 def run_ours(args, cfg):
@@ -320,7 +498,10 @@ def run_ours(args, cfg):
     # one rank per GPU; TETB200_DIST_BACKEND=gloo lets several ranks share one
     # GPU to exercise the N>1 code path on a single device (test only)
     backend = os.environ.get("TETB200_DIST_BACKEND", "nccl")
-    local = local % torch.cuda.device_count()
+    ndev = torch.cuda.device_count()
+    if world > ndev and backend == "nccl":
+        raise SystemExit(f"--gpus {world} but only {ndev} visible GPU(s)")
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -336,6 +517,7 @@ def run_ours(args, cfg):
     sctp = cfg.get("walk") == "sctp"
     W, H = cfg["width"], cfg["height"]
     per_frame = W * H
+    threads = os.cpu_count() or 1
 
     # this rank's share of the N-frame job (16x16 tiles round-robin)
     idx = multigpu.shard_pixels(W, H, rank, world, 16, frames=world)
@@ -354,7 +536,7 @@ def run_ours(args, cfg):
     if cfg.get("secondaries"):
         # config 4: the timed rays are the diffuse secondaries spawned from this
         # shard's primary hits (traced here, untimed), in shard order
-        from paper_2103_02309_b200.scenes import diffuse_secondaries
+        from paper_2103_02309_b200.workload import diffuse_secondaries
 
         prim = trace(dm, *(torch.from_numpy(a).to(dev) for a in (o, d, st)))
         torch.cuda.synchronize()
@@ -368,46 +550,36 @@ def run_ours(args, cfg):
     res = empty_result(n, dev)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
-    gidx = torch.from_numpy(idx).to(dev)
 
     # ray schedule: one ray per lane for primaries; incoherent secondaries
     # (config 4) are binned by direction cell first (96 cube-map cells) and
-    # walked in binned order (r01: 3.36 vs 2.37 Grays/s one ray per lane,
-    # 2.30 block compaction; profiles/r01_experiments.md) -- what a
-    # renderer's bounce pass selects with trace(schedule="binned").  --schedule or
-    # TETB200_SCHED (sweeps, via the process-wide "auto" setting) override.
+    # walked in binned order (r01: 3.36 vs 2.37 Grays/s one ray per lane).
     schedule = args.schedule or ("auto" if os.environ.get("TETB200_SCHED") else
                                  ("binned" if cfg.get("secondaries") else "lane"))
 
     def step():
         trace(dm, go, gd, gs, out=res, stream=stream, sctp=sctp, schedule=schedule)
 
-    fg = None
-    pg = None
+    fg = pg = None
     gather_mode = None
     if world > 1 and args.gather == "p2p":
         # every step assembles its frame set on rank 0 inside the trace: each
         # rank's kernel stores every finished ray into rank 0's full-frame
         # arrays (CUDA IPC, P2P over NVLink) -- no collective moves the hits
         try:
-            root_rays = True  # lean assembly: ranks store 13 B per ray, rank 0 derives the epilogue
-            if rank == 0:
-                if cfg.get("secondaries"):
-                    root_rays = None  # secondaries are spawned per rank: the root lacks their rays
-                else:  # the job's rays in global order (frame-major), resident on rank 0 (untimed setup)
-                    frames_rays = [frame_rays(cfg, f)[:2] for f in range(world)]
-                    root_rays = tuple(torch.from_numpy(np.ascontiguousarray(np.concatenate([fr[i] for fr in
-                                                                                             frames_rays])))
+            lean = not cfg.get("secondaries")  # secondaries are spawned per rank: the root lacks their rays
+            root_rays = None
+            if lean:
+                root_rays = True
+                if rank == 0:  # the job's rays in global order (frame-major), resident on rank 0 (untimed setup)
+                    frs = [frame_rays(cfg, f)[:2] for f in range(world)]
+                    root_rays = tuple(torch.from_numpy(np.ascontiguousarray(np.concatenate([fr[i] for fr in frs])))
                                       .to(dev) for i in (0, 1))
-            lean_flags = [None] * world
-            dist.all_gather_object(lean_flags, root_rays is not None)
-            if not all(lean_flags):
-                root_rays = None
-            pg = multigpu.PeerFrameGather(W, H, world, rank, world, dev, root_rays=root_rays)
+            pg = multigpu.PeerFrameGather(W, H, world, rank, world, dev, root_rays=root_rays, index=idx)
             gather_mode = "p2p"
 
             def step():  # noqa: F811  (the N > 1 step: fused trace + frame assembly)
-                return pg.step(dm, go, gd, gs, stream)
+                return pg.step(dm, go, gd, gs, stream, schedule=schedule, sctp=sctp)
         except Exception as exc:  # no peer access / IPC: fall back to the NCCL gather
             log(f"[bench] p2p frame assembly unavailable ({exc!r}); using the NCCL gather")
             pg = None
@@ -418,10 +590,11 @@ def run_ours(args, cfg):
         from paper_2103_02309_b200.trace import TraceResult
 
         gather_mode = "nccl"
-        fg = multigpu.FrameGather(W, H, world, rank, world, args.gather_chunks, dev, mesh.cf_triangle, mesh.cf_tets)
-        views = [TraceResult(*(getattr(res, f)[a:b] for f in ("status", "cf", "triangle", "t", "tet", "tet_back",
-                                                                 "visited"))) for (a, b) in fg.my_pieces()]
+        fg = multigpu.FrameGather(W, H, world, rank, world, args.gather_chunks, dev, mesh.cf_triangle, mesh.cf_tets,
+                                  index=idx)
         pieces = fg.my_pieces()
+        views = [TraceResult(*(getattr(res, f)[a:b] for f in ("status", "cf", "triangle", "t", "tet", "tet_back",
+                                                                 "visited"))) for (a, b) in pieces]
 
         def step():  # noqa: F811  (the N > 1 step: trace + per-frame gather)
             for k, ((a, b), v) in enumerate(zip(pieces, views)):
@@ -430,20 +603,19 @@ def run_ours(args, cfg):
                 fg.send(k, v.status, v.cf, v.tet, v.visited, v.t)
             return fg.finish()
 
-    # warm-up
     for _ in range(args.warmup):
         flush.zero_()
         step()
     torch.cuda.synchronize()
-    if pg is not None:
-        # p2p: the hits live in rank 0's frame; rank 0 checks its own rays'
-        # slice below, and the visited statistics come from the whole frame
+    if pg is not None and rank == 0:
+        # p2p: this rank's hits live in the root's frame
         from paper_2103_02309_b200.trace import TraceResult as _TR
 
-        if rank == 0:
-            res = _TR(*(pg.frame[k][gidx] for k in ("status", "cf", "triangle", "t", "tet", "tet_back", "visited")))
+        gidx = torch.from_numpy(idx).to(dev)
+        res = _TR(*(pg.frame[k][gidx] for k in ("status", "cf", "triangle", "t", "tet", "tet_back", "visited")))
 
-    # parity at full size: the reference's own digest of this frame (rank 0, N=1)
+    # parity at full size: the reference's own digest of this frame (N=1,
+    # config 2 / config 1 sizes); otherwise a strided sample vs the reference
     parity = None
     dig_path = os.path.join(ROOT, "tests", "golden", "golden_digests.json")
     key = f"blob{cfg.get('grid')}/{cfg['scheme']}/cast"
@@ -457,32 +629,33 @@ def run_ours(args, cfg):
             def rm(x):
                 return x.cpu().numpy()[inv]
 
-            got = digest(rm(res.status), rm(res.cf), rm(res.tet), rm(res.visited))
-            ep = digest(rm(res.triangle), rm(res.t), rm(res.tet_back))
             parity = {"vs": "reference digest " + key,
-                      "traversal_bit_exact": got == digs[key],
-                      "epilogue_bit_exact": ep == digs[key.replace("/cast", "/epilogue")]}
+                      "traversal_bit_exact": digest(rm(res.status), rm(res.cf), rm(res.tet), rm(res.visited))
+                      == digs[key],
+                      "epilogue_bit_exact": digest(rm(res.triangle), rm(res.t), rm(res.tet_back))
+                      == digs[key.replace("/cast", "/epilogue")]}
+    got_all = None
     if parity is None and rank == 0 and not args.no_parity:
-        # no reference digest for this workload: check a strided sample of
-        # rays against the CPU oracle (the checker, never the measured path)
-        from oracle import pyoracle
+        got_all = [x.cpu().numpy() for x in (res.status, res.cf, res.tet, res.visited, res.triangle, res.t,
+                                             res.tet_back)]
+        parity = parity_vs_reference(mesh, o, d, st, got_all, max(1, n // args.parity_sample), threads,
+                                     cfg["layout"])
+        if sctp:
+            # the ScTP walk has no reference implementation: bit-exact vs its C
+            # restatement; vs the reference's 2-D walk only ties may differ
+            from oracle import pyoracle
 
-        stride = max(1, n // args.parity_sample)
-        sl = slice(0, n, stride)
-        exp = pyoracle.cast_rays_full(mesh, o[sl], d[sl], st[sl], layout=dm.layout, sctp=sctp)
-        got = [x.cpu().numpy()[sl] for x in (res.status, res.cf, res.tet, res.visited, res.triangle, res.t,
-                                              res.tet_back)]
-        mism = int(sum(np.count_nonzero(a != b) for a, b in zip(got, exp)))
-        parity = {"vs": f"C oracle (oracle/tetoracle.c) on every {stride}th ray", "rays_checked": int(len(exp[0])),
-                  "mismatched_values": mism, "bit_exact": mism == 0}
-    if pg is None:
-        visited = res.visited.cpu().numpy()
-    else:  # the whole job's visited counts on rank 0, none elsewhere
-        visited = pg.frame["visited"].cpu().numpy() if rank == 0 else np.zeros(0, np.int32)
+            sl = slice(0, n, max(1, n // args.parity_sample))
+            exp = pyoracle.cast_rays_full(mesh, o[sl], d[sl], st[sl], layout=dm.layout, sctp=True)
+            parity["sctp_vs_c_restatement_bit_exact"] = all(np.array_equal(g[sl], e) for g, e in zip(got_all, exp))
+            parity["note"] = "ScTP vs the reference's 2-D walk: mismatches are exact ties (SURVEY s8 a-14)"
+
+    # visited statistics over the rays actually traced (every rank's own)
+    visited_mine = res.visited.cpu().numpy() if (pg is None or rank == 0) else None
+    if pg is not None and rank != 0:
+        visited_mine = None  # lives in rank 0's frame; rank 0 reports the whole job's below
 
     # timed region: K steps between barrier + sync; per-step kernel events.
-    # nvidia-smi samples clocks from a short untimed ramp (so the sampler is
-    # up and the clocks have left idle) through the end of the timed region.
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     gather_check = None
     gather_error = None
@@ -517,23 +690,21 @@ def run_ours(args, cfg):
         time.sleep(0.05)
     kernel_ms = np.array([a.elapsed_time(b) for a, b in evs])
     if world > 1:
-        # N > 1: the gathered frame set of the last step, checked on rank 0
+        # N > 1: the assembled frame set of the last step, checked on rank 0
         try:
             full = step()
             torch.cuda.synchronize()
             if full is not None:
-                gather_check = int((full["visited"] > 0).sum().item())
-                dig_path = os.path.join(ROOT, "tests", "golden", "golden_digests.json")
-                key = f"blob{cfg.get('grid')}/{cfg['scheme']}/cast"
+                gather_check = {"rays_in_frame": int((full["visited"] > 0).sum().item())}
                 if os.path.exists(dig_path) and "grid" in cfg and (W, H) == (1920, 1080) \
                         and not cfg.get("secondaries") and cfg["layout"] != "tet80":
                     digs = json.load(open(dig_path))
                     if key in digs:  # frame 0 is the reference camera: compare with its digest
                         f0 = [full[k][:per_frame].cpu().numpy() for k in ("status", "cf", "tet", "visited")]
                         e0 = [full[k][:per_frame].cpu().numpy() for k in ("triangle", "t", "tet_back")]
-                        gather_check = {"rays": gather_check, "frame0_vs_reference_digest": digest(*f0) == digs[key],
-                                        "frame0_epilogue_vs_reference_digest":
-                                            digest(*e0) == digs[key.replace("/cast", "/epilogue")]}
+                        gather_check["frame0_vs_reference_digest"] = digest(*f0) == digs[key]
+                        gather_check["frame0_epilogue_vs_reference_digest"] = \
+                            digest(*e0) == digs[key.replace("/cast", "/epilogue")]
         except Exception as exc:  # report, do not lose the line
             gather_error = repr(exc)
     my_ms = float(kernel_ms.sum())
@@ -541,137 +712,86 @@ def run_ours(args, cfg):
         t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         max_ms = float(t.item())
-        vt = torch.tensor([int(visited.sum()), int(visited.max(initial=0)), len(visited)], dtype=torch.int64,
-                          device=dev)
-        vmax = vt.clone()
-        dist.all_reduce(vt, op=dist.ReduceOp.SUM)
-        dist.all_reduce(vmax, op=dist.ReduceOp.MAX)
-        vis_sum, vis_max, total_rays = int(vt[0]), int(vmax[1]), int(vt[2])
+        if pg is not None:  # every traced ray's visited count is in rank 0's frame
+            fv = pg.frame["visited"].cpu().numpy() if rank == 0 else np.zeros(0, np.int32)
+            vt = torch.tensor([int(fv.sum()), int(fv.max(initial=0)), n], dtype=torch.int64, device=dev)
+        else:
+            vt = torch.tensor([int(visited_mine.sum()), int(visited_mine.max(initial=0)), n], dtype=torch.int64,
+                              device=dev)
+        vsum = vt.clone()
+        dist.all_reduce(vsum, op=dist.ReduceOp.SUM)
+        dist.all_reduce(vt, op=dist.ReduceOp.MAX)
+        vis_sum, vis_max, total_rays = int(vsum[0]), int(vt[1]), int(vsum[2])
     else:
         max_ms = my_ms
-        vis_sum, vis_max, total_rays = int(visited.sum()), int(visited.max()), n
+        vis_sum, vis_max, total_rays = int(visited_mine.sum()), int(visited_mine.max()), n
 
     value = total_rays * args.steps / (max_ms / 1e3) / 1e6
     ms_per_step = max_ms / args.steps
 
-    # end to end through the C ABI with pinned host buffers
+    # end to end with pinned HOST buffers, per step
     e2e = None
     if not args.no_e2e:
         ho = torch.from_numpy(o).pin_memory()
         hd = torch.from_numpy(d).pin_memory()
         hs = torch.from_numpy(st).pin_memory()
-        outs = [torch.empty(n, dtype=dt).pin_memory() for dt in
-                (torch.uint8, torch.int32, torch.int32, torch.int32, torch.int32, torch.float64, torch.int32)]
+        if world == 1:
+            outs = [torch.empty(n, dtype=dt).pin_memory() for dt in
+                    (torch.uint8, torch.int32, torch.int32, torch.int32, torch.int32, torch.float64, torch.int32)]
+            host_fn = lib.tb_sctp_cast_rays_host if sctp else lib.tb_cast_rays_host
 
-        host_fn = lib.tb_sctp_cast_rays_host if sctp else lib.tb_cast_rays_host
+            def e2e_call():
+                check(host_fn(dm.handle, n, addr(ho), addr(hd), addr(hs), *[addr(x) for x in outs]),
+                      "tb_sctp_cast_rays_host" if sctp else "tb_cast_rays_host")
+            h2d, d2h = n * (12 + 12 + 4), n * (1 + 4 * 5 + 8)
+            path = (f"{'tb_sctp_cast_rays_host' if sctp else 'tb_cast_rays_host'} (C ABI) on pinned host buffers: "
+                    "zero-copy trace over PCIe")
+        else:
+            # each rank: its rays host -> HBM, the fused trace + frame assembly
+            # into rank 0, and rank 0 copies the assembled job back to the host
+            full0 = step()  # every rank (the step may hold collectives); rank 0 gets the frame set
+            fr_host = None
+            if rank == 0:
+                fr_host = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in full0.items()}
 
-        def host_call():
-            check(host_fn(dm.handle, n, addr(ho), addr(hd), addr(hs), *[addr(x) for x in outs]),
-                  "tb_sctp_cast_rays_host" if sctp else "tb_cast_rays_host")
-
+            def e2e_call():
+                go.copy_(ho, non_blocking=True)
+                gd.copy_(hd, non_blocking=True)
+                gs.copy_(hs, non_blocking=True)
+                full = step()
+                if rank == 0:
+                    for k2, v2 in full.items():
+                        fr_host[k2].copy_(v2, non_blocking=True)
+                torch.cuda.synchronize()
+            h2d = n * (12 + 12 + 4)
+            d2h = (total_rays * 29) if rank == 0 else 0
+            path = ("H2D of each rank's rays (pinned), fused trace + P2P frame assembly on rank 0, D2H of the "
+                    "assembled frame set (29 B/ray) from rank 0, synchronised; max over ranks")
         for _ in range(max(1, args.warmup)):
-            host_call()
+            e2e_call()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            host_call()
+            e2e_call()
         e_s = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([e_s], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_s = float(t.item())
-        e2e = {"value": total_rays * args.steps / e_s / 1e6, "unit": "Mrays/s",
-               "h2d_bytes_per_step": int(n * (12 + 12 + 4)), "d2h_bytes_per_step": int(n * (1 + 4 * 5 + 8)),
-               "ms_per_step": e_s / args.steps * 1e3,
-               "gpu_launches_per_step": 1 if os.environ.get("TETB200_E2E", "0") == "0" else -(-n // (1 << 18)),
-               "path": f"{'tb_sctp_cast_rays_host' if sctp else 'tb_cast_rays_host'} (C ABI) on pinned host "
-                       "buffers: zero-copy trace over PCIe (TETB200_E2E=1: 3-stream chunked H2D/trace/D2H)"}
+        e2e = {"value": total_rays * args.steps / e_s / 1e6, "unit": "Mrays/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_s / args.steps * 1e3, "path": path}
 
-    # incoherent secondaries of this frame (BASELINE's metric names primary
-    # AND incoherent secondary rays): diffuse bounces from this rank's
-    # primary hits (render.py:353-359 semantics, seed 4), traced on the
-    # device under each schedule, same timing protocol; checked on
-    # a strided sample against the oracle.
-    secondary = None
-    if not args.no_secondary and not cfg.get("secondaries") and not sctp and world == 1:
-        from paper_2103_02309_b200.scenes import diffuse_secondaries
-        from paper_2103_02309_b200.trace import TraceResult as _TR
-
-        so, sd, sst = diffuse_secondaries(o, d, res.t.cpu().numpy(), res.triangle.cpu().numpy(),
-                                          res.tet.cpu().numpy(), mesh.triangle_coords(), seed=4)
-        ns = len(sst)
-        if ns:
-            g2 = [torch.from_numpy(a).to(dev) for a in (so, sd, sst)]
-            r2 = empty_result(ns, dev)
-            sec = {}
-            for sched2 in ("compact", "lane", "binned"):
-                for _ in range(args.warmup):
-                    flush.zero_()
-                    trace(dm, *g2, out=r2, stream=stream, schedule=sched2)
-                ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                       for _ in range(args.steps)]
-                torch.cuda.synchronize()
-                for a, b in ev2:
-                    flush.zero_()
-                    a.record(stream)
-                    trace(dm, *g2, out=r2, stream=stream, schedule=sched2)
-                    b.record(stream)
-                torch.cuda.synchronize()
-                sec[sched2] = float(np.mean([a.elapsed_time(b) for a, b in ev2]))
-            v2 = r2.visited.cpu().numpy()
-            par2 = None
-            if not args.no_parity:
-                from oracle import pyoracle
-
-                stride = max(1, ns // args.parity_sample)
-                sl2 = slice(0, ns, stride)
-                exp2 = pyoracle.cast_rays_full(mesh, so[sl2], sd[sl2], sst[sl2], layout=dm.layout)
-                got2 = [x.cpu().numpy()[sl2] for x in (r2.status, r2.cf, r2.tet, r2.visited, r2.triangle, r2.t,
-                                                        r2.tet_back)]
-                mism2 = int(sum(np.count_nonzero(a != b) for a, b in zip(got2, exp2)))
-                par2 = {"vs": f"C oracle on every {stride}th ray", "rays_checked": int(len(exp2[0])),
-                        "bit_exact": mism2 == 0}
-            secondary = {"value": ns / sec["binned"] / 1e3, "unit": "Mrays/s", "rays": ns,
-                         "kernel_ms": sec["binned"], "schedule": "binned",
-                         "note": "direction-cell counting sort (96 cube-map cells) + the walk in binned order, "
-                                 "both inside the events",
-                         "one_ray_per_lane": {"value": ns / sec["lane"] / 1e3, "kernel_ms": sec["lane"]},
-                         "block_compaction": {"value": ns / sec["compact"] / 1e3, "kernel_ms": sec["compact"]},
-                         "tets_visited_per_ray": {"mean": float(v2.mean()), "max": int(v2.max())},
-                         "rays_from": "diffuse hemisphere bounces of this frame's primary hits (seed 4)",
-                         "parity": par2}
-
-    # render-style end to end: camera rays generated in HBM (no ray upload),
-    # trace, all 7 hit arrays copied back to pinned host memory, per step
-    e2e_render = None
-    if not args.no_e2e and world == 1 and not cfg.get("secondaries"):
-        from paper_2103_02309_b200.scenes import BLOB_CAMERA, kuhn_camera
-        from paper_2103_02309_b200.trace import trace_camera
-
-        from paper_2103_02309_b200.trace import TraceResult
-
-        cam = kuhn_camera(cfg["kuhn"]) if "kuhn" in cfg else BLOB_CAMERA
-        # hits land in pinned host memory, written by the trace kernel itself
-        hres = TraceResult(*[torch.empty(W * H, dtype=dt).pin_memory() for dt in
-                             (torch.uint8, torch.int32, torch.int32, torch.float64, torch.int32, torch.int32,
-                              torch.int32)])
-        _, cam_tet = trace_camera(dm, cam, W, H, out=hres, stream=stream, sctp=sctp)  # camera located once
-
-        def render_call():
-            trace_camera(dm, cam, W, H, out=hres, stream=stream, cam_tet=cam_tet, sctp=sctp)
-            torch.cuda.synchronize()
-
-        for _ in range(max(1, args.warmup)):
-            render_call()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            render_call()
-        r_s = time.perf_counter() - t0
-        e2e_render = {"value": W * H * args.steps / r_s / 1e6, "unit": "Mrays/s", "h2d_bytes_per_step": 14 * 8,
-                      "d2h_bytes_per_step": int(W * H * 29), "ms_per_step": r_s / args.steps * 1e3,
-                      "path": "trace_camera: rays generated in HBM, trace writes all 7 hit arrays straight to "
-                              "pinned host memory (camera tet located once)"}
+    extra = {}
+    if world == 1 and not cfg.get("secondaries") and not sctp:
+        if not args.no_secondary:
+            extra["secondary"] = frame_secondaries(args, cfg, mesh, dm, o, d, res, stream, flush, threads)
+        if not args.no_cfg4 and args.config == 2:
+            extra["secondary_cfg4"] = config4_secondaries(args, mesh, stream, flush, threads, clocks)
+        if not args.no_e2e:
+            extra["e2e_render"] = render_e2e(args, cfg, dm, stream, sctp)
+        if not args.no_small_batch:
+            extra["small_batch"] = small_batch(args, mesh, o, d, st, threads)
 
     if rank != 0:
         if pg is not None:
@@ -681,111 +801,261 @@ def run_ours(args, cfg):
         return
 
     peak, peak_src = measured_peak()
-    alg = algorithmic_bytes(visited, cfg["layout"])
+    alg = algorithmic_bytes(visited_mine, cfg["layout"])  # this rank's launch
     kern_s = float(kernel_ms.mean()) / 1e3
-    achieved = alg / kern_s / 1e9
-    # Issue roofline of the walk (the kernel is instruction-issue / ALU-pipe
-    # bound, ncu r01): peak ray-steps/s if every scheduler issued one
-    # full-warp step instruction per cycle = SMs x 4 x clock x 32 lanes /
-    # SASS instructions per step (tools/sass_steps.py, committed per build).
-    roofline_issue = None
-    sp = os.path.join(ROOT, "profiles", "sass_step_counts.json")
-    clk_mhz = clocks.summary(clocks.t_ramp, clocks.t_end).get("sm_mhz")
-    if os.path.exists(sp) and clk_mhz and not sctp:
-        counts = json.load(open(sp))
-        kname = ("cast_compact_kernel" if schedule in ("compact", "compact512") else "cast_kernel")
-        entry = counts.get(f"{kname}<{cfg['layout'][3:]}, validated>") or counts.get(f"{kname}<{cfg['layout'][3:]}, clamp>")
-        if entry:
-            per_step = (entry.get("unrolled_x4_per_step") or entry["single_step"])["total"]
-            sms = torch.cuda.get_device_properties(dev).multi_processor_count
-            peak_steps = sms * 4 * clk_mhz * 1e6 * 32 / per_step
-            steps = (vis_sum - total_rays) / world  # walk steps of one rank's launch
-            ach_steps = steps / kern_s
-            roofline_issue = {"bound": "issue", "achieved": ach_steps / 1e9, "peak": peak_steps / 1e9,
-                              "unit": "G ray-steps/s", "frac": ach_steps / peak_steps,
-                              "sass_per_step": per_step, "sms": sms, "sm_mhz": clk_mhz,
-                              "note": "peak = SMs x 4 schedulers x clock x 32 lanes / SASS per walk step; "
-                                      "the gap is init/epilogue, SIMT divergence, latency and the tail"}
-    roofline_l2 = None
-    if not sctp and cfg["layout"] != "tet80" and not args.no_l2_probe:
-        roofline_l2 = l2_gather_roof(dm, stream, flush, cfg["layout"], (vis_sum - total_rays) / world, achieved)
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(f"cfg{args.config}/{cfg['layout']}")
+    clk = clocks.summary(clocks.t_ramp, clocks.t_end)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    walk_steps = (vis_sum - total_rays) / world  # one rank's launch
+    roof = issue_roof(cfg["layout"], schedule, walk_steps, kern_s, clk.get("sm_mhz"), sms) if not sctp else None
+    traffic = traffic_of(f"cfg{args.config}/{cfg['layout']}")
+    kname = (f"sctp_kernel<{cfg['layout'][3:]}>" if sctp else
+             f"{'cast_compact_kernel' if schedule in ('compact', 'compact512') else 'cast_kernel'}"
+             f"<{cfg['layout'][3:]}>" + (" after bin_count/bin_seg_scan/bin_scatter (direction binning, inside "
+                                          "the events)" if schedule == "binned" else ""))
+    hbm = {"bound": "hbm", "achieved": alg / kern_s / 1e9, "peak": peak, "unit": "GB/s", "peak_source": peak_src,
+           "algorithmic_bytes_per_launch": alg,
+           "frac": alg / kern_s / 1e9 / peak,
+           "dram_bytes_per_launch": traffic,
+           "dram_frac": (traffic / kern_s / 1e9 / peak) if traffic else None,
+           "note": "SURVEY s8(d) algorithmic gather bytes over the HBM copy peak: the walk's gathers are served "
+                   "by L1/L2 (DRAM sees a few % of them, dram_bytes_per_launch from ncu), so this can exceed 1 "
+                   "and is not the binding roof"}
+    if roof is None:
+        roof = dict(hbm)
+    roof = dict(roof, traffic=traffic, kernel=kname)
     line = {
         "metric": "Mrays/s", "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "rays_per_gpu": n, "layout": cfg["layout"], "scheme": cfg["scheme"],
-                   "parallelism": f"tile-shard x{world}, mesh replicated", "l2": "flushed between steps (256 MiB)",
-                   "schedule": schedule,
-                   "frames": world},
+        "config": config_dict(cfg, world),
+        "schedule": schedule, "rays_per_step": total_rays,
         "tets_visited_per_ray": {"mean": vis_sum / total_rays, "max": vis_max},
         "kernel_ms": {"mean": float(kernel_ms.mean()), "min": float(kernel_ms.min()), "max": float(kernel_ms.max())},
-        "gather_ms": None,
-        "gather": None if world == 1 else (
-            {"rays_gathered_to_rank0": gather_check, "rays_expected": per_frame * world, "error": gather_error,
-             "mode": "p2p",
-             "per_step": "every step assembles its frame set on rank 0 inside the timed region: each rank's trace "
+        "gather": None if world == 1 else {
+            "mode": gather_mode, "check": gather_check, "error": gather_error,
+            "per_step": ("every step assembles its frame set on rank 0 inside the timed region: each rank's trace "
                          "epilogue stores every finished ray into rank 0's full-frame arrays (CUDA IPC, P2P over "
-                         "NVLink), then stream sync + barrier",
-             "bytes_to_rank0_per_step": int((13 if pg.lean else 29) * per_frame * (world - 1)),
-             "lean": bool(pg.lean), "collective": "none (barrier only)"}
-            if gather_mode == "p2p" else
-            {"rays_gathered_to_rank0": gather_check, "rays_expected": per_frame * world, "error": gather_error,
-             "mode": "nccl",
-             "per_step": "every step gathers its frame set to rank 0 inside the timed region (chunked, overlapped "
-                         "with the trace)",
-             "bytes_to_rank0_per_step": int(20 * per_frame * (world - 1)), "chunks": args.gather_chunks,
-             "collective": "torch.distributed.gather (NCCL, async), 20 B records"}),
+                         "NVLink), then stream sync + barrier" if gather_mode == "p2p" else
+                         "every step gathers its frame set to rank 0 inside the timed region (chunked NCCL "
+                         "gather, overlapped with the trace)"),
+            "bytes_to_rank0_per_step": int((13 if (pg is not None and pg.lean) else (29 if pg is not None else 20))
+                                           * (total_rays - n)),
+            "lean": bool(pg is not None and pg.lean)},
         "wall_ms_per_step": wall / args.steps * 1e3,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": alg,
-                     "kernel": (f"sctp_kernel<{cfg['layout'][3:]}>" if sctp else
-                                f"{'cast_compact_kernel' if schedule in ('compact', 'compact512') else 'cast_kernel'}"
-                                f"<{cfg['layout'][3:]}>"
-                                + (" after bin_count/bin_seg_scan/bin_scatter (direction binning, inside the events)"
-                                   if schedule == "binned" else "")),
-                     "note": "algorithmic gather bytes (SURVEY s8d) over the HBM copy peak; the walk's "
-                             "gathers are served by L1/L2 (ncu: DRAM traffic is a few % of them), so frac "
-                             "can exceed 1 -- the binding roofline is roofline_issue"},
-        "roofline_issue": roofline_issue,
-        "roofline_l2": roofline_l2,
-        "clocks": dict(clocks.summary(clocks.t_ramp, clocks.t_end), window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
+        "roofline": roof,
+        "roofline_hbm": hbm,
+        "roofline_l2": (l2_gather_roof(dm, stream, flush, cfg["layout"], walk_steps, alg / kern_s / 1e9)
+                        if (not sctp and cfg["layout"] != "tet80" and not args.no_l2_probe) else None),
+        "clocks": dict(clk, window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
         "gpu_launches": args.steps * ((1 if fg is None else sum(1 for a, b in fg.my_pieces() if b > a))
                                       * (4 if schedule == "binned" else 1)  # binned: count, scan, scatter, walk
+                                      + (1 if (pg is not None and schedule == "binned") else 0)  # compose
                                       + (1 if pg is not None and pg.lean else 0)),  # lean p2p: root epilogue
         "parity": parity,
         "e2e": e2e,
-        "e2e_render": e2e_render,
-        "secondary": secondary,
+        "mesh_bytes": {"hbm_total": int(dm.hbm_bytes), "hot": int(dm.hot_bytes),
+                       "reference_accelerator_bytes": int(mesh.records_u32().nbytes + mesh.points.nbytes)},
+        **extra,
     }
     if not args.no_cpu_baseline and world == 1:
-        from concurrent.futures import ThreadPoolExecutor  # noqa: F401
-
-        threads = os.cpu_count() or 1
         m = min(n, args.cpu_sample)
         t0 = time.perf_counter()
-        reps = 0
-        best = None
+        reps, best = 0, None
         while reps < 3 and (time.perf_counter() - t0) < 20.0:
             s0 = time.perf_counter()
-            kind, _ = cpu_reference_trace(mesh, o[:m], d[:m], st[:m], threads)
+            ref_trace(mesh_for_ref(mesh, cfg), o[:m], d[:m], st[:m], threads)
             dt = time.perf_counter() - s0
             best = dt if best is None else min(best, dt)
             reps += 1
-        m1 = min(m, 131072)
-        line["cpu_baseline"] = {"value": m / best / 1e6, "unit": "Mrays/s", "cores": threads, "kind": kind,
-                                "sample": f"first {m} rays of the frame, best of {reps}: compiled reference "
-                                          "kernels + batch epilogue on a thread pool",
-                                "single_thread": cpu_single_thread(mesh, o[:m1], d[:m1], st[:m1])}
+        line["cpu_baseline"] = {"value": m / best / 1e6, "unit": "Mrays/s", "cores": threads, "kind": "reference",
+                                "sample": f"first {m} rays of the frame, best of {reps}: the reference's "
+                                          "tetray.batch.cast_rays (compiled kernels + batch epilogue, oracle/_ref) "
+                                          "on a thread pool"
+                                          + (" on the Tet32 mesh, 2-D walk (no TetMesh-80 / ScTP in the reference)"
+                                             if cfg["layout"] == "tet80" else "")}
     print(json.dumps(line), flush=True)
     if pg is not None:
         pg.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def mesh_for_ref(mesh, cfg):
+    ref_package()
+    if cfg["layout"] == "tet80":
+        from paper_2103_02309_b200.tetmesh import relayout
+
+        return relayout(mesh, "tet32")
+    return mesh
+
+
+def frame_secondaries(args, cfg, mesh, dm, o, d, res, stream, flush, threads):
+    """The frame's own diffuse bounces (render.py:353-359 semantics, seed 4),
+    binned and one ray per lane, parity-sampled against the reference."""
+    import torch
+
+    from paper_2103_02309_b200.trace import empty_result, trace
+    from paper_2103_02309_b200.workload import diffuse_secondaries
+
+    dev = flush.device
+    so, sd, sst = diffuse_secondaries(o, d, res.t.cpu().numpy(), res.triangle.cpu().numpy(), res.tet.cpu().numpy(),
+                                      mesh.triangle_coords(), seed=4)
+    ns = len(sst)
+    if not ns:
+        return None
+    g2 = [torch.from_numpy(a).to(dev) for a in (so, sd, sst)]
+    r2 = empty_result(ns, dev)
+    ms = {}
+    for sched in ("lane", "binned"):
+        ms[sched] = float(timed(lambda: trace(dm, *g2, out=r2, stream=stream, schedule=sched), args.steps,
+                                args.warmup, stream, flush).mean())
+    v2 = r2.visited.cpu().numpy()
+    par = None
+    if not args.no_parity:
+        got = [x.cpu().numpy() for x in (r2.status, r2.cf, r2.tet, r2.visited, r2.triangle, r2.t, r2.tet_back)]
+        par = parity_vs_reference(mesh, so, sd, sst, got, max(1, ns // args.parity_sample), threads, cfg["layout"])
+    return {"value": ns / ms["binned"] / 1e3, "unit": "Mrays/s", "rays": ns, "kernel_ms": ms["binned"],
+            "schedule": "binned", "one_ray_per_lane": {"value": ns / ms["lane"] / 1e3, "kernel_ms": ms["lane"]},
+            "tets_visited_per_ray": {"mean": float(v2.mean()), "max": int(v2.max())},
+            "rays_from": "diffuse hemisphere bounces of this frame's primary hits (seed 4)", "parity": par}
+
+
+def config4_secondaries(args, mesh20, stream, flush, threads, clocks):
+    """BASELINE config 4 inside the default run: 4096x4096 primaries on the
+    Tet16 encoding of the same scene (untimed), their 16.7 M diffuse
+    secondaries (render.py:353-359 semantics, seed 4) traced binned and one
+    ray per lane (timed), parity on a strided sample vs the reference."""
+    import torch
+
+    from paper_2103_02309_b200.device import DeviceMesh
+    from paper_2103_02309_b200.tetmesh import relayout
+    from paper_2103_02309_b200.trace import empty_result, locate, trace
+    from paper_2103_02309_b200.workload import diffuse_secondaries
+
+    cfg = CONFIGS[4]
+    dev = flush.device
+    mesh = relayout(mesh20, cfg["layout"])
+    dm = DeviceMesh(mesh, dev.index)
+    o, d, pos = frame_rays(cfg, 0)
+    cam, _ = locate(dm, torch.tensor(pos[None], dtype=torch.float64, device=dev),
+                    torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))
+    st = np.full(len(o), int(cam.item()), np.int32)
+    prim = trace(dm, torch.from_numpy(o).to(dev), torch.from_numpy(d).to(dev), torch.from_numpy(st).to(dev))
+    so, sd, sst = diffuse_secondaries(o, d, prim.t.cpu().numpy(), prim.triangle.cpu().numpy(), prim.tet.cpu().numpy(),
+                                      mesh.triangle_coords(), seed=4)
+    del prim
+    ns = len(sst)
+    g2 = [torch.from_numpy(a).to(dev) for a in (so, sd, sst)]
+    r2 = empty_result(ns, dev)
+    ms = {}
+    for sched in ("lane", "binned"):
+        ms[sched] = timed(lambda: trace(dm, *g2, out=r2, stream=stream, schedule=sched), args.steps, args.warmup,
+                          stream, flush)
+    v2 = r2.visited.cpu().numpy()
+    par = None
+    if not args.no_parity:
+        got = [x.cpu().numpy() for x in (r2.status, r2.cf, r2.tet, r2.visited, r2.triangle, r2.t, r2.tet_back)]
+        par = parity_vs_reference(mesh, so, sd, sst, got, max(1, ns // args.parity_sample), threads, "tet16")
+    kb = float(ms["binned"].mean())
+    clk = clocks.summary(clocks.t_ramp, clocks.t_end).get("sm_mhz")
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    roof = issue_roof("tet16", "binned", float(v2.astype(np.int64).sum() - ns), kb / 1e3, clk, sms)
+    out = {"value": ns / kb / 1e3, "unit": "Mrays/s", "rays": ns, "kernel_ms": kb, "schedule": "binned",
+           "one_ray_per_lane": {"value": ns / float(ms["lane"].mean()) / 1e3, "kernel_ms": float(ms["lane"].mean())},
+           "tets_visited_per_ray": {"mean": float(v2.mean()), "max": int(v2.max())},
+           "roofline_issue": roof, "traffic": traffic_of("cfg4/tet16"),
+           "algorithmic_bytes_per_launch": algorithmic_bytes(v2, "tet16"),
+           "rays_from": "diffuse hemisphere bounces of the 4096x4096 blob-camera frame's primary hits (seed 4), "
+                        "Tet16 Hilbert mesh of the same scene",
+           "parity": par}
+    dm.close()
+    return out
+
+
+def render_e2e(args, cfg, dm, stream, sctp):
+    """Render-style end to end: camera rays generated in HBM, hits written by
+    the trace straight to pinned host memory, per step."""
+    import torch
+
+    from paper_2103_02309_b200.trace import TraceResult, trace_camera
+
+    W, H = cfg["width"], cfg["height"]
+    cam = camera_of(cfg, 0)
+    hres = TraceResult(*[torch.empty(W * H, dtype=dt).pin_memory() for dt in
+                         (torch.uint8, torch.int32, torch.int32, torch.float64, torch.int32, torch.int32, torch.int32)])
+    _, cam_tet = trace_camera(dm, cam, W, H, out=hres, stream=stream, sctp=sctp)  # camera located once
+
+    def call():
+        trace_camera(dm, cam, W, H, out=hres, stream=stream, cam_tet=cam_tet, sctp=sctp)
+        torch.cuda.synchronize()
+
+    for _ in range(max(1, args.warmup)):
+        call()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        call()
+    r_s = time.perf_counter() - t0
+    return {"value": W * H * args.steps / r_s / 1e6, "unit": "Mrays/s", "h2d_bytes_per_step": 14 * 8,
+            "d2h_bytes_per_step": int(W * H * 29), "ms_per_step": r_s / args.steps * 1e3,
+            "path": "trace_camera: rays generated in HBM, trace writes all 7 hit arrays straight to pinned host "
+                    "memory (camera tet located once)"}
+
+
+def small_batch(args, mesh, o, d, st, threads):
+    """Renderer granularity (render.py:192-207,300-331,538-541: one
+    batch.cast_rays per 16x16 tile from a thread pool): the reference's
+    batch.cast_rays with kernels= the CUDA module vs its own compiled
+    kernels, at 256 / 4096 / 65536 rays per call from all host threads over
+    the frame's first 2^20 rays."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import paper_2103_02309_b200.kernels as cuda
+
+    ref_package()
+    from tetray import backend, batch
+
+    K = backend.get_kernels("compiled")
+    total = min(len(st), 1 << 20)
+    out = {}
+    for size in (256, 4096, 65536):
+        starts = list(range(0, total, size))
+
+        def run(kern):
+            def one(a):
+                batch.cast_rays(mesh, o[a:a + size], d[a:a + size], st[a:a + size], kernels=kern)
+            with ThreadPoolExecutor(max_workers=threads) as pool:
+                list(pool.map(one, starts))
+
+        row = {}
+        for name, kern in (("cuda", cuda), ("reference", K)):
+            run(kern)  # warm (uploads, thread contexts)
+            t0 = time.perf_counter()
+            reps = 0
+            while reps < 2 or time.perf_counter() - t0 < 0.5:
+                run(kern)
+                reps += 1
+            row[name] = total * reps / (time.perf_counter() - t0) / 1e6
+        row["speedup"] = row["cuda"] / row["reference"]
+        out[str(size)] = row
+    cross = next((int(s) for s, r in out.items() if r["speedup"] >= 1.0), None)
+    return {"unit": "Mrays/s", "threads": threads, "rays": total, "per_call": out,
+            "crossover_rays_per_call": cross,
+            "path": "tetray.batch.cast_rays(kernels=paper_2103_02309_b200.kernels) vs kernels=its compiled "
+                    "_kernels, host numpy buffers, one call per chunk from a thread pool"}
+
+
+def relaunch(args):
+    """--gpus N outside torchrun: one rank per GPU via torch.distributed.run."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"[bench] --gpus {args.gpus}: relaunching under torch.distributed.run")
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -797,31 +1067,46 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--layout", default=None)
     ap.add_argument("--scheme", default=None)
-    ap.add_argument("--no-secondary", action="store_true", help="skip the secondary-ray measurement")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the frame's own secondary rays")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 secondaries in the default run")
+    ap.add_argument("--no-small-batch", action="store_true", help="skip the renderer-granularity measurement")
     ap.add_argument("--gather", choices=("p2p", "nccl"), default="p2p",
                     help="N > 1 frame assembly: fused P2P stores (default) or the chunked NCCL gather")
-    ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1: trace/gather pipeline depth per step")
+    ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1 NCCL gather: trace/gather pipeline depth")
     ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512", "binned"),
-                    help="ray-to-lane schedule of the timed trace (default: compact for secondaries, else lane)")
+                    help="ray-to-lane schedule of the timed trace (default: binned for secondaries, else lane)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-l2-probe", action="store_true", help="skip the L2 gather-roof probe (roofline_l2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=2_073_600)
+    ap.add_argument("--ref-sample", type=int, default=2_097_152, help="reference arm: rays per step (config 4)")
     ap.add_argument("--ramp-s", type=float, default=0.5, help="untimed load before the timed region (clock ramp)")
     ap.add_argument("--no-parity", action="store_true")
-    ap.add_argument("--parity-sample", type=int, default=262_144, help="rays checked against the oracle")
+    ap.add_argument("--parity-sample", type=int, default=65_536, help="rays checked against the reference")
+    ap.add_argument("--dump-scene", type=int, default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--out", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.dump_scene is not None:
+        dump_scene(args.dump_scene, args.layout, args.scheme, args.out)
+        return
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     cfg = dict(CONFIGS[args.config])
     if args.layout:
         cfg["layout"] = args.layout
     if args.scheme:
         cfg["scheme"] = args.scheme
+    world = int(os.environ.get("WORLD_SIZE", "0"))
     if args.impl == "reference":
         run_reference_arm(args, cfg)
-    else:
-        run_ours(args, cfg)
+        return
+    if world == 0 and args.gpus > 1:
+        relaunch(args)
+    if world and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    run_ours(args, cfg)
 
 
 if __name__ == "__main__":

@@ -180,6 +180,21 @@ int tb_cast_rays_scatter(tb_mesh* mesh, int64_t n, const float* o, const float* 
                          const int32_t* start, const int64_t* out_index, uint8_t* status,
                          int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t,
                          int32_t* tet_back, void* stream);
+/* tb_cast_rays_scatter with an explicit schedule: 1 one ray per lane, 6 the
+ * direction-binned walk (its permutation composed with out_index, so rays
+ * are walked in binned order and still land at out_index[r]); 0 = the
+ * process-wide setting; 2-4 (refill / compaction) have no scatter variant
+ * and run one ray per lane.  Same results in every mode. */
+int tb_cast_rays_scatter_sched(tb_mesh* mesh, int64_t n, const float* o, const float* d,
+                               const int32_t* start, const int64_t* out_index, uint8_t* status,
+                               int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t,
+                               int32_t* tet_back, int schedule, void* stream);
+/* The ScTP fallback walk (tb_sctp_cast_rays) with scattered outputs, as
+ * tb_cast_rays_scatter: the multi-GPU frame assembly of a ScTP job. */
+int tb_sctp_cast_rays_scatter(tb_mesh* mesh, int64_t n, const float* o, const float* d,
+                              const int32_t* start, const int64_t* out_index, uint8_t* status,
+                              int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t,
+                              int32_t* tet_back, void* stream);
 
 /* CUDA IPC of device allocations between the ranks of one node: the
  * 64-byte handle of the allocation holding dev_ptr (which must be the start

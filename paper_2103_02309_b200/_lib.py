@@ -45,6 +45,8 @@ _SIGS = {
     "tb_cast_rays": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),
     "tb_cast_rays_sched": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_int, c_void_p]),
     "tb_cast_rays_scatter": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, P, c_void_p]),
+    "tb_cast_rays_scatter_sched": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, P, c_int, c_void_p]),
+    "tb_sctp_cast_rays_scatter": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, P, c_void_p]),
     "tb_device_alloc": (c_int, [c_size_t, c_int, POINTER(c_void_p)]),
     "tb_device_free": (c_int, [P]),
     "tb_ipc_get_handle": (c_int, [P, P]),

@@ -197,6 +197,14 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint8_t*
   }
 }
 
+// Scatter target of a binned walk whose results go to a caller's index
+// (multi-GPU frame assembly): widx[r] = oidx[perm[r]].
+__global__ void compose_index_kernel(const int64_t* __restrict__ perm, const int64_t* __restrict__ oidx, int64_t n,
+                                     int64_t* __restrict__ widx) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) widx[r] = __ldg(oidx + __ldg(perm + r));
+}
+
 // Sorting segments (r01, bench.py device values): binning sorts within
 // segments of 262144 consecutive rays rather than over the whole batch.  A
 // global permutation scatters every ray's gathered reads and result stores

@@ -71,7 +71,7 @@ struct tb_mesh {
     MeshView v;
     v.pts = pts; v.rec4 = rec4; v.vx = vx; v.sv = sv; v.sn = sn;
     v.cf_tri = cf_tri; v.cf_tets = cf_tets; v.tri = tri; v.orient = orient;
-    v.n_points = n_points; v.n_tets = n_tets;
+    v.n_points = n_points; v.n_tets = n_tets; v.n_cf = n_cf; v.n_tri = n_tri;
     return v;
   }
 };
@@ -143,10 +143,13 @@ __global__ void orient_kernel(const int4* __restrict__ sv, const float4* __restr
 // sn[u][k] == t for u's vertex k off that face).  A mesh passing all three
 // runs the kernels without the per-step index clamp; any violation (e.g. a
 // record mutated by a test) keeps the clamp, so a corrupt mesh still cannot
-// read out of bounds.  Sets *bad on any violation.
+// read out of bounds.  (4) extends the proof across constrained faces, which
+// the locate / shadow walks cross through cf_tets and the epilogue gathers
+// through cf_tri.  Sets *bad on any violation.
 __global__ void validate_kernel(int layout, const int4* __restrict__ sv, const uint4* __restrict__ sn,
                                 const uint4* __restrict__ rec4, const uint32_t* __restrict__ vx, int64_t n_tets,
-                                int64_t n_points, unsigned int* __restrict__ bad) {
+                                int64_t n_points, const int32_t* __restrict__ cf_tri, const int2* __restrict__ cf_tets,
+                                int64_t n_cf, int64_t n_tri, unsigned int* __restrict__ bad) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n_tets) return;
   const int4 v = sv[t];
@@ -167,9 +170,26 @@ __global__ void validate_kernel(int layout, const int4* __restrict__ sv, const u
   const int vv[4] = {v.x, v.y, v.z, v.w};
   const uint32_t nn[4] = {nb.x, nb.y, nb.z, nb.w};
   for (int j = 0; j < 4 && ok; ++j) {
-    const uint32_t u = nn[j];
-    if (u >= (uint64_t)n_tets) continue;  // boundary / constrained: the walk stops there
+    uint32_t u = nn[j];
+    if ((u & kConstrained) != 0u) {
+      // (4) a constrained ref names a row of the cf tables that lists t as one
+      // side, a scene triangle in range, and, on the other side, -1 (hull) or
+      // a tet sharing the face whose slot holds the same tagged ref -- the
+      // epilogue, locate and shadow walks gather through exactly these
+      const uint32_t cfi = u & kPayload;
+      if (cfi >= (uint64_t)n_cf) { ok = false; break; }
+      const int2 ct = cf_tets[cfi];
+      const int32_t tri = cf_tri[cfi];
+      if ((ct.x != (int32_t)t && ct.y != (int32_t)t) || tri < 0 || (int64_t)tri >= n_tri) { ok = false; break; }
+      const int32_t other = (ct.x == (int32_t)t) ? ct.y : ct.x;
+      if (other < 0) continue;  // hull
+      if ((int64_t)other >= n_tets || (int64_t)other == t) { ok = false; break; }
+      u = (uint32_t)other;  // then the face-sharing check below, expecting the tagged ref back
+    } else if (u >= (uint64_t)n_tets) {
+      continue;  // boundary (or a corrupt plain ref): the walk stops there
+    }
     if ((int64_t)u == t) { ok = false; break; }
+    const uint32_t back = (nn[j] & kConstrained) ? nn[j] : (uint32_t)t;
     const int4 w = sv[u];
     const int ww[4] = {w.x, w.y, w.z, w.w};
     const uint4 un = sn[u];
@@ -180,7 +200,7 @@ __global__ void validate_kernel(int layout, const int4* __restrict__ sv, const u
       for (int i = 0; i < 4; ++i) in_face = in_face || (i != j && vv[i] == ww[k]);
       if (in_face) ++shared; else off = k;
     }
-    ok = shared == 3 && off >= 0 && unn[off] == (uint32_t)t;
+    ok = shared == 3 && off >= 0 && unn[off] == back;
   }
   if (!ok) atomicOr(bad, 1u);
 }
@@ -265,9 +285,12 @@ __device__ __forceinline__ void write_result(const MeshView& m, int64_t r, uint8
   if (triangle != nullptr || t != nullptr || tet_back != nullptr) {
     int32_t tri = -1, back = -1;
     double tt = INFINITY;
-    if (cfi >= 0) {
+    // A corrupt (unvalidated) mesh can carry a constrained ref past the cf
+    // table: no gather then -- the host wrappers raise IndexError on cf >=
+    // n_cf, as the reference's batch epilogue does (batch.py:63).
+    if (cfi >= 0 && cfi < m.n_cf) {
       tri = __ldg(&m.cf_tri[cfi]);
-      if (t != nullptr)
+      if (t != nullptr && (uint32_t)tri < (uint64_t)m.n_tri)
         tt = mt_t((double)o0, (double)o1, (double)o2, (double)d0, (double)d1, (double)d2,
                   m.tri + 9 * (int64_t)tri);
       const int2 ct = __ldg(&m.cf_tets[cfi]);
@@ -291,9 +314,9 @@ __global__ void __launch_bounds__(256) epilogue_kernel(MeshView m, int64_t n, co
   const int32_t cfi = __ldg(cf + r);
   int32_t tri = -1, back = -1;
   double tt = INFINITY;
-  if (cfi >= 0) {
+  if (cfi >= 0 && cfi < m.n_cf) {
     tri = __ldg(&m.cf_tri[cfi]);
-    if (t != nullptr)
+    if (t != nullptr && (uint32_t)tri < (uint64_t)m.n_tri)
       tt = mt_t((double)__ldg(o + 3 * r), (double)__ldg(o + 3 * r + 1), (double)__ldg(o + 3 * r + 2),
                 (double)__ldg(d + 3 * r), (double)__ldg(d + 3 * r + 1), (double)__ldg(d + 3 * r + 2),
                 m.tri + 9 * (int64_t)tri);
@@ -365,9 +388,10 @@ constexpr int kUnroll = 4;
 // r -- the multi-GPU frame assembly, where the outputs are the root GPU's
 // full-frame arrays mapped into this process (CUDA IPC over NVLink) and each
 // ray's result is stored there by the epilogue the moment its walk ends.
-// kGather (with kScatter): ray r is read from index oidx[r] as well -- the
-// direction-binned schedule walks the rays in binned order straight from the
-// caller's arrays, so the binning pass writes only the 8-byte permutation.
+// kGather: ray r is read from index ridx[r] -- the direction-binned schedule
+// walks the rays in binned order straight from the caller's arrays, so the
+// binning pass writes only the 8-byte permutation; with kScatter its results
+// go back to oidx[r] (oidx == ridx: the ray's own slot).
 template <int L, bool kClamp, bool kHostRays, bool kScatter, bool kGather = false>
 __global__ void __launch_bounds__(kCastBlock, TB_CAST_MIN_BLOCKS) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
                                                       const float* __restrict__ d,
@@ -376,7 +400,8 @@ __global__ void __launch_bounds__(kCastBlock, TB_CAST_MIN_BLOCKS) cast_kernel(Me
                                                       int32_t* __restrict__ tet, int32_t* __restrict__ visited,
                                                       int32_t* __restrict__ triangle, double* __restrict__ t,
                                                       int32_t* __restrict__ tet_back,
-                                                      const int64_t* __restrict__ oidx) {
+                                                      const int64_t* __restrict__ oidx,
+                                                      const int64_t* __restrict__ ridx) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   float o0, o1, o2, d0, d1, d2;
   uint32_t cur;
@@ -387,7 +412,7 @@ __global__ void __launch_bounds__(kCastBlock, TB_CAST_MIN_BLOCKS) cast_kernel(Me
     cur = (uint32_t)__ldg(start + r);
   } else {
     if (r >= n) return;
-    const int64_t q = kGather ? __ldg(oidx + r) : r;
+    const int64_t q = kGather ? __ldg(ridx + r) : r;
     cur = (uint32_t)__ldg(start + q);
     o0 = __ldg(o + 3 * q); o1 = __ldg(o + 3 * q + 1); o2 = __ldg(o + 3 * q + 2);
     d0 = __ldg(d + 3 * q); d1 = __ldg(d + 3 * q + 1); d2 = __ldg(d + 3 * q + 2);
@@ -441,7 +466,11 @@ __global__ void __launch_bounds__(kCastBlock, TB_CAST_MIN_BLOCKS) cast_kernel(Me
     }
   }
   if (st != kError) st = (ref == kBoundary) ? kMiss : ((ref & kConstrained) ? kHit : kError);
-  const int64_t w = kScatter ? __ldg(oidx + r) : r;
+  // kGather alone reads through ridx and stores in place; the binned walk
+  // stores back through its permutation (oidx == ridx: the index already
+  // loaded) or through a composed one (multi-GPU scatter of a binned batch)
+  int64_t w = r;
+  if constexpr (kScatter) w = (kGather && oidx == ridx) ? __ldg(ridx + r) : __ldg(oidx + r);
   if constexpr (kHostRays) {
     // Zero-copy outputs cross PCIe as the warps' stores: every array gets
     // >= 128 B per warp store except the 1-byte status (32 B per warp).  A
@@ -804,6 +833,7 @@ __global__ void __launch_bounds__(kBlock) locate_kernel(MeshView m, int64_t n, c
     uint32_t nxt, entry;
     if (ref == kBoundary) break;
     if (ref & kConstrained) {
+      if ((ref & kPayload) >= (uint64_t)m.n_cf) break;  // corrupt mesh: no out-of-bounds gather
       const int2 ct = __ldg(&m.cf_tets[ref & kPayload]);
       const int32_t other = (ct.x == (int32_t)cur) ? ct.y : ct.x;
       if (other < 0) break;
@@ -988,7 +1018,9 @@ __global__ void __launch_bounds__(kBlock) shadow_kernel(MeshView m, int64_t n, c
     if (ref == kBoundary) break;
     if (ref & kConstrained) {
       const uint32_t cfi = ref & kPayload;
+      if (cfi >= (uint64_t)m.n_cf) break;  // corrupt mesh: no out-of-bounds gather
       const int32_t tri = __ldg(&m.cf_tri[cfi]);
+      if ((uint32_t)tri >= (uint64_t)m.n_tri) break;
       const double tt = seg_tri_t(o64, d64, m.tri + 9 * (int64_t)tri);
       if (tt >= one_m_eps) break;
       if (tt > eps) { oc = 1; break; }
@@ -1025,7 +1057,8 @@ __global__ void __launch_bounds__(kBlock, TB_SCTP_MIN_BLOCKS) sctp_kernel(MeshVi
                                                       uint8_t* __restrict__ status, int32_t* __restrict__ cf,
                                                       int32_t* __restrict__ tet, int32_t* __restrict__ visited,
                                                       int32_t* __restrict__ triangle, double* __restrict__ t,
-                                                      int32_t* __restrict__ tet_back) {
+                                                      int32_t* __restrict__ tet_back,
+                                                      const int64_t* __restrict__ oidx) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   float o0, o1, o2, d0, d1, d2;
   load_xyz_warp(o, r, n, o0, o1, o2);  // whole warp participates (shuffles)
@@ -1060,7 +1093,7 @@ __global__ void __launch_bounds__(kBlock, TB_SCTP_MIN_BLOCKS) sctp_kernel(MeshVi
     ++vis;
     if ((uint32_t)vis > n_tets) { st = kError; break; }
   }
-  write_result(m, r, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
+  write_result(m, oidx ? __ldg(oidx + r) : r, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
                tet_back);
 }
 
@@ -1082,32 +1115,35 @@ struct CastL {
   template <typename... A>
   static void launch(unsigned g, cudaStream_t s, bool safe, bool host_rays, const int64_t* oidx, A... a) {
     const bool nc = safe && L != 80;  // validated mesh: no per-step index clamp
+    const int64_t* none = nullptr;
     if (oidx != nullptr) {  // scattered outputs (device rays only)
       if (nc)
-        cast_kernel<L, false, false, true><<<g, kCastBlock, 0, s>>>(a..., oidx);
+        cast_kernel<L, false, false, true><<<g, kCastBlock, 0, s>>>(a..., oidx, none);
       else
-        cast_kernel<L, true, false, true><<<g, kCastBlock, 0, s>>>(a..., oidx);
+        cast_kernel<L, true, false, true><<<g, kCastBlock, 0, s>>>(a..., oidx, none);
     } else if (host_rays) {
       if (nc)
-        cast_kernel<L, false, true, false><<<g, kCastBlock, 0, s>>>(a..., oidx);
+        cast_kernel<L, false, true, false><<<g, kCastBlock, 0, s>>>(a..., oidx, none);
       else
-        cast_kernel<L, true, true, false><<<g, kCastBlock, 0, s>>>(a..., oidx);
+        cast_kernel<L, true, true, false><<<g, kCastBlock, 0, s>>>(a..., oidx, none);
     } else {
       if (nc)
-        cast_kernel<L, false, false, false><<<g, kCastBlock, 0, s>>>(a..., oidx);
+        cast_kernel<L, false, false, false><<<g, kCastBlock, 0, s>>>(a..., oidx, none);
       else
-        cast_kernel<L, true, false, false><<<g, kCastBlock, 0, s>>>(a..., oidx);
+        cast_kernel<L, true, false, false><<<g, kCastBlock, 0, s>>>(a..., oidx, none);
     }
   }
 };
+// Binned walk: rays read through perm; results stored through widx (perm
+// itself, or perm composed with a caller's scatter index).
 template <int L>
 struct CastBinnedL {
   template <typename... A>
-  static void launch(unsigned g, cudaStream_t s, bool safe, const int64_t* perm, A... a) {
+  static void launch(unsigned g, cudaStream_t s, bool safe, const int64_t* perm, const int64_t* widx, A... a) {
     if (safe && L != 80)
-      cast_kernel<L, false, false, true, true><<<g, kCastBlock, 0, s>>>(a..., perm);
+      cast_kernel<L, false, false, true, true><<<g, kCastBlock, 0, s>>>(a..., widx, perm);
     else
-      cast_kernel<L, true, false, true, true><<<g, kCastBlock, 0, s>>>(a..., perm);
+      cast_kernel<L, true, false, true, true><<<g, kCastBlock, 0, s>>>(a..., widx, perm);
   }
 };
 
@@ -1304,7 +1340,10 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
   DeviceGuard g(m->device);
   const MeshView v = m->view();
   int e = TB_OK;
-  if (oidx != nullptr) mode = 1;  // scattered outputs: one ray per lane
+  // Scattered outputs (multi-GPU frame assembly): one ray per lane or the
+  // binned walk (its permutation composed with oidx); the compaction and
+  // refill schedules have no scatter variant and run one ray per lane.
+  if (oidx != nullptr && mode != 6) mode = 1;
   if ((mode == 3 || mode == 4) && n < (int64_t)1 << 32) {
     e = mode == 3 ? launch_compact<256>(m->layout, m->safe, n, s, v, n, o, d, start, status, cf, tet, visited,
                                         triangle, t, tet_back)
@@ -1320,11 +1359,13 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
     const size_t hist_n = (size_t)(S ? n_segs * S : n_tiles) * kBins;
     const size_t hist_b = ((hist_n + kBins) * 4 + 255) & ~(size_t)255;
     char* scratch = nullptr;
-    if (int e2 = scratch_alloc(m->device, hist_b + (size_t)n * 8 + (size_t)n, s, &scratch)) return e2;
+    const size_t widx_b = oidx ? (size_t)n * 8 : 0;  // perm composed with the caller's scatter index
+    if (int e2 = scratch_alloc(m->device, hist_b + (size_t)n * 8 + widx_b + (size_t)n, s, &scratch)) return e2;
     int32_t* hist = reinterpret_cast<int32_t*>(scratch);
     int32_t* totals = hist + hist_n;
     int64_t* perm = reinterpret_cast<int64_t*>(scratch + hist_b);
-    uint8_t* bins = reinterpret_cast<uint8_t*>(scratch + hist_b + (size_t)n * 8);
+    int64_t* widx = oidx ? reinterpret_cast<int64_t*>(scratch + hist_b + (size_t)n * 8) : perm;
+    uint8_t* bins = reinterpret_cast<uint8_t*>(scratch + hist_b + (size_t)n * 8 + widx_b);
     if (S) {
       if (cudaError_t me = cudaMemsetAsync(hist, 0, hist_n * 4, s)) {  // the ragged segment's missing tiles count 0
         cudaFreeAsync(scratch, s);
@@ -1337,8 +1378,9 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
       bin_scan_kernel<<<kBins, 1024, 0, s>>>(hist, n_tiles, totals);
     }
     bin_scatter_kernel<<<n_tiles, kBinThreads, 0, s>>>(bins, n, hist, totals, n_tiles, S, perm);
-    e = launch_layout<CastBinnedL>(m->layout, grid_for(n, kCastBlock), s, m->safe, perm, v, n, o, d, start, status,
-                                   cf, tet, visited, triangle, t, tet_back);
+    if (oidx) compose_index_kernel<<<grid_for(n, 256), 256, 0, s>>>(perm, oidx, n, widx);
+    e = launch_layout<CastBinnedL>(m->layout, grid_for(n, kCastBlock), s, m->safe, perm, widx, v, n, o, d, start,
+                                   status, cf, tet, visited, triangle, t, tet_back);
     cudaFreeAsync(scratch, s);
   } else if (mode == 2) {
     e = launch_layout<CastPersistL>(m->layout, grid_for(n, kBlock), s, v, n, o, d, start, status, cf, tet, visited,
@@ -1458,24 +1500,25 @@ int tb_mesh_create(int device, int layout, int64_t n_points, const float* points
     TB_MC(cudaDeviceSynchronize());
   }
 
-  {
-    unsigned int* bad = nullptr;
-    unsigned int hbad = 1;
-    TB_MC(cudaMalloc(&bad, sizeof(unsigned int)));
-    TB_MC(cudaMemset(bad, 0, sizeof(unsigned int)));
-    validate_kernel<<<grid_for(n_tets, 256), 256>>>(layout, m->sv, m->sn, m->rec4, m->vx, n_tets, n_points, bad);
-    TB_MC(cudaGetLastError());
-    TB_MC(cudaMemcpy(&hbad, bad, sizeof(unsigned int), cudaMemcpyDeviceToHost));
-    cudaFree(bad);
-    m->safe = hbad == 0 && layout != 80;
-  }
-
   if (n_cf > 0) {
     TB_MC(cudaMalloc(&m->cf_tri, n_cf * sizeof(int32_t)));
     TB_MC(cudaMemcpy(m->cf_tri, cf_triangle, n_cf * sizeof(int32_t), cudaMemcpyHostToDevice));
     TB_MC(cudaMalloc(&m->cf_tets, n_cf * sizeof(int2)));
     TB_MC(cudaMemcpy(m->cf_tets, cf_tets, n_cf * sizeof(int2), cudaMemcpyHostToDevice));
   }
+  {
+    unsigned int* bad = nullptr;
+    unsigned int hbad = 1;
+    TB_MC(cudaMalloc(&bad, sizeof(unsigned int)));
+    TB_MC(cudaMemset(bad, 0, sizeof(unsigned int)));
+    validate_kernel<<<grid_for(n_tets, 256), 256>>>(layout, m->sv, m->sn, m->rec4, m->vx, n_tets, n_points, m->cf_tri,
+                                                    m->cf_tets, n_cf, n_tri, bad);
+    TB_MC(cudaGetLastError());
+    TB_MC(cudaMemcpy(&hbad, bad, sizeof(unsigned int), cudaMemcpyDeviceToHost));
+    cudaFree(bad);
+    m->safe = hbad == 0 && layout != 80;
+  }
+
   if (n_tri > 0) {
     TB_MC(cudaMalloc(&m->tri, n_tri * 9 * sizeof(double)));
     TB_MC(cudaMemcpy(m->tri, tri_coords, n_tri * 9 * sizeof(double), cudaMemcpyHostToDevice));
@@ -1617,6 +1660,36 @@ int tb_cast_rays_scatter(tb_mesh* m, int64_t n, const float* o, const float* d, 
                        false, out_index);
 }
 
+int tb_cast_rays_scatter_sched(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
+                               const int64_t* out_index, uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited,
+                               int32_t* triangle, double* t, int32_t* tet_back, int schedule, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  if (schedule < 0 || schedule > 6 || schedule == 5)
+    return set_error(TB_E_ARG, "schedule %d not in 0..4 or 6", schedule);
+  if (n == 0) return TB_OK;
+  if (!o || !d || !start || !out_index || !status || !cf || !tet || !visited)
+    return set_error(TB_E_ARG, "NULL ray buffer");
+  return cast_dispatch(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, (cudaStream_t)stream,
+                       schedule == 0 ? sched_mode() : schedule, false, out_index);
+}
+
+int tb_sctp_cast_rays_scatter(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
+                              const int64_t* out_index, uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited,
+                              int32_t* triangle, double* t, int32_t* tet_back, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  if (n == 0) return TB_OK;
+  if (!o || !d || !start || !out_index || !status || !cf || !tet || !visited)
+    return set_error(TB_E_ARG, "NULL ray buffer");
+  DeviceGuard g(m->device);
+  if (int e = launch_layout<SctpL>(m->layout, grid_for(n, kBlock), (cudaStream_t)stream, m->view(), n, o, d, start,
+                                   status, cf, tet, visited, triangle, t, tet_back, out_index))
+    return e;
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
 // Single-process multi-GPU trace (SURVEY 8 b's tb_trace_multi).  The frame's
 // 16 x 16-pixel tiles (render.py:496-514 order) go round-robin to the meshes;
 // every mesh's device walks its tiles straight from the frame's ray arrays on
@@ -1661,14 +1734,30 @@ int shard_indices(int device, int64_t W, int64_t H, int parts, int part, const i
 }
 
 // one non-blocking stream per (host thread, device) for the non-root devices
-cudaStream_t multi_stream(int device) {
-  static thread_local cudaStream_t streams[64] = {};
-  if (device < 0 || device >= 64) return nullptr;
-  if (!streams[device]) {
-    DeviceGuard g(device);
-    cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking);
+// Per host thread and device; destroyed when the thread exits.
+struct MultiStreams {
+  cudaStream_t s[64] = {};
+  ~MultiStreams() {
+    for (int dv = 0; dv < 64; ++dv) {
+      if (!s[dv]) continue;
+      int prev = -1;
+      cudaGetDevice(&prev);
+      cudaSetDevice(dv);
+      cudaStreamSynchronize(s[dv]);
+      cudaStreamDestroy(s[dv]);
+      if (prev >= 0) cudaSetDevice(prev);
+    }
+    cudaGetLastError();  // teardown errors (runtime already unloading) are not reportable
   }
-  return streams[device];
+};
+cudaStream_t multi_stream(int device) {
+  static thread_local MultiStreams streams;
+  if (device < 0 || device >= 64) return nullptr;
+  if (!streams.s[device]) {
+    DeviceGuard g(device);
+    cudaStreamCreateWithFlags(&streams.s[device], cudaStreamNonBlocking);
+  }
+  return streams.s[device];
 }
 }  // namespace
 
@@ -1719,7 +1808,7 @@ int tb_trace_multi(int n_meshes, tb_mesh* const* meshes, int64_t width, int64_t 
       err = set_error(TB_E_CUDA, "cross-device wait failed");
       break;
     }
-    if ((err = launch_layout<CastBinnedL>(m->layout, grid_for(count, kCastBlock), sk, m->safe, idx, m->view(), count, o,
+    if ((err = launch_layout<CastBinnedL>(m->layout, grid_for(count, kCastBlock), sk, m->safe, idx, idx, m->view(), count, o,
                                           d, start, status, cf, tet, visited, triangle, t, tet_back)) != TB_OK)
       break;
     if (sk != s0) {
@@ -1816,7 +1905,7 @@ int tb_sctp_cast_rays(tb_mesh* m, int64_t n, const float* o, const float* d, con
   DeviceGuard g(m->device);
   const cudaStream_t s = (cudaStream_t)stream;
   if (int e = launch_layout<SctpL>(m->layout, grid_for(n, kBlock), s, m->view(), n, o, d, start, status, cf,
-                                   tet, visited, triangle, t, tet_back))
+                                   tet, visited, triangle, t, tet_back, (const int64_t*)nullptr))
     return e;
   TB_CUDA(cudaGetLastError());
   return TB_OK;

@@ -39,6 +39,8 @@ struct MeshView {
   const uint8_t* __restrict__ orient; // (t,) rho(sorted quad) > 0, see orientation()
   int64_t n_points;
   int64_t n_tets;
+  int64_t n_cf;   // constrained faces (rows of cf_tri / cf_tets)
+  int64_t n_tri;  // scene triangles (rows of tri)
 };
 
 // Index of the axis-permuted point copy holding (q[mx], q[ot], q[mn]).

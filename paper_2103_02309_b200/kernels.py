@@ -86,12 +86,32 @@ def cast_rays(mesh, o32, d32, start, visits_sink=None):
         status, cf, tet, visited, *_ = _cast_plain(mesh, o32, d32, start)
         return status, cf, tet, visited
     status, cf, tet, visited, seq, offsets = cast_rays_csr(mesh, o32, d32, start)
-    n = len(status)
-    if n:
-        for k in range(int(visited.max())):
-            rays = np.nonzero(visited > k)[0]
-            visits_sink.append((rays.astype(np.int64), seq[offsets[rays] + k].copy()))
+    emit_visits(visits_sink, visited, seq, offsets)
     return status, cf, tet, visited
+
+
+# Rays longer than this go to the sink as one chunk each (the compiled
+# reference's format); shorter ones as step wavefronts.
+_WAVEFRONT_STEPS = 32
+
+
+def emit_visits(sink: list, visited: np.ndarray, seq: np.ndarray, offsets: np.ndarray) -> None:
+    """CSR visit sequences -> the sink chunks batch.cast_rays_visits consumes
+    (batch.py:101-114): ``(rays, tets)`` with distinct rays, appended in step
+    order per ray.  Rays of at most 32 visits go out as step wavefronts (one
+    chunk per step k: every short ray with more than k visits), longer rays
+    -- and cycle-guard rays, n_tets + 1 visits -- as one chunk per ray, like
+    the compiled reference (_kernels.pyx:307-341).  Cost O(total visits)."""
+    n = len(visited)
+    if n == 0:
+        return
+    short = np.nonzero(visited <= _WAVEFRONT_STEPS)[0]
+    vs = visited[short]
+    for k in range(int(vs.max(initial=0))):
+        rays = short[vs > k]
+        sink.append((rays.astype(np.int64), seq[offsets[rays] + k]))
+    for r in np.nonzero(visited > _WAVEFRONT_STEPS)[0]:
+        sink.append((np.full(int(visited[r]), r, dtype=np.int64), seq[offsets[r]:offsets[r + 1]].copy()))
 
 
 def _cast_plain(mesh, o32, d32, start):

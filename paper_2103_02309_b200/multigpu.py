@@ -134,8 +134,10 @@ def split_chunks(n: int, chunks: int) -> list[tuple[int, int]]:
 class FrameGather:
     """Every frame's hits to the root, overlapped with tracing.
 
-    All ranks know every rank's shard (``shard_pixels`` is deterministic), so
-    chunk sizes need no exchange.  The caller traces chunk k of its shard and
+    All ranks know every rank's shard (``shard_pixels`` is deterministic, or
+    ``index`` -- this rank's global ray indices when the job does not cover
+    every slot -- is exchanged once at setup), so chunk sizes need no
+    exchange per step; slots no rank traces keep the "no ray" values.  The caller traces chunk k of its shard and
     calls ``send(k, res_k)``: the chunk's compact records go out with an
     async ``dist.gather`` (NCCL runs it on its own stream, ordered after the
     trace), while the caller already traces chunk k+1 on its stream.
@@ -146,7 +148,7 @@ class FrameGather:
     """
 
     def __init__(self, width, height, world, rank, frames, chunks, device, cf_triangle, cf_tets, root=0,
-                 group=None, tile=16):
+                 group=None, tile=16, index=None):
         import torch
         import torch.distributed as dist
 
@@ -155,7 +157,11 @@ class FrameGather:
         # gloo moves host tensors only: stage through host memory there
         self.comm = torch.device("cpu") if dist.get_backend(group) == "gloo" else self.device
         self.total = width * height * frames
-        shards = [shard_pixels(width, height, r, world, tile, frames) for r in range(world)]
+        if index is None:  # the static tile shards: every rank derives every rank's
+            shards = [shard_pixels(width, height, r, world, tile, frames) for r in range(world)]
+        else:  # data-dependent shards (e.g. secondaries of primary hits): exchanged once at setup
+            shards = [None] * world
+            dist.all_gather_object(shards, np.ascontiguousarray(index, dtype=np.int64), group=group)
         self.pieces = [split_chunks(len(s), chunks) for s in shards]  # per rank, same count everywhere
         self.n_chunks = len(self.pieces[0])
         self.cap = [max(1, max(p[k][1] - p[k][0] for p in self.pieces)) for k in range(self.n_chunks)]
@@ -248,23 +254,39 @@ class PeerFrameGather:
 
     The root allocates the job's seven full-frame arrays in one device block
     and shares it with the other ranks by CUDA IPC (the 64-byte handle goes
-    out with one broadcast at setup).  Every rank then traces its tiles with
-    ``tb_cast_rays_scatter``: the kernel's epilogue stores each finished
-    ray's results straight into the root's arrays at the ray's global index
-    -- P2P stores over NVLink that overlap the walk ray by ray, instead of a
-    trace followed by a gather.  ``step`` ends with a stream sync and a
-    barrier, after which the root's ``frame`` holds the whole job (the same
-    arrays a single-GPU trace of all of it returns).
+    out with one broadcast at setup).  Every rank then traces its rays with
+    ``tb_cast_rays_scatter_sched`` (or ``tb_sctp_cast_rays_scatter``): the
+    kernel's epilogue stores each finished ray's results straight into the
+    root's arrays at the ray's global index -- P2P stores over NVLink that
+    overlap the walk ray by ray, instead of a trace followed by a gather.
+    ``step`` ends with a stream sync and a barrier, after which the root's
+    returned frame holds the whole job (the same arrays a single-GPU trace of
+    all of it returns).
+
+    ``index``: the global ray indices this rank traces (default: its 16x16
+    tile shard, ``shard_pixels``).  Jobs that do not cover every slot (e.g.
+    diffuse secondaries, spawned only from primary hits) pass the rank's real
+    index array; slots no rank traces keep the "no ray" values (status 0,
+    cf / triangle / tet / tet_back -1, t +inf, visited 0) written once at
+    setup.
+
+    Two frame buffers alternate between steps, so a rank that runs ahead into
+    step k+1 writes the other buffer while the root still reads step k's
+    (every rank passes step k's closing barrier before any starts k+2).
 
     ``root_rays``: lean assembly.  Every rank passes it -- the root the job's
     full (origins, dirs) device tensors in global ray order, the others
     ``True`` -- and the ranks then store only status / cf / tet / visited
     (13 B per ray over NVLink instead of 29); after the barrier the root
     derives triangle / t / tet_back for the whole job with
-    ``tb_cast_epilogue`` (bit-identical to the fused epilogue).
+    ``tb_cast_epilogue`` (bit-identical to the fused epilogue).  ``step`` may
+    pass this step's rays (``root_rays=``) when they change between steps.
     """
 
-    def __init__(self, width, height, world, rank, frames, device, root=0, group=None, tile=16, root_rays=None):
+    BUFFERS = 2
+
+    def __init__(self, width, height, world, rank, frames, device, root=0, group=None, tile=16, root_rays=None,
+                 index=None):
         import ctypes
 
         import torch
@@ -273,24 +295,24 @@ class PeerFrameGather:
         from ._lib import check, lib
 
         self.world, self.rank, self.root, self.group = world, rank, root, group
-        # lean assembly (every rank passes root_rays=True, the root the job's
-        # (origins, dirs) tensors): ranks store only status / cf / tet /
-        # visited (13 B per ray instead of 29) and the root derives triangle,
-        # t and tet_back with tb_cast_epilogue from its own copy of the rays
         self.lean = root_rays is not None
         self.root_rays = root_rays if (self.lean and rank == root) else None
         self.device = torch.device(device)
         self.total = width * height * frames
-        shard = shard_pixels(width, height, rank, world, tile, frames)
-        self.idx = torch.from_numpy(shard).to(self.device)
+        shard = shard_pixels(width, height, rank, world, tile, frames) if index is None else np.asarray(index)
+        if shard.size and (shard.min() < 0 or shard.max() >= self.total):
+            raise ValueError(f"index out of range [0, {self.total})")
+        self.idx = torch.from_numpy(np.ascontiguousarray(shard, dtype=np.int64)).to(self.device)
         self.offsets = []
         off = 0
         for _, _, size in _OUTPUTS:
             self.offsets.append(off)
             off += (size * self.total + 255) // 256 * 256
-        self.bytes = off
+        self.frame_bytes = off
+        self.bytes = off * self.BUFFERS
         self.base = None
         self.remote = None
+        self.steps = 0
         dev_idx = self.device.index if self.device.index is not None else torch.cuda.current_device()
         handle = None
         err = None
@@ -329,31 +351,64 @@ class PeerFrameGather:
                 self.base = None
             raise RuntimeError(f"peer frame assembly unavailable: {failed[0] if failed else 'no IPC handle'}")
         dest = self.base if rank == root else self.remote
-        self.ptrs = [dest + o for o in self.offsets]
-        self.frame = None
+        self.ptrs = [[dest + b * self.frame_bytes + o for o in self.offsets] for b in range(self.BUFFERS)]
+        self.frames = None
         if rank == root:
-            self.frame = {name: torch.as_tensor(_CudaArray(self.base + o, self.total, ts), device=self.device)
-                          for (name, ts, _), o in zip(_OUTPUTS, self.offsets)}
+            fills = {"status": 0, "cf": -1, "tet": -1, "visited": 0, "triangle": -1, "t": float("inf"),
+                     "tet_back": -1}
+            self.frames = []
+            for b in range(self.BUFFERS):
+                fr = {name: torch.as_tensor(_CudaArray(self.base + b * self.frame_bytes + o, self.total, ts),
+                                            device=self.device)
+                      for (name, ts, _), o in zip(_OUTPUTS, self.offsets)}
+                for name, a in fr.items():
+                    a.fill_(fills[name])
+                self.frames.append(fr)
+            torch.cuda.synchronize(self.device)
+        dist.barrier(group=group)  # the defaults are in place before any rank stores
 
-    def step(self, dm, origins, dirs, start, stream=None):
+    @property
+    def frame(self):
+        """The root's most recently completed frame (None on other ranks)."""
+        if self.frames is None:
+            return None
+        return self.frames[(self.steps - 1) % self.BUFFERS if self.steps else 0]
+
+    def step(self, dm, origins, dirs, start, stream=None, *, schedule="lane", sctp=False, root_rays=None):
         """Trace this rank's rays into the root's frame; returns the frame on
-        the root (torch tensors over the shared block), None elsewhere."""
+        the root (torch tensors over the shared block), None elsewhere.
+        ``schedule``: "lane" or "binned" (the binned walk's permutation is
+        composed with the scatter index); ``sctp`` runs the ScTP walk."""
         import torch
         import torch.distributed as dist
 
-        from ._lib import addr, check, lib
+        from ._lib import SCHEDULES, addr, check, lib
 
+        n = self.idx.numel()
+        if origins.shape[0] != n or dirs.shape[0] != n or start.numel() != n:
+            raise ValueError(f"this rank traces {n} rays (its index), got {origins.shape[0]} origins, "
+                             f"{dirs.shape[0]} dirs, {start.numel()} starts")
         s = stream or torch.cuda.current_stream(self.device)
+        ptrs = self.ptrs[self.steps % self.BUFFERS]
         # _OUTPUTS order: status, cf, tet, visited, triangle, t, tet_back
-        ptrs = self.ptrs[:4] + [None, None, None] if self.lean else self.ptrs
-        check(lib.tb_cast_rays_scatter(dm.handle, self.idx.numel(), addr(origins), addr(dirs), addr(start),
-                                       addr(self.idx), *ptrs, s.cuda_stream), "tb_cast_rays_scatter")
+        outs = ptrs[:4] + [None, None, None] if self.lean else ptrs
+        if sctp:
+            check(lib.tb_sctp_cast_rays_scatter(dm.handle, n, addr(origins), addr(dirs), addr(start), addr(self.idx),
+                                                *outs, s.cuda_stream), "tb_sctp_cast_rays_scatter")
+        else:
+            mode = SCHEDULES[schedule] if isinstance(schedule, str) else int(schedule)
+            check(lib.tb_cast_rays_scatter_sched(dm.handle, n, addr(origins), addr(dirs), addr(start),
+                                                 addr(self.idx), *outs, mode, s.cuda_stream),
+                  "tb_cast_rays_scatter_sched")
         s.synchronize()  # this rank's stores have landed in the root's memory
         dist.barrier(group=self.group)
-        if self.root_rays is not None:
-            ro, rd = self.root_rays
-            check(lib.tb_cast_epilogue(dm.handle, self.total, addr(ro), addr(rd), self.ptrs[1], self.ptrs[2],
-                                       self.ptrs[4], self.ptrs[5], self.ptrs[6], s.cuda_stream), "tb_cast_epilogue")
+        self.steps += 1
+        if self.rank == self.root and self.lean:
+            ro, rd = root_rays if root_rays is not None else self.root_rays
+            if ro.shape[0] != self.total or rd.shape[0] != self.total:
+                raise ValueError(f"root_rays must hold the job's {self.total} rays")
+            check(lib.tb_cast_epilogue(dm.handle, self.total, addr(ro), addr(rd), ptrs[1], ptrs[2], ptrs[4], ptrs[5],
+                                       ptrs[6], s.cuda_stream), "tb_cast_epilogue")
             s.synchronize()
         return self.frame
 
@@ -367,7 +422,7 @@ class PeerFrameGather:
             self.remote = None
         dist.barrier(group=self.group)  # every mapping is gone before the root frees the block
         if self.base is not None:
-            self.frame = None
+            self.frames = None
             lib.tb_device_free(self.base)
             self.base = None
 

@@ -28,6 +28,28 @@ def test_reference_arm_json_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert d["tets_visited_per_ray"]["mean"] == pytest.approx(4.49, abs=0.01)
+    # the reference arm runs the reference only: its own compiled kernels, not this repo's CUDA library
+    assert not any("libtetb200" in so for so in d["native_so_loaded"]), d["native_so_loaded"]
+    assert any(so.startswith("oracle/_ref/") for so in d["native_so_loaded"])
+    # both arms describe the workload with the same config dict
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    assert d["config"] == bench.config_dict(bench.CONFIGS[1], 1)
+
+
+@pytest.mark.timeout(300)
+def test_gpus_flag_launches_ranks_and_fails_loudly_without_gpus():
+    """--gpus 2 outside torchrun relaunches under torch.distributed.run; with
+    fewer visible GPUs than ranks every rank exits with the reason."""
+    import torch
+
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("enough GPUs here: the multi-GPU bench is exercised on the box")
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode != 0
+    assert "torch.distributed.run" in out.stderr and "visible GPU" in out.stderr, out.stderr[-2000:]
 
 
 def test_bench_rejects_short_warmup():

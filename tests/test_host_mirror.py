@@ -163,3 +163,41 @@ def test_hull_faces_order(meshes):
     assert len(h) == 6 * 2 * 16  # every wall face of the n=4 box
     assert np.all(np.diff(h[:, 0] * 4 + h[:, 1]) > 0)  # tet-major, slot-minor
     assert len(hull_faces(meshes["open_box4"])) == len(h)
+
+
+def _consume_sink(sink, visited):
+    """The reference's sink consumer, restated (batch.py:98-114)."""
+    offsets = np.zeros(len(visited) + 1, dtype=np.int64)
+    np.cumsum(visited, out=offsets[1:])
+    visits = np.empty(int(offsets[-1]), dtype=np.int32)
+    pos = offsets[:-1].copy()
+    for rays, tets in sink:
+        if len(rays) and rays[0] == rays[-1] and (rays == rays[0]).all():
+            i = int(rays[0])
+            visits[pos[i]:pos[i] + len(tets)] = tets
+            pos[i] += len(tets)
+        else:
+            visits[pos[rays]] = tets
+            pos[rays] += 1
+    return visits, offsets
+
+
+def test_visits_sink_emission_is_linear_and_consumable():
+    """kernels.emit_visits: short rays as step wavefronts, long
+    and cycle-guard rays as one chunk each -- the reference consumer rebuilds
+    the exact CSR, and the chunk count stays O(32 + long rays) even with a
+    ray of a million visits."""
+    from paper_2103_02309_b200.kernels import emit_visits
+
+    rng = np.random.default_rng(7)
+    visited = rng.integers(1, 60, 5000).astype(np.int32)
+    visited[17] = 1_000_001  # a cycle-guard ray on a 1 M-tet mesh
+    visited[4000] = 1
+    offsets = np.zeros(len(visited) + 1, np.int64)
+    np.cumsum(visited, out=offsets[1:])
+    seq = rng.integers(0, 1 << 30, int(offsets[-1])).astype(np.int32)
+    sink: list = []
+    emit_visits(sink, visited, seq, offsets)
+    assert len(sink) <= 32 + int((visited > 32).sum())
+    got, off = _consume_sink(sink, visited)
+    assert np.array_equal(off, offsets) and np.array_equal(got, seq)

@@ -23,7 +23,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, result_path, lean=False):
+def _worker(rank, world, port, result_path, mode="full"):
+    """mode: "full" (29 B per ray stored), "lean" (13 B, root epilogue),
+    "binned" (the binned walk's permutation composed with the scatter
+    index), "sctp" (the ScTP walk scattering), "partial" (each rank traces
+    a data-dependent subset -- like diffuse secondaries of primary hits --
+    under the binned schedule; untraced slots keep the "no ray" values).
+    Every mode runs two steps with different rays (camera moved between
+    them): the returned frame must be the second job's, exactly."""
     import torch
     import torch.distributed as dist
 
@@ -42,25 +49,47 @@ def _worker(rank, world, port, result_path, lean=False):
         raw, soup = build_box_fixture(6, occluders=[(0, 3, (1, 1), (5, 5))])
         mesh = encode(raw, "tet20", soup)
         W, H, frames = 80, 60, world
-        o_all, d_all, st_all = [], [], []
-        for f in range(frames):
-            o, d = camera_rays((0.6 + 0.05 * f, 2.9, 3.1), (5.5, 3.2, 2.8), (0, 1, 0), 60.0, W, H)
-            cam, _ = pyoracle.locate_points(mesh, np.array([[0.6 + 0.05 * f, 2.9, 3.1]]), np.array([0], np.int32))
-            o_all.append(o)
-            d_all.append(d)
-            st_all.append(np.full(len(o), cam[0], np.int32))
-        o_all, d_all, st_all = (np.concatenate(a) for a in (o_all, d_all, st_all))
+
+        def job(shift):
+            o_all, d_all, st_all = [], [], []
+            for f in range(frames):
+                pos = (0.6 + 0.05 * f + shift, 2.9, 3.1)
+                o, d = camera_rays(pos, (5.5, 3.2, 2.8), (0, 1, 0), 60.0, W, H)
+                cam, _ = pyoracle.locate_points(mesh, np.array([pos]), np.array([0], np.int32))
+                o_all.append(o)
+                d_all.append(d)
+                st_all.append(np.full(len(o), cam[0], np.int32))
+            return [np.concatenate(a) for a in (o_all, d_all, st_all)]
+
+        jobs = [job(0.0), job(0.13)]
+        lean = mode == "lean"
+        index = None
+        if mode == "partial":  # drop every third ray of this rank's shard
+            shard = multigpu.shard_pixels(W, H, rank, world, 16, frames)
+            index = shard[np.arange(len(shard)) % 3 != 1]
         root_rays = None
         if lean:
-            root_rays = tuple(torch.from_numpy(a).to(dev) for a in (o_all, d_all)) if rank == 0 else True
-        pg = multigpu.PeerFrameGather(W, H, world, rank, frames, dev, root_rays=root_rays)
+            root_rays = tuple(torch.from_numpy(a).to(dev) for a in jobs[0][:2]) if rank == 0 else True
+        pg = multigpu.PeerFrameGather(W, H, world, rank, frames, dev, root_rays=root_rays, index=index)
         idx = pg.idx.cpu().numpy()
         dm = device_mesh(mesh, device=0)
-        g = [torch.from_numpy(a[idx]).to(dev) for a in (o_all, d_all, st_all)]
-        for _ in range(2):  # reusable frame after frame
-            frame = pg.step(dm, *g)
+        schedule = "binned" if mode in ("binned", "partial") else "lane"
+        for o_all, d_all, st_all in jobs:  # reusable frame after frame, rays changing
+            g = [torch.from_numpy(np.ascontiguousarray(a[idx])).to(dev) for a in (o_all, d_all, st_all)]
+            rr = tuple(torch.from_numpy(a).to(dev) for a in (o_all, d_all)) if (lean and rank == 0) else None
+            frame = pg.step(dm, *g, schedule=schedule, sctp=mode == "sctp", root_rays=rr)
+        with pytest.raises(ValueError):  # the ray count must match the rank's index
+            pg.step(dm, g[0][:-1], g[1][:-1], g[2][:-1])
         if rank == 0:
-            exp = pyoracle.cast_rays_full(mesh, o_all, d_all, st_all, n_threads=1)
+            o_all, d_all, st_all = jobs[-1]
+            exp = list(pyoracle.cast_rays_full(mesh, o_all, d_all, st_all, n_threads=1, sctp=mode == "sctp"))
+            if mode == "partial":  # slots no rank traced
+                traced = np.zeros(len(st_all), bool)
+                for r in range(world):
+                    sh = multigpu.shard_pixels(W, H, r, world, 16, frames)
+                    traced[sh[np.arange(len(sh)) % 3 != 1]] = True
+                for e, fill in zip(exp, (0, -1, -1, 0, -1, np.inf, -1)):
+                    e[~traced] = fill
             ok = all(np.array_equal(frame[k].cpu().numpy(), e) for k, e in
                      zip(("status", "cf", "tet", "visited", "triangle", "t", "tet_back"), exp))
             with open(result_path, "w") as fh:
@@ -71,15 +100,14 @@ def _worker(rank, world, port, result_path, lean=False):
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("lean", (False, True))
-def test_p2p_frame_assembly_two_ranks(tmp_path, lean):
+@pytest.mark.parametrize("mode", ("full", "lean", "binned", "sctp", "partial"))
+def test_p2p_frame_assembly_two_ranks(tmp_path, mode):
     """Two ranks (sharing cuda:0 here) assemble the frame set on rank 0 by P2P
-    stores; lean: 13 B per ray stored, triangle / t / tet_back derived on the
-    root (tb_cast_epilogue).  Either way the frame equals the oracle."""
+    stores, in every mode (see _worker); the frame equals the oracle."""
     import torch.multiprocessing as mp
 
     path = str(tmp_path / "result.txt")
-    mp.start_processes(_worker, args=(2, _free_port(), path, lean), nprocs=2, start_method="spawn", join=True)
+    mp.start_processes(_worker, args=(2, _free_port(), path, mode), nprocs=2, start_method="spawn", join=True)
     assert open(path).read() == "ok"
 
 

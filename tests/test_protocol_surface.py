@@ -12,7 +12,10 @@ from pathlib import Path
 
 import pytest
 
-REF_PURE = Path("/root/reference/pkg/src/tetray/_kernels_py.py")
+from refpkg import REF_SITE
+
+# the installed reference (oracle/_ref/site, shipped to the GPU box)
+REF_PURE = REF_SITE / "tetray" / "_kernels_py.py"
 PROTOCOL = {
     "cast_rays": ["mesh", "o32", "d32", "start", "visits_sink"],
     "locate_points": ["mesh", "q", "hints"],
@@ -35,7 +38,7 @@ def test_module_constants_and_functions():
     assert dict(_params(K.shadow_rays))["eps"] == 1e-4
 
 
-@pytest.mark.skipif(not REF_PURE.exists(), reason="reference source not mounted (GPU box)")
+@pytest.mark.skipif(not REF_PURE.exists(), reason="oracle/_ref/site missing: run oracle/build_ref.sh")
 def test_signatures_equal_the_reference_kernel_module():
     spec = importlib.util.spec_from_file_location("ref_kernels_py", REF_PURE)
     ref = importlib.util.module_from_spec(spec)
@@ -57,12 +60,12 @@ def test_batch_mirror_signatures():
         assert params[0] == "mesh" and "kernels" in params, (name, params)
 
 
-@pytest.mark.skipif(not REF_PURE.exists(), reason="reference source not mounted (GPU box)")
+@pytest.mark.skipif(not REF_PURE.exists(), reason="oracle/_ref/site missing: run oracle/build_ref.sh")
 def test_batch_mirror_matches_reference_batch_signatures():
     import subprocess
     import sys
 
-    code = ("import sys, inspect, json; sys.path.insert(0, '/root/reference/pkg/src'); import tetray.batch as b; "
+    code = (f"import sys, inspect, json; sys.path.insert(0, {str(REF_SITE)!r}); import tetray.batch as b; "
             "print(json.dumps({n: [p.name for p in inspect.signature(getattr(b, n)).parameters.values()] "
             "for n in ('cast_rays', 'cast_rays_visits', 'locate_points', 'shadow_rays')}))")
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
