@@ -1073,7 +1073,7 @@ def main():
     ap.add_argument("--gather", choices=("p2p", "nccl"), default="p2p",
                     help="N > 1 frame assembly: fused P2P stores (default) or the chunked NCCL gather")
     ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1 NCCL gather: trace/gather pipeline depth")
-    ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512", "binned"),
+    ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512", "dynamic", "binned"),
                     help="ray-to-lane schedule of the timed trace (default: binned for secondaries, else lane)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-l2-probe", action="store_true", help="skip the L2 gather-roof probe (roofline_l2)")

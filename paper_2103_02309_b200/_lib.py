@@ -94,7 +94,7 @@ def check(code: int, what: str) -> None:
         raise TetB200Error(f"{what} failed ({code}): {msg.decode() if msg else 'unknown error'}")
 
 
-SCHEDULES = {"auto": 0, "lane": 1, "refill": 2, "compact": 3, "compact512": 4, "binned": 6}
+SCHEDULES = {"auto": 0, "lane": 1, "refill": 2, "compact": 3, "compact512": 4, "dynamic": 5, "binned": 6}
 
 
 def set_schedule(mode: str | int | None = None, steps_per_round: int | None = None) -> None:

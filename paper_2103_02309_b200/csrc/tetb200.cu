@@ -371,9 +371,69 @@ __device__ __forceinline__ bool long_walk(const MeshView& m, const float4* __res
   return false;
 }
 
+// The walk of one ray, _kernels.pyx:343-369: init (basis, start window,
+// first exit), the 4x-unrolled xor walk, the exact single-step tail with the
+// cycle guard.  On return `cur` is the terminating tet, `ref` the exit
+// reference, `vis` the visited count and `st` the status.  Shared by the
+// launch-per-128-rays kernel and the dynamically scheduled one.
+constexpr int kUnroll = 4;
+
+template <int L, bool kClamp>
+__device__ __forceinline__ void walk_ray(const MeshView& m, float o0, float o1, float o2, float d0, float d1,
+                                         float d2, uint32_t& cur, uint32_t& ref, int& vis, uint8_t& st) {
+  Basis b;
+  uint32_t idx[3];
+  float p[6];
+  const int j = init_ray(m, o0, o1, o2, d0, d1, d2, (int)cur, b, idx, p);
+  ref = pick4u(__ldg(&m.sn[cur]), j);
+  const float4* __restrict__ P = ray_points(m, b);
+  vis = 1;
+  st = 255;
+  const uint32_t n_tets = (uint32_t)m.n_tets;
+  // Every plain tet reference is < n_tets; the boundary sentinel
+  // (0x7FFFFFFF) and constrained refs (bit 31) are >= n_tets, so one
+  // unsigned compare per step decides "keep walking" (corrupt refs also land
+  // outside and are classified below).
+  const uint32_t fast_limit = n_tets < kCycleCheckAfter ? n_tets : kCycleCheckAfter;
+  // Unrolled fast loop: the visited count and its threshold test once per
+  // kUnroll steps (saves ~2.5 ALU-pipe ops per step, r01 A/B +1.5-3 %).  It
+  // only runs while all kUnroll steps fit under fast_limit; the exact
+  // single-step loop below finishes the walk.
+  // (The early exits add their own step count, so no per-step counter.)
+  static_assert(kUnroll == 4, "the unrolled body below is written out for 4 steps");
+  while (ref < n_tets && vis + kUnroll <= (int)fast_limit) {
+    uint32_t nxt = ref;
+    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+    cur = nxt;
+    if (ref >= n_tets) { vis += 1; break; }
+    nxt = ref;
+    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+    cur = nxt;
+    if (ref >= n_tets) { vis += 2; break; }
+    nxt = ref;
+    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+    cur = nxt;
+    if (ref >= n_tets) { vis += 3; break; }
+    nxt = ref;
+    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+    cur = nxt;
+    vis += 4;
+  }
+  while (ref < n_tets) {
+    const uint32_t nxt = ref;
+    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
+    cur = nxt;
+    if ((uint32_t)++vis > fast_limit) {
+      // Long walk: finish it in the cycle-detecting slow path (exact).
+      if ((uint32_t)vis > n_tets || long_walk<L, kClamp>(m, P, b, idx, p, ref, cur, vis)) st = kError;
+      break;
+    }
+  }
+  if (st != kError) st = (ref == kBoundary) ? kMiss : ((ref & kConstrained) ? kHit : kError);
+}
+
 // ----------------------------------------------------------------------------
 // Primary traversal kernel: one lane per ray, _kernels.pyx:343-369.
-constexpr int kUnroll = 4;
 
 // kHostRays: the ray arrays are mapped pinned host memory (zero-copy e2e
 // path) -- load them with the warp-cooperative 16 B row loads so every input
@@ -417,55 +477,10 @@ __global__ void __launch_bounds__(kCastBlock, TB_CAST_MIN_BLOCKS) cast_kernel(Me
     o0 = __ldg(o + 3 * q); o1 = __ldg(o + 3 * q + 1); o2 = __ldg(o + 3 * q + 2);
     d0 = __ldg(d + 3 * q); d1 = __ldg(d + 3 * q + 1); d2 = __ldg(d + 3 * q + 2);
   }
-  Basis b;
-  uint32_t idx[3];
-  float p[6];
-  const int j = init_ray(m, o0, o1, o2, d0, d1, d2, (int)cur, b, idx, p);
-  uint32_t ref = pick4u(__ldg(&m.sn[cur]), j);
-  const float4* __restrict__ P = ray_points(m, b);
-  int vis = 1;
-  uint8_t st = 255;
-  const uint32_t n_tets = (uint32_t)m.n_tets;
-  // Every plain tet reference is < n_tets; the boundary sentinel
-  // (0x7FFFFFFF) and constrained refs (bit 31) are >= n_tets, so one
-  // unsigned compare per step decides "keep walking" (corrupt refs also land
-  // outside and are classified below).
-  const uint32_t fast_limit = n_tets < kCycleCheckAfter ? n_tets : kCycleCheckAfter;
-  // Unrolled fast loop: the visited count and its threshold test once per
-  // kUnroll steps (saves ~2.5 ALU-pipe ops per step, r01 A/B +1.5-3 %).  It
-  // only runs while all kUnroll steps fit under fast_limit; the exact
-  // single-step loop below finishes the walk.
-  // (The early exits add their own step count, so no per-step counter.)
-  static_assert(kUnroll == 4, "the unrolled body below is written out for 4 steps");
-  while (ref < n_tets && vis + kUnroll <= (int)fast_limit) {
-    uint32_t nxt = ref;
-    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
-    cur = nxt;
-    if (ref >= n_tets) { vis += 1; break; }
-    nxt = ref;
-    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
-    cur = nxt;
-    if (ref >= n_tets) { vis += 2; break; }
-    nxt = ref;
-    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
-    cur = nxt;
-    if (ref >= n_tets) { vis += 3; break; }
-    nxt = ref;
-    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
-    cur = nxt;
-    vis += 4;
-  }
-  while (ref < n_tets) {
-    const uint32_t nxt = ref;
-    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
-    cur = nxt;
-    if ((uint32_t)++vis > fast_limit) {
-      // Long walk: finish it in the cycle-detecting slow path (exact).
-      if ((uint32_t)vis > n_tets || long_walk<L, kClamp>(m, P, b, idx, p, ref, cur, vis)) st = kError;
-      break;
-    }
-  }
-  if (st != kError) st = (ref == kBoundary) ? kMiss : ((ref & kConstrained) ? kHit : kError);
+  uint32_t ref;
+  int vis;
+  uint8_t st;
+  walk_ray<L, kClamp>(m, o0, o1, o2, d0, d1, d2, cur, ref, vis, st);
   // kGather alone reads through ridx and stores in place; the binned walk
   // stores back through its permutation (oidx == ridx: the index already
   // loaded) or through a composed one (multi-GPU scatter of a binned batch)
@@ -491,6 +506,46 @@ __global__ void __launch_bounds__(kCastBlock, TB_CAST_MIN_BLOCKS) cast_kernel(Me
   }
   write_result(m, w, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
                tet_back);
+}
+
+// ----------------------------------------------------------------------------
+// Dynamically scheduled walk (schedule 5, "dynamic"): one wave of resident
+// blocks; each warp takes the next 32 consecutive rays from a global counter
+// (one atomicAdd per chunk, issued a chunk ahead so its latency hides under
+// the walk) until the batch is exhausted.  Chunks go out in batch order, so
+// the frame-order wavefront of the block launch is kept, but a warp whose
+// rays end early takes new work at once instead of holding its block's slot
+// until the block's slowest warp ends, and no SM idles through a tail of
+// late-launched blocks (ncu r01, config 2: achieved occupancy 54 % of a 62.5 %
+// limit, SMs active 89 %).  Same init / walk / epilogue code (walk_ray), so
+// results are identical.  *next must be 0 at launch.
+template <int L, bool kClamp>
+__global__ void __launch_bounds__(kCastBlock, TB_CAST_MIN_BLOCKS) cast_dyn_kernel(
+    MeshView m, int64_t n, const float* __restrict__ o, const float* __restrict__ d,
+    const int32_t* __restrict__ start, uint8_t* __restrict__ status, int32_t* __restrict__ cf,
+    int32_t* __restrict__ tet, int32_t* __restrict__ visited, int32_t* __restrict__ triangle, double* __restrict__ t,
+    int32_t* __restrict__ tet_back, unsigned long long* __restrict__ next) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(next, 32ull);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  while (base < (unsigned long long)n) {
+    unsigned long long ahead = 0;
+    if (lane == 0) ahead = atomicAdd(next, 32ull);  // the next chunk, fetched while this one walks
+    const int64_t r = (int64_t)base + lane;
+    if (r < n) {
+      uint32_t cur = (uint32_t)__ldg(start + r);
+      const float o0 = __ldg(o + 3 * r), o1 = __ldg(o + 3 * r + 1), o2 = __ldg(o + 3 * r + 2);
+      const float d0 = __ldg(d + 3 * r), d1 = __ldg(d + 3 * r + 1), d2 = __ldg(d + 3 * r + 2);
+      uint32_t ref;
+      int vis;
+      uint8_t st;
+      walk_ray<L, kClamp>(m, o0, o1, o2, d0, d1, d2, cur, ref, vis, st);
+      write_result(m, r, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
+                   tet_back);
+    }
+    base = __shfl_sync(0xffffffffu, ahead, 0);
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -1147,6 +1202,33 @@ struct CastBinnedL {
   }
 };
 
+template <int L>
+struct CastDynL {
+  // grid: one full wave of resident blocks (fewer for small batches)
+  template <typename... A>
+  static void launch(int64_t n, cudaStream_t s, bool safe, A... a) {
+    static int per_sm[2] = {0, 0}, sms = 0;
+    const bool nc = safe && L != 80;
+    if (per_sm[nc] == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (nc)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], cast_dyn_kernel<L, false>, kCastBlock, 0);
+      else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], cast_dyn_kernel<L, true>, kCastBlock, 0);
+      if (per_sm[nc] < 1) per_sm[nc] = 1;
+    }
+    const int64_t full = (int64_t)per_sm[nc] * sms;
+    const int64_t need = (n + kCastBlock - 1) / kCastBlock;
+    const unsigned g = (unsigned)(need < full ? need : full);
+    if (nc)
+      cast_dyn_kernel<L, false><<<g, kCastBlock, 0, s>>>(a...);
+    else
+      cast_dyn_kernel<L, true><<<g, kCastBlock, 0, s>>>(a...);
+  }
+};
+
 // Stream-ordered scratch from a per-device pool that keeps its memory
 // between calls (the default pool returns it to the driver at every
 // synchronisation, turning each call into a fresh cudaMalloc).
@@ -1194,14 +1276,15 @@ struct CastPersistL {
 
 // TETB200_SCHED: 0 = auto, 1 = one ray per lane (cast_kernel), 2 = persistent
 // refill (cast_persist_kernel), 3 / 4 = block compaction with 256 / 512
-// threads (cast_compact_kernel).  TETB200_ROUND: steps per compaction round.
+// threads (cast_compact_kernel), 5 = dynamic warp chunks (cast_dyn_kernel),
+// 6 = direction-binned.  TETB200_ROUND: steps per compaction round.
 std::atomic<int> g_sched_mode{-1}, g_round_steps{-1};
 int sched_mode() {
   int mode = g_sched_mode.load(std::memory_order_relaxed);
   if (mode < 0) {
     const char* v = getenv("TETB200_SCHED");
     mode = v ? atoi(v) : 0;
-    if (mode < 0 || mode > 6 || mode == 5) mode = 0;
+    if (mode < 0 || mode > 6) mode = 0;
     int expect = -1;
     g_sched_mode.compare_exchange_strong(expect, mode);
     mode = g_sched_mode.load();
@@ -1381,6 +1464,22 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
     if (oidx) compose_index_kernel<<<grid_for(n, 256), 256, 0, s>>>(perm, oidx, n, widx);
     e = launch_layout<CastBinnedL>(m->layout, grid_for(n, kCastBlock), s, m->safe, perm, widx, v, n, o, d, start,
                                    status, cf, tet, visited, triangle, t, tet_back);
+    cudaFreeAsync(scratch, s);
+  } else if (mode == 5 && !host_rays) {
+    char* scratch = nullptr;
+    if (int e2 = scratch_alloc(m->device, 256, s, &scratch)) return e2;
+    unsigned long long* next = reinterpret_cast<unsigned long long*>(scratch);
+    if (cudaError_t me = cudaMemsetAsync(next, 0, sizeof(*next), s)) {
+      cudaFreeAsync(scratch, s);
+      return set_error(TB_E_CUDA, "dynamic schedule counter: %s", cudaGetErrorString(me));
+    }
+    switch (m->layout) {
+      case 16: CastDynL<16>::launch(n, s, m->safe, v, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, next); break;
+      case 20: CastDynL<20>::launch(n, s, m->safe, v, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, next); break;
+      case 32: CastDynL<32>::launch(n, s, m->safe, v, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, next); break;
+      case 80: CastDynL<80>::launch(n, s, m->safe, v, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, next); break;
+      default: e = set_error(TB_E_LAYOUT, "unsupported layout %d", m->layout);
+    }
     cudaFreeAsync(scratch, s);
   } else if (mode == 2) {
     e = launch_layout<CastPersistL>(m->layout, grid_for(n, kBlock), s, v, n, o, d, start, status, cf, tet, visited,
@@ -1665,8 +1764,7 @@ int tb_cast_rays_scatter_sched(tb_mesh* m, int64_t n, const float* o, const floa
                                int32_t* triangle, double* t, int32_t* tet_back, int schedule, void* stream) {
   if (int e = check_mesh(m)) return e;
   if (n < 0) return set_error(TB_E_ARG, "negative ray count");
-  if (schedule < 0 || schedule > 6 || schedule == 5)
-    return set_error(TB_E_ARG, "schedule %d not in 0..4 or 6", schedule);
+  if (schedule < 0 || schedule > 6) return set_error(TB_E_ARG, "schedule %d not in 0..6", schedule);
   if (n == 0) return TB_OK;
   if (!o || !d || !start || !out_index || !status || !cf || !tet || !visited)
     return set_error(TB_E_ARG, "NULL ray buffer");
@@ -1887,8 +1985,7 @@ int tb_cast_rays_sched(tb_mesh* m, int64_t n, const float* o, const float* d, co
                        int32_t* tet_back, int schedule, void* stream) {
   if (int e = check_mesh(m)) return e;
   if (n < 0) return set_error(TB_E_ARG, "negative ray count");
-  if (schedule < 0 || schedule > 6 || schedule == 5)
-    return set_error(TB_E_ARG, "schedule %d not in 0..4 or 6", schedule);
+  if (schedule < 0 || schedule > 6) return set_error(TB_E_ARG, "schedule %d not in 0..6", schedule);
   if (n == 0) return TB_OK;
   if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
   return cast_dispatch(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, (cudaStream_t)stream,
@@ -1981,35 +2078,96 @@ int tb_shadow_rays(tb_mesh* m, int64_t n, const double* p, const double* light, 
 }
 
 // ----------------------------------------------------------------------------
-// Host-buffer entry points: stage -> launch -> copy back -> synchronise, on a
-// private stream with stream-ordered scratch (reentrant per host thread).
+// Host-buffer entry points (what the kernel-module protocol calls: numpy
+// arrays in, numpy arrays out).  Streams and staging come from a
+// process-wide pool of slots per device, checked out per call and returned
+// after it -- never owned by a host thread -- so a renderer whose tile pool
+// creates and joins threads every frame (render.py:538-541) pays no
+// per-thread allocation, stream creation or implicit device synchronisation
+// at thread exit (r01's per-thread contexts made 256..65536-ray calls 2-3x
+// slower than the CPU reference; bench small_batch).  Pageable buffers are
+// staged through the slot's pinned, mapped host memory and the kernels read
+// and write that memory over PCIe themselves: one launch and one sync per
+// chunk, chunks double-buffered so host memcpy overlaps the GPU.
 }  // extern "C"
 namespace {
-struct HostCall {
+
+inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+struct HostSlot {
+  int device = -1;
   cudaStream_t s = nullptr;
-  char* base = nullptr;
-  size_t off = 0;
-  ~HostCall() {
-    if (base) cudaFreeAsync(base, s);
-    if (s) {
+  char* h = nullptr;   // pinned, mapped host staging
+  char* hd = nullptr;  // its device alias
+  size_t h_bytes = 0;
+  int host(size_t b) {
+    if (h_bytes >= b) return TB_OK;
+    if (h) {
       cudaStreamSynchronize(s);
-      cudaStreamDestroy(s);
+      cudaFreeHost(h);
+    }
+    h = hd = nullptr;
+    h_bytes = 0;
+    const size_t want = std::max(b, (size_t)1 << 20);
+    TB_CUDA(cudaHostAlloc((void**)&h, want, cudaHostAllocMapped | cudaHostAllocPortable));
+    if (cudaError_t e = cudaHostGetDevicePointer((void**)&hd, h, 0)) {
+      cudaFreeHost(h);
+      h = nullptr;
+      return set_error(TB_E_CUDA, "mapped staging: %s", cudaGetErrorString(e));
+    }
+    h_bytes = want;
+    return TB_OK;
+  }
+  // device alias of a pointer into h
+  template <typename T>
+  T* dev(T* p) const { return reinterpret_cast<T*>(hd + (reinterpret_cast<char*>(p) - h)); }
+};
+
+std::mutex g_slot_mu;
+std::vector<HostSlot*> g_free_slots[64];
+
+int slot_get(int device, HostSlot** out) {
+  if (device < 0 || device >= 64) return set_error(TB_E_ARG, "device %d out of range", device);
+  {
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    if (!g_free_slots[device].empty()) {
+      *out = g_free_slots[device].back();
+      g_free_slots[device].pop_back();
+      return TB_OK;
     }
   }
-  static size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
-  template <typename T>
-  T* take(size_t count) {
-    T* p = reinterpret_cast<T*>(base + off);
-    off += al(count * sizeof(T));
-    return p;
+  HostSlot* sl = new HostSlot();
+  sl->device = device;
+  DeviceGuard g(device);
+  if (cudaError_t e = cudaStreamCreateWithFlags(&sl->s, cudaStreamNonBlocking)) {
+    delete sl;
+    return set_error(TB_E_CUDA, "host-path stream: %s", cudaGetErrorString(e));
+  }
+  *out = sl;
+  return TB_OK;
+}
+
+// Returns the slot to the pool after draining its stream (error paths
+// included: nothing queued may still touch the staging afterwards).
+struct SlotLease {
+  HostSlot* p = nullptr;
+  SlotLease() = default;
+  SlotLease(const SlotLease&) = delete;
+  SlotLease& operator=(const SlotLease&) = delete;
+  ~SlotLease() {
+    if (!p) return;
+    cudaStreamSynchronize(p->s);
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    g_free_slots[p->device].push_back(p);
   }
 };
 
-// Per-thread, per-device pipeline context for tb_cast_rays_host: streams and
-// device staging buffers are created once and reused by every call.
+// Device-staged copy pipeline (TETB200_E2E=1 only: an A/B knob against the
+// zero-copy path): three streams, each with HBM staging for one chunk.
 struct PipeCtx {
   static constexpr int kStreams = 3;
   static constexpr int64_t kChunk = 1 << 18;  // rays per pipeline chunk
+  int device = -1;
   struct Slot {
     cudaStream_t s = nullptr;
     char* base = nullptr;
@@ -2018,6 +2176,62 @@ struct PipeCtx {
     uint8_t* status = nullptr;
     double* t = nullptr;
   } slot[kStreams];
+};
+
+std::vector<PipeCtx*> g_free_pipes[64];
+
+int pipe_get(int device, PipeCtx** out) {
+  if (device < 0 || device >= 64) return set_error(TB_E_ARG, "device %d out of range", device);
+  {
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    if (!g_free_pipes[device].empty()) {
+      *out = g_free_pipes[device].back();
+      g_free_pipes[device].pop_back();
+      return TB_OK;
+    }
+  }
+  PipeCtx* c = new PipeCtx();
+  c->device = device;
+  const size_t k = (size_t)PipeCtx::kChunk;
+  for (int i = 0; i < PipeCtx::kStreams; ++i) {
+    PipeCtx::Slot& sl = c->slot[i];
+    cudaError_t e = cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking);
+    const size_t total = al256(k * 12) * 2 + al256(k * 4) * 6 + al256(k) + al256(k * 8);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&sl.base, total);
+    if (e != cudaSuccess) {
+      for (PipeCtx::Slot& x : c->slot) {
+        if (x.s) cudaStreamDestroy(x.s);
+        if (x.base) cudaFree(x.base);
+      }
+      delete c;
+      return set_error(e == cudaErrorMemoryAllocation ? TB_E_OOM : TB_E_CUDA, "host-path staging: %s",
+                       cudaGetErrorString(e));
+    }
+    char* p = sl.base;
+    auto take = [&](size_t bytes) { char* q = p; p += al256(bytes); return q; };
+    sl.o = reinterpret_cast<float*>(take(k * 12));
+    sl.d = reinterpret_cast<float*>(take(k * 12));
+    sl.st = reinterpret_cast<int32_t*>(take(k * 4));
+    sl.status = reinterpret_cast<uint8_t*>(take(k));
+    sl.cf = reinterpret_cast<int32_t*>(take(k * 4));
+    sl.tet = reinterpret_cast<int32_t*>(take(k * 4));
+    sl.vis = reinterpret_cast<int32_t*>(take(k * 4));
+    sl.tri = reinterpret_cast<int32_t*>(take(k * 4));
+    sl.t = reinterpret_cast<double*>(take(k * 8));
+    sl.back = reinterpret_cast<int32_t*>(take(k * 4));
+  }
+  *out = c;
+  return TB_OK;
+}
+
+struct PipeLease {
+  PipeCtx* p = nullptr;
+  ~PipeLease() {
+    if (!p) return;
+    for (PipeCtx::Slot& sl : p->slot) cudaStreamSynchronize(sl.s);
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    g_free_pipes[p->device].push_back(p);
+  }
 };
 
 // Device address of a mapped pinned host buffer (false for pageable memory).
@@ -2032,75 +2246,41 @@ bool mapped_ptr(const void* p, void** dev) {
   return true;
 }
 
-// TETB200_E2E: 0 = auto (zero-copy when all host buffers are mapped pinned),
-// 1 = always stage through device buffers.
+// TETB200_E2E: 0 = auto (zero-copy: mapped pinned buffers directly, pageable
+// ones through pinned staging), 1 = the device-staged copy pipeline.
 int e2e_mode() {
   const char* v = getenv("TETB200_E2E");
   return v ? atoi(v) : 0;
 }
 
-void free_pipe_ctx(PipeCtx* c, int device) {
-  if (!c) return;
-  int prev = -1;
-  cudaGetDevice(&prev);
-  cudaSetDevice(device);
-  for (PipeCtx::Slot& sl : c->slot) {
-    if (sl.s) {
-      cudaStreamSynchronize(sl.s);
-      cudaStreamDestroy(sl.s);
-    }
-    if (sl.base) cudaFree(sl.base);
-  }
-  if (prev >= 0) cudaSetDevice(prev);
-  cudaGetLastError();  // teardown errors (e.g. runtime already unloading) are not reportable here
-  delete c;
-}
+// Rays per pinned staging chunk for pageable buffers (double-buffered).
+constexpr int64_t kHostChunk = 1 << 17;
 
-// Per host thread and device: the chunked host path's 3 streams and HBM
-// staging (~44 MB), created on first use and released when the thread exits
-// (renderer tile pools come and go).
-struct PipeCtxSet {
-  PipeCtx* ctxs[64] = {nullptr};
-  ~PipeCtxSet() {
-    for (int dv = 0; dv < 64; ++dv) free_pipe_ctx(ctxs[dv], dv);
+// Per-ray staging of one cast chunk of C rays in a slot's pinned memory.
+struct CastStage {
+  float *o, *d;
+  int32_t* st;
+  uint8_t* status;
+  int32_t *cf, *tet, *vis, *tri, *back;
+  double* t;
+  static size_t bytes(size_t C) {
+    return al256(C * 12) * 2 + al256(C * 4) * 6 + al256(C) + al256(C * 8);
+  }
+  CastStage(char* base, size_t C) {
+    char* p = base;
+    auto take = [&](size_t b) { char* q = p; p += al256(b); return q; };
+    o = reinterpret_cast<float*>(take(C * 12));
+    d = reinterpret_cast<float*>(take(C * 12));
+    st = reinterpret_cast<int32_t*>(take(C * 4));
+    status = reinterpret_cast<uint8_t*>(take(C));
+    cf = reinterpret_cast<int32_t*>(take(C * 4));
+    tet = reinterpret_cast<int32_t*>(take(C * 4));
+    vis = reinterpret_cast<int32_t*>(take(C * 4));
+    tri = reinterpret_cast<int32_t*>(take(C * 4));
+    t = reinterpret_cast<double*>(take(C * 8));
+    back = reinterpret_cast<int32_t*>(take(C * 4));
   }
 };
-
-int pipe_ctx(int device, PipeCtx** out) {
-  static thread_local PipeCtxSet set;
-  if (device < 0 || device >= 64) return set_error(TB_E_ARG, "device %d out of range", device);
-  if (set.ctxs[device] == nullptr) {
-    PipeCtx* c = new PipeCtx();
-    const size_t k = (size_t)PipeCtx::kChunk;
-    for (int i = 0; i < PipeCtx::kStreams; ++i) {
-      PipeCtx::Slot& sl = c->slot[i];
-      cudaError_t e = cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking);
-      const size_t total = HostCall::al(k * 12) * 2 + HostCall::al(k * 4) * 6 + HostCall::al(k) + HostCall::al(k * 8);
-      if (e == cudaSuccess) e = cudaMalloc((void**)&sl.base, total);
-      if (e != cudaSuccess) {
-        free_pipe_ctx(c, device);
-        return set_error(e == cudaErrorMemoryAllocation ? TB_E_OOM : TB_E_CUDA, "host-path staging: %s",
-                         cudaGetErrorString(e));
-      }
-      HostCall hc;  // reuse the bump allocator arithmetic
-      hc.base = sl.base;
-      sl.o = hc.take<float>(k * 3);
-      sl.d = hc.take<float>(k * 3);
-      sl.st = hc.take<int32_t>(k);
-      sl.status = hc.take<uint8_t>(k);
-      sl.cf = hc.take<int32_t>(k);
-      sl.tet = hc.take<int32_t>(k);
-      sl.vis = hc.take<int32_t>(k);
-      sl.tri = hc.take<int32_t>(k);
-      sl.t = hc.take<double>(k);
-      sl.back = hc.take<int32_t>(k);
-      hc.base = nullptr;  // owned by the slot, not freed by ~HostCall
-    }
-    set.ctxs[device] = c;
-  }
-  *out = set.ctxs[device];
-  return TB_OK;
-}
 
 }  // namespace
 
@@ -2110,8 +2290,7 @@ extern "C" {
 
 namespace {
 
-// Host-buffer traversal (both walks): zero-copy when every buffer is mapped
-// pinned memory, else a chunked 3-stream copy/trace pipeline.
+// Host-buffer traversal (both walks).
 int cast_host(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start, uint8_t* status,
               int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back,
               bool sctp) {
@@ -2120,8 +2299,6 @@ int cast_host(tb_mesh* m, int64_t n, const float* o, const float* d, const int32
   if (n == 0) return TB_OK;
   if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
   DeviceGuard g(m->device);
-  PipeCtx* ctx = nullptr;
-  if (int e = pipe_ctx(m->device, &ctx)) return e;
   const int mode = e2e_mode();
   // Host batches run one ray per lane unless a schedule is set: the walk
   // hides under PCIe time here, and the zero-copy path depends on
@@ -2146,60 +2323,100 @@ int cast_host(tb_mesh* m, int64_t n, const float* o, const float* d, const int32
                            (!t || mapped_ptr(t, &dT)) && (!tet_back || mapped_ptr(tet_back, &dBack));
   const bool ins_mapped = mapped_ptr(o, &dO) && mapped_ptr(d, &dD) && mapped_ptr(start, &dS);
   if (mode == 0 && outs_mapped && ins_mapped) {
-    const cudaStream_t s = ctx->slot[0].s;
+    SlotLease L;
+    if (int e = slot_get(m->device, &L.p)) return e;
     if (int e = launch(n, (const float*)dO, (const float*)dD, (const int32_t*)dS, (uint8_t*)dSt, (int32_t*)dCf,
-                       (int32_t*)dTet, (int32_t*)dVis, (int32_t*)dTri, (double*)dT, (int32_t*)dBack, s, true))
+                       (int32_t*)dTet, (int32_t*)dVis, (int32_t*)dTri, (double*)dT, (int32_t*)dBack, L.p->s, true))
       return e;
-    TB_CUDA(cudaStreamSynchronize(s));
+    TB_CUDA(cudaStreamSynchronize(L.p->s));
     return TB_OK;
   }
-  // Chunked 3-stream pipeline: chunk c's H2D, kernel and D2H are ordered on
-  // stream c % 3, so copies of one chunk overlap the trace of the previous
-  // one and the D2H of the one before (H2D and D2H use separate copy engines).
+  if (mode == 0) {
+    // Pageable buffers: chunks staged through pinned, mapped slots (two,
+    // alternating, when the batch spans several chunks) -- the caller's
+    // thread copies chunk c in while the GPU walks chunk c-1 straight from
+    // / into the other slot's pinned memory.
+    const int64_t C = n < kHostChunk ? n : kHostChunk;
+    const int k = n > C ? 2 : 1;
+    SlotLease L[2];
+    for (int i = 0; i < k; ++i) {
+      if (int e = slot_get(m->device, &L[i].p)) return e;
+      if (int e = L[i].p->host(CastStage::bytes((size_t)C))) return e;
+    }
+    int64_t c_start[2] = {-1, -1}, c_len[2] = {0, 0};
+    auto drain = [&](int i) -> int {
+      if (c_start[i] < 0) return TB_OK;
+      TB_CUDA(cudaStreamSynchronize(L[i].p->s));
+      const CastStage v(L[i].p->h, (size_t)C);
+      const int64_t a = c_start[i];
+      const size_t len = (size_t)c_len[i];
+      memcpy(status + a, v.status, len);
+      memcpy(cf + a, v.cf, len * 4);
+      memcpy(tet + a, v.tet, len * 4);
+      memcpy(visited + a, v.vis, len * 4);
+      if (triangle) memcpy(triangle + a, v.tri, len * 4);
+      if (t) memcpy(t + a, v.t, len * 8);
+      if (tet_back) memcpy(tet_back + a, v.back, len * 4);
+      c_start[i] = -1;
+      return TB_OK;
+    };
+    for (int64_t c0 = 0, c = 0; c0 < n; c0 += C, ++c) {
+      const int i = (int)(c % k);
+      if (int e = drain(i)) return e;
+      const int64_t len = (n - c0 < C) ? (n - c0) : C;
+      HostSlot& sl = *L[i].p;
+      const CastStage v(sl.h, (size_t)C);
+      memcpy(v.o, o + 3 * c0, (size_t)len * 12);
+      memcpy(v.d, d + 3 * c0, (size_t)len * 12);
+      memcpy(v.st, start + c0, (size_t)len * 4);
+      if (int e = launch(len, sl.dev(v.o), sl.dev(v.d), sl.dev(v.st), sl.dev(v.status), sl.dev(v.cf), sl.dev(v.tet),
+                         sl.dev(v.vis), triangle ? sl.dev(v.tri) : nullptr, t ? sl.dev(v.t) : nullptr,
+                         tet_back ? sl.dev(v.back) : nullptr, sl.s, true))
+        return e;
+      c_start[i] = c0;
+      c_len[i] = len;
+    }
+    for (int i = 0; i < k; ++i)
+      if (int e = drain(i)) return e;
+    return TB_OK;
+  }
+  // TETB200_E2E=1: chunked 3-stream copy pipeline through HBM staging --
+  // chunk c's H2D, kernel and D2H are ordered on stream c % 3, so copies of
+  // one chunk overlap the trace of the previous one (an A/B knob; r01 chose
+  // zero copy).
+  PipeLease P;
+  if (int e = pipe_get(m->device, &P.p)) return e;
+  PipeCtx* ctx = P.p;
   int64_t chunk = PipeCtx::kChunk;
   if (const char* v = getenv("TETB200_CHUNK")) {  // experiment knob: rays per chunk (<= kChunk)
     const int64_t c = atoll(v);
     if (c > 0 && c < chunk) chunk = c;
   }
-  // on any failure, drain the slot streams before returning so no queued copy
-  // still touches the caller's buffers afterwards
-  auto drain = [&](int code) {
-    for (int i = 0; i < PipeCtx::kStreams; ++i) cudaStreamSynchronize(ctx->slot[i].s);
-    return code;
-  };
-#define TB_CUDA_DRAIN(call)                                                                             \
-  do {                                                                                                  \
-    cudaError_t e_ = (call);                                                                            \
-    if (e_ != cudaSuccess) return drain(set_error(TB_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_))); \
+#define TB_CUDA_PIPE(call)                                                                          \
+  do {                                                                                              \
+    cudaError_t e_ = (call);                                                                        \
+    if (e_ != cudaSuccess) return set_error(TB_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
   } while (0)
   for (int64_t c0 = 0, c = 0; c0 < n; c0 += chunk, ++c) {
     const int64_t k = (n - c0 < chunk) ? (n - c0) : chunk;
     const size_t uk = (size_t)k;
     PipeCtx::Slot& sl = ctx->slot[c % PipeCtx::kStreams];
     const cudaStream_t s = sl.s;
-    TB_CUDA_DRAIN(cudaMemcpyAsync(sl.o, o + 3 * c0, uk * 12, cudaMemcpyHostToDevice, s));
-    TB_CUDA_DRAIN(cudaMemcpyAsync(sl.d, d + 3 * c0, uk * 12, cudaMemcpyHostToDevice, s));
-    TB_CUDA_DRAIN(cudaMemcpyAsync(sl.st, start + c0, uk * 4, cudaMemcpyHostToDevice, s));
-    if (outs_mapped && mode == 2) {
-      // inputs by copy engine, hits written by the kernel straight to host
-      if (int e = launch(k, sl.o, sl.d, sl.st, (uint8_t*)dSt + c0, (int32_t*)dCf + c0, (int32_t*)dTet + c0,
-                         (int32_t*)dVis + c0, dTri ? (int32_t*)dTri + c0 : nullptr, dT ? (double*)dT + c0 : nullptr,
-                         dBack ? (int32_t*)dBack + c0 : nullptr, s, false))
-        return drain(e);
-      continue;
-    }
+    TB_CUDA_PIPE(cudaMemcpyAsync(sl.o, o + 3 * c0, uk * 12, cudaMemcpyHostToDevice, s));
+    TB_CUDA_PIPE(cudaMemcpyAsync(sl.d, d + 3 * c0, uk * 12, cudaMemcpyHostToDevice, s));
+    TB_CUDA_PIPE(cudaMemcpyAsync(sl.st, start + c0, uk * 4, cudaMemcpyHostToDevice, s));
     if (int e = launch(k, sl.o, sl.d, sl.st, sl.status, sl.cf, sl.tet, sl.vis, triangle ? sl.tri : nullptr,
                        t ? sl.t : nullptr, tet_back ? sl.back : nullptr, s, false))
-      return drain(e);
-    TB_CUDA_DRAIN(cudaMemcpyAsync(status + c0, sl.status, uk, cudaMemcpyDeviceToHost, s));
-    TB_CUDA_DRAIN(cudaMemcpyAsync(cf + c0, sl.cf, uk * 4, cudaMemcpyDeviceToHost, s));
-    TB_CUDA_DRAIN(cudaMemcpyAsync(tet + c0, sl.tet, uk * 4, cudaMemcpyDeviceToHost, s));
-    TB_CUDA_DRAIN(cudaMemcpyAsync(visited + c0, sl.vis, uk * 4, cudaMemcpyDeviceToHost, s));
-    if (triangle) TB_CUDA_DRAIN(cudaMemcpyAsync(triangle + c0, sl.tri, uk * 4, cudaMemcpyDeviceToHost, s));
-    if (t) TB_CUDA_DRAIN(cudaMemcpyAsync(t + c0, sl.t, uk * 8, cudaMemcpyDeviceToHost, s));
-    if (tet_back) TB_CUDA_DRAIN(cudaMemcpyAsync(tet_back + c0, sl.back, uk * 4, cudaMemcpyDeviceToHost, s));
+      return e;
+    TB_CUDA_PIPE(cudaMemcpyAsync(status + c0, sl.status, uk, cudaMemcpyDeviceToHost, s));
+    TB_CUDA_PIPE(cudaMemcpyAsync(cf + c0, sl.cf, uk * 4, cudaMemcpyDeviceToHost, s));
+    TB_CUDA_PIPE(cudaMemcpyAsync(tet + c0, sl.tet, uk * 4, cudaMemcpyDeviceToHost, s));
+    TB_CUDA_PIPE(cudaMemcpyAsync(visited + c0, sl.vis, uk * 4, cudaMemcpyDeviceToHost, s));
+    if (triangle) TB_CUDA_PIPE(cudaMemcpyAsync(triangle + c0, sl.tri, uk * 4, cudaMemcpyDeviceToHost, s));
+    if (t) TB_CUDA_PIPE(cudaMemcpyAsync(t + c0, sl.t, uk * 8, cudaMemcpyDeviceToHost, s));
+    if (tet_back) TB_CUDA_PIPE(cudaMemcpyAsync(tet_back + c0, sl.back, uk * 4, cudaMemcpyDeviceToHost, s));
   }
-#undef TB_CUDA_DRAIN
+#undef TB_CUDA_PIPE
   for (int i = 0; i < PipeCtx::kStreams; ++i) TB_CUDA(cudaStreamSynchronize(ctx->slot[i].s));
   return TB_OK;
 }
@@ -2220,26 +2437,34 @@ int tb_sctp_cast_rays_host(tb_mesh* m, int64_t n, const float* o, const float* d
   return cast_host(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, true);
 }
 
+// Point location / shadow rays on host buffers: the same pooled slots, inputs
+// memcpy'd into pinned mapped staging, the kernel reading and writing it over
+// PCIe, one launch + one sync per chunk (renderers call these per tile).
 int tb_locate_points_host(tb_mesh* m, int64_t n, const double* q, const int32_t* hints, int32_t* tet,
                           int32_t* visited) {
   if (int e = check_mesh(m)) return e;
   if (n < 0) return set_error(TB_E_ARG, "negative point count");
   if (n == 0) return TB_OK;
+  if (!q || !hints || !tet || !visited) return set_error(TB_E_ARG, "NULL buffer");
   DeviceGuard g(m->device);
-  HostCall hc;
-  TB_CUDA(cudaStreamCreateWithFlags(&hc.s, cudaStreamNonBlocking));
-  const size_t un = (size_t)n;
-  TB_CUDA(cudaMallocAsync((void**)&hc.base, HostCall::al(un * 24) + HostCall::al(un * 4) * 3, hc.s));
-  double* dQ = hc.take<double>(un * 3);
-  int32_t* dH = hc.take<int32_t>(un);
-  int32_t* dT = hc.take<int32_t>(un);
-  int32_t* dV = hc.take<int32_t>(un);
-  TB_CUDA(cudaMemcpyAsync(dQ, q, un * 24, cudaMemcpyHostToDevice, hc.s));
-  TB_CUDA(cudaMemcpyAsync(dH, hints, un * 4, cudaMemcpyHostToDevice, hc.s));
-  if (int e = tb_locate_points(m, n, dQ, dH, dT, dV, hc.s)) return e;
-  TB_CUDA(cudaMemcpyAsync(tet, dT, un * 4, cudaMemcpyDeviceToHost, hc.s));
-  TB_CUDA(cudaMemcpyAsync(visited, dV, un * 4, cudaMemcpyDeviceToHost, hc.s));
-  TB_CUDA(cudaStreamSynchronize(hc.s));
+  SlotLease L;
+  if (int e = slot_get(m->device, &L.p)) return e;
+  const size_t C = (size_t)(n < kHostChunk ? n : kHostChunk);
+  if (int e = L.p->host(al256(C * 24) + al256(C * 4) * 3)) return e;
+  HostSlot& sl = *L.p;
+  double* hq = reinterpret_cast<double*>(sl.h);
+  int32_t* hh = reinterpret_cast<int32_t*>(sl.h + al256(C * 24));
+  int32_t* ht = reinterpret_cast<int32_t*>(sl.h + al256(C * 24) + al256(C * 4));
+  int32_t* hv = reinterpret_cast<int32_t*>(sl.h + al256(C * 24) + al256(C * 4) * 2);
+  for (int64_t c0 = 0; c0 < n; c0 += (int64_t)C) {
+    const size_t len = (size_t)((n - c0 < (int64_t)C) ? (n - c0) : (int64_t)C);
+    memcpy(hq, q + 3 * c0, len * 24);
+    memcpy(hh, hints + c0, len * 4);
+    if (int e = tb_locate_points(m, (int64_t)len, sl.dev(hq), sl.dev(hh), sl.dev(ht), sl.dev(hv), sl.s)) return e;
+    TB_CUDA(cudaStreamSynchronize(sl.s));
+    memcpy(tet + c0, ht, len * 4);
+    memcpy(visited + c0, hv, len * 4);
+  }
   return TB_OK;
 }
 
@@ -2249,36 +2474,48 @@ int tb_shadow_rays_host(tb_mesh* m, int64_t n, const double* p, const double* li
   if (int e = check_mesh(m)) return e;
   if (n < 0) return set_error(TB_E_ARG, "negative ray count");
   if (n == 0) return TB_OK;
+  if (!p || !light || !p_tet || !light_tet || !occluded || !visited) return set_error(TB_E_ARG, "NULL buffer");
   if ((light_stride != 0 && light_stride != 3) || (light_tet_stride != 0 && light_tet_stride != 1))
     return set_error(TB_E_ARG, "bad light strides %d/%d", light_stride, light_tet_stride);
   DeviceGuard g(m->device);
-  HostCall hc;
-  TB_CUDA(cudaStreamCreateWithFlags(&hc.s, cudaStreamNonBlocking));
-  const size_t un = (size_t)n;
-  const size_t nl = light_stride ? un : 1, nlt = light_tet_stride ? un : 1;
-  TB_CUDA(cudaMallocAsync((void**)&hc.base,
-                          HostCall::al(un * 24) + HostCall::al(nl * 24) + HostCall::al(un * 4) * 2 +
-                              HostCall::al(nlt * 4) + HostCall::al(un),
-                          hc.s));
-  double* dP = hc.take<double>(un * 3);
-  double* dL = hc.take<double>(nl * 3);
-  int32_t* dPT = hc.take<int32_t>(un);
-  int32_t* dLT = hc.take<int32_t>(nlt);
-  uint8_t* dOcc = hc.take<uint8_t>(un);
-  int32_t* dV = hc.take<int32_t>(un);
-  TB_CUDA(cudaMemcpyAsync(dP, p, un * 24, cudaMemcpyHostToDevice, hc.s));
-  TB_CUDA(cudaMemcpyAsync(dL, light, nl * 24, cudaMemcpyHostToDevice, hc.s));
-  TB_CUDA(cudaMemcpyAsync(dPT, p_tet, un * 4, cudaMemcpyHostToDevice, hc.s));
-  TB_CUDA(cudaMemcpyAsync(dLT, light_tet, nlt * 4, cudaMemcpyHostToDevice, hc.s));
-  if (int e = tb_shadow_rays(m, n, dP, dL, light_stride, dPT, dLT, light_tet_stride, eps, dOcc, dV, hc.s)) return e;
-  TB_CUDA(cudaMemcpyAsync(occluded, dOcc, un, cudaMemcpyDeviceToHost, hc.s));
-  TB_CUDA(cudaMemcpyAsync(visited, dV, un * 4, cudaMemcpyDeviceToHost, hc.s));
-  TB_CUDA(cudaStreamSynchronize(hc.s));
+  SlotLease L;
+  if (int e = slot_get(m->device, &L.p)) return e;
+  const size_t C = (size_t)(n < kHostChunk ? n : kHostChunk);
+  const size_t CL = light_stride ? C : 1, CLT = light_tet_stride ? C : 1;
+  if (int e = L.p->host(al256(C * 24) + al256(CL * 24) + al256(C * 4) * 2 + al256(CLT * 4) + al256(C))) return e;
+  HostSlot& sl = *L.p;
+  char* b = sl.h;
+  double* hp = reinterpret_cast<double*>(b);
+  b += al256(C * 24);
+  double* hl = reinterpret_cast<double*>(b);
+  b += al256(CL * 24);
+  int32_t* hpt = reinterpret_cast<int32_t*>(b);
+  b += al256(C * 4);
+  int32_t* hlt = reinterpret_cast<int32_t*>(b);
+  b += al256(CLT * 4);
+  int32_t* hv = reinterpret_cast<int32_t*>(b);
+  b += al256(C * 4);
+  uint8_t* ho = reinterpret_cast<uint8_t*>(b);
+  if (!light_stride) memcpy(hl, light, 24);
+  if (!light_tet_stride) memcpy(hlt, light_tet, 4);
+  for (int64_t c0 = 0; c0 < n; c0 += (int64_t)C) {
+    const size_t len = (size_t)((n - c0 < (int64_t)C) ? (n - c0) : (int64_t)C);
+    memcpy(hp, p + 3 * c0, len * 24);
+    memcpy(hpt, p_tet + c0, len * 4);
+    if (light_stride) memcpy(hl, light + 3 * c0, len * 24);
+    if (light_tet_stride) memcpy(hlt, light_tet + c0, len * 4);
+    if (int e = tb_shadow_rays(m, (int64_t)len, sl.dev(hp), sl.dev(hl), light_stride, sl.dev(hpt), sl.dev(hlt),
+                               light_tet_stride, eps, sl.dev(ho), sl.dev(hv), sl.s))
+      return e;
+    TB_CUDA(cudaStreamSynchronize(sl.s));
+    memcpy(occluded + c0, ho, len);
+    memcpy(visited + c0, hv, len * 4);
+  }
   return TB_OK;
 }
 
 int tb_set_schedule(int mode, int steps_per_round) {
-  if (mode > 6 || mode == 5) return set_error(TB_E_ARG, "schedule mode %d not in 0..4 or 6", mode);
+  if (mode > 6) return set_error(TB_E_ARG, "schedule mode %d not in 0..6", mode);
   if (steps_per_round == 0) return set_error(TB_E_ARG, "steps_per_round must be >= 1");
   if (mode >= 0) g_sched_mode.store(mode);
   if (steps_per_round > 0) g_round_steps.store(steps_per_round);

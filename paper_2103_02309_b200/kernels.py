@@ -72,7 +72,19 @@ def cast_rays_full(mesh, o32, d32, start, *, layout: str | None = None, sctp: bo
                addr(triangle), addr(t), addr(back)),
             "tb_sctp_cast_rays_host" if sctp else "tb_cast_rays_host",
         )
+        _check_cf(dm, mesh, status, cf)
     return status, cf, tet, visited, triangle, t, back
+
+
+def _check_cf(dm, mesh, status, cf) -> None:
+    """An unvalidated (corrupt) mesh can hit a constrained ref past the cf
+    table; the kernel then skips the epilogue gathers and this raises, as the
+    reference's batch epilogue does on mesh.cf_triangle[cf] (batch.py:63)."""
+    if not dm.validated:
+        bad = np.nonzero((status == STATUS_HIT) & ((cf < 0) | (cf >= len(mesh.cf_triangle))))[0]
+        if len(bad):
+            raise IndexError(f"ray {int(bad[0])} hit constrained face {int(cf[bad[0]])}, outside the mesh's "
+                             f"{len(mesh.cf_triangle)} constrained faces")
 
 
 def cast_rays(mesh, o32, d32, start, visits_sink=None):
@@ -117,10 +129,11 @@ def emit_visits(sink: list, visited: np.ndarray, seq: np.ndarray, offsets: np.nd
 def _cast_plain(mesh, o32, d32, start):
     o, d, st = _prep_cast(mesh, o32, d32, start)
     n = len(st)
-    status = np.zeros(n, dtype=np.uint8)
-    cf = np.full(n, -1, dtype=np.int32)
-    tet = np.full(n, -1, dtype=np.int32)
-    visited = np.ones(n, dtype=np.int32)
+    # every output element is written by the kernel
+    status = np.empty(n, dtype=np.uint8)
+    cf = np.empty(n, dtype=np.int32)
+    tet = np.empty(n, dtype=np.int32)
+    visited = np.empty(n, dtype=np.int32)
     if n:
         dm = device_mesh(mesh)
         check(
