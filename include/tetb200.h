@@ -87,8 +87,11 @@ int tb_mesh_create(int device, int layout, int64_t n_points, const float* points
                    const int32_t* cf_tets, int64_t n_tri, const double* tri_coords,
                    tb_mesh** out);
 int tb_mesh_destroy(tb_mesh* mesh);
-/* Bytes of HBM the mesh occupies, and the hot "accelerator" bytes
- * (records + points, CompactMesh.accelerator_bytes, tetmesh.py:182-185). */
+/* Bytes of HBM the mesh occupies, and the hot bytes the walk gathers from on
+ * the device: records + the six axis-permuted float4 point copies (96 B per
+ * point; TetMesh-80: records only).  The reference's own accelerator count
+ * (records + 12 B points, CompactMesh.accelerator_bytes, tetmesh.py:182-185)
+ * is records + 12 * n_points. */
 int tb_mesh_info(const tb_mesh* mesh, int* device, int* layout, int64_t* n_points,
                  int64_t* n_tets, int64_t* n_cf, int64_t* hbm_bytes, int64_t* hot_bytes);
 

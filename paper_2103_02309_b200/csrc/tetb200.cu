@@ -1624,8 +1624,12 @@ int tb_mesh_create(int device, int layout, int64_t n_points, const float* points
   }
 #undef TB_MC
   m->hbm_bytes = n_points * 16 * 6 + n_tets * 33 + rec_bytes + n_cf * 12 + n_tri * 72;
-  // Hot accelerator bytes as the reference counts them (records + f32 xyz points).
-  m->hot_bytes = (layout == 80) ? rec_bytes : rec_bytes + n_points * 12;
+  // Hot bytes the walk actually gathers from on this device: the records plus
+  // the six axis-permuted float4 point copies (96 B per point; a ray reads one
+  // copy, an incoherent batch all six).  TetMesh-80 reads only its records.
+  // (The reference's accelerator -- records + 12 B f32 points -- is reported
+  // beside it by bench.py as mesh_bytes.reference_accelerator_bytes.)
+  m->hot_bytes = (layout == 80) ? rec_bytes : rec_bytes + n_points * 16 * 6;
   *out = m;
   return TB_OK;
 }

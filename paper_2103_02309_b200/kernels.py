@@ -81,10 +81,11 @@ def _check_cf(dm, mesh, status, cf) -> None:
     table; the kernel then skips the epilogue gathers and this raises, as the
     reference's batch epilogue does on mesh.cf_triangle[cf] (batch.py:63)."""
     if not dm.validated:
-        bad = np.nonzero((status == STATUS_HIT) & ((cf < 0) | (cf >= len(mesh.cf_triangle))))[0]
+        n_cf = dm.n_cf  # ``mesh`` may itself be the DeviceMesh
+        bad = np.nonzero((status == STATUS_HIT) & ((cf < 0) | (cf >= n_cf)))[0]
         if len(bad):
             raise IndexError(f"ray {int(bad[0])} hit constrained face {int(cf[bad[0]])}, outside the mesh's "
-                             f"{len(mesh.cf_triangle)} constrained faces")
+                             f"{n_cf} constrained faces")
 
 
 def cast_rays(mesh, o32, d32, start, visits_sink=None):

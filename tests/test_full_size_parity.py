@@ -20,7 +20,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from refpkg import have_ref, ref_cast_full
+from refpkg import have_ref, hits_mismatch, ref_cast_full
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_ref(), reason="oracle/_ref/site missing")]
 
@@ -46,7 +46,7 @@ def _trace_all(mesh, o, d, st, schedule="lane", chunk=1 << 24):
 
 
 def _assert_equal(got, exp, what):
-    bad = {n: int(np.count_nonzero(g != e)) for n, g, e in zip(NAMES, got, exp)}
+    bad = hits_mismatch(got, exp)
     assert not any(bad.values()), f"{what}: mismatched values per array {bad}"
 
 
