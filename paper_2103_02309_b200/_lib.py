@@ -110,10 +110,22 @@ def get_schedule() -> tuple[int, int]:
     return m.value, k.value
 
 
+_from_buffer = ctypes.c_char.from_buffer
+_addressof = ctypes.addressof
+
+
 def addr(a) -> int | None:
-    """Raw address of a numpy array or torch tensor (None stays NULL)."""
+    """Raw address of a numpy array or torch tensor (None stays NULL).
+    Writable numpy arrays go through the buffer protocol (~0.4 us; the
+    per-tile protocol calls pass 7-10 arrays), read-only ones through
+    ``ndarray.ctypes`` (~2.5 us)."""
     if a is None:
         return None
     if hasattr(a, "data_ptr"):
         return a.data_ptr()
+    if a.flags.writeable and a.size:
+        try:
+            return _addressof(_from_buffer(a))
+        except (TypeError, ValueError, BufferError):
+            pass
     return a.ctypes.data

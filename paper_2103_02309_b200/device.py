@@ -3,11 +3,16 @@
 The reference kernels read the mesh arrays on every call
 (_kernels.pyx:276-282); here a ``CompactMesh`` is uploaded to HBM on first
 use and the handle is cached.  The cache key is the mesh object plus the
-data pointers and shapes of every array the device copy is built from, so
-replacing an array (``relayout``, ``reorder``, ``dataclasses.replace``)
-triggers a fresh upload; in-place mutation of an array does not -- call
-``invalidate(mesh)`` after mutating (the reference tests that do so only
-exercise ``validate``, test_tetmesh.py:123-148).
+identity and shape of every array the device copy is built from (the entry
+holds those arrays, so identities cannot be recycled while it lives):
+replacing an array (``relayout``, ``reorder``, ``dataclasses.replace``,
+``mesh.points = ...``) triggers a fresh upload.  In-place mutation cannot go
+stale silently: while a device copy is cached, the arrays it mirrors are
+marked read-only, so writing into them raises numpy's "assignment
+destination is read-only" -- call ``invalidate(mesh)`` first (it restores
+writability; the next call uploads again).  The per-call check is a tuple
+of ids and shapes (~1 us), not a hash of the data: renderers call
+``cast_rays`` once per 16x16 tile (render.py:538-541).
 """
 
 from __future__ import annotations
@@ -116,10 +121,40 @@ class DeviceMesh:
         self.handle = ctypes.c_void_p()
 
 
-def _fingerprint(mesh):
-    arrs = [mesh.points, mesh.records, mesh.side_verts, mesh.side_neighbors, mesh.cf_triangle, mesh.cf_tets,
-            mesh.soup.vertices, mesh.soup.triangles]
-    return tuple((a.__array_interface__["data"][0], a.shape) for a in arrs) + (mesh.layout,)
+def _mirrored(mesh) -> tuple:
+    """The host arrays a device copy is built from."""
+    return (mesh.points, mesh.records, mesh.side_verts, mesh.side_neighbors, mesh.cf_triangle, mesh.cf_tets,
+            mesh.soup.vertices, mesh.soup.triangles)
+
+
+def _fingerprint(arrs, layout) -> tuple:
+    return tuple((id(a), a.shape) for a in arrs) + (layout,)
+
+
+class _Entry:
+    """A cached upload: the device mesh, its fingerprint, the mirrored arrays
+    (kept alive) and their writeable flags before the cache froze them."""
+
+    __slots__ = ("dm", "fp", "arrs", "was_writeable")
+
+    def __init__(self, dm, fp, arrs):
+        self.dm, self.fp, self.arrs = dm, fp, arrs
+        self.was_writeable = []
+        for a in arrs:
+            w = bool(a.flags.writeable)
+            self.was_writeable.append(w)
+            if w:
+                a.flags.writeable = False
+
+    def thaw(self) -> None:
+        """Restore writability (unless another cached copy still mirrors the array)."""
+        frozen = {id(a) for e in _cache.values() if e is not self for a in e.arrs}
+        for a, w in zip(self.arrs, self.was_writeable):
+            if w and id(a) not in frozen:
+                try:
+                    a.flags.writeable = True
+                except ValueError:  # a view whose base became read-only meanwhile
+                    pass
 
 
 _lock = threading.Lock()
@@ -132,13 +167,17 @@ def device_mesh(mesh, device: int | None = None, layout: str | None = None) -> D
         return mesh
     dev = default_device() if device is None else int(device)
     key = (id(mesh), layout or mesh.layout, dev)
-    fp = _fingerprint(mesh)
+    arrs = _mirrored(mesh)
+    fp = _fingerprint(arrs, mesh.layout)
     with _lock:
         hit = _cache.get(key)
-        if hit is not None and hit[1] == fp:
-            return hit[0]
+        if hit is not None and hit.fp == fp:
+            return hit.dm
+        if hit is not None:  # an array was replaced: the old entry's arrays are no longer the mesh's
+            _cache.pop(key)
+            hit.thaw()
         dm = DeviceMesh(mesh, dev, layout)
-        _cache[key] = (dm, fp)
+        _cache[key] = _Entry(dm, fp, arrs)
         try:
             weakref.finalize(mesh, _evict, key)
         except TypeError:
@@ -151,16 +190,19 @@ def _evict(key) -> None:
     # freed by DeviceMesh's own finalizer once no caller holds it any more
     # (a caller may keep using a DeviceMesh after its host mesh is gone).
     with _lock:
-        _cache.pop(key, None)
+        e = _cache.pop(key, None)
+        if e is not None:
+            e.thaw()
 
 
 def invalidate(mesh) -> None:
-    """Drop every cached device copy of ``mesh`` (after in-place mutation):
-    the next ``device_mesh(mesh)`` uploads again.  DeviceMesh objects already
-    handed out stay valid until released."""
+    """Drop every cached device copy of ``mesh`` and make its arrays writeable
+    again (call before mutating them in place): the next ``device_mesh(mesh)``
+    uploads again.  DeviceMesh objects already handed out stay valid until
+    released."""
     with _lock:
         for k in [k for k in _cache if k[0] == id(mesh)]:
-            _cache.pop(k)
+            _cache.pop(k).thaw()
 
 
 __all__ = ["DeviceMesh", "device_mesh", "invalidate", "default_device", "LAYOUT_CODES", "_lib"]

@@ -172,3 +172,66 @@ def test_sctp_degenerate_and_extreme_rays_vs_c_oracle(layout):
     exp = pyoracle.cast_rays_full(m, oo, dd, ss, layout=layout, sctp=True)
     for k, a, b in zip(("status", "cf", "tet", "visited", "triangle", "t", "tet_back"), got, exp):
         assert np.array_equal(a, b, equal_nan=(k == "t")), k
+
+
+def test_cached_mesh_arrays_are_frozen_until_invalidate():
+    """The device cache cannot go stale silently: while a mesh is cached, its
+    mirrored arrays are read-only (the reference re-reads them every call,
+    _kernels.pyx:276-282); invalidate() thaws them and the next call uploads
+    the mutated mesh."""
+    from paper_2103_02309_b200 import device, kernels as K
+    from paper_2103_02309_b200.ingestion import build_box_fixture
+    from paper_2103_02309_b200.scenes import interior_rays
+    from paper_2103_02309_b200.tetmesh import encode
+    from oracle import pyoracle
+
+    raw, soup = build_box_fixture(4, occluders=[(0, 2, (1, 1), (3, 3))])
+    mesh = encode(raw, "tet20", soup)
+    o, d, st = interior_rays(mesh, 2000, 5)
+    first = K.cast_rays(mesh, o, d, st)
+    assert not mesh.points.flags.writeable and not mesh.side_neighbors.flags.writeable
+    with pytest.raises(ValueError):
+        mesh.points[0, 0] = 0.5
+    device.invalidate(mesh)
+    assert mesh.points.flags.writeable and mesh.records.flags.writeable
+    mesh.points[:] = mesh.points * np.float32(2.0)  # scale the scene in place
+    o2 = o * np.float32(2.0)
+    got = K.cast_rays(mesh, o2, d, st)
+    exp = pyoracle.cast_rays(mesh, o2, d, st)
+    for a, b in zip(got, exp):
+        assert np.array_equal(a, b)
+    assert first[3].shape == got[3].shape
+    # replacing an array (not in place) re-uploads without invalidate and thaws the old one
+    old = mesh.points
+    mesh.points = mesh.points.copy()
+    K.cast_rays(mesh, o2, d, st)
+    assert old.flags.writeable and not mesh.points.flags.writeable
+    device.invalidate(mesh)
+
+
+def test_small_batch_protocol_calls_from_threads(REF):
+    """Renderer granularity: 256-ray calls of the protocol module from 16
+    host threads (render.py:538-541) give the reference's results."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2103_02309_b200 import kernels as K
+    from paper_2103_02309_b200.ingestion import build_box_fixture
+    from paper_2103_02309_b200.scenes import interior_rays
+    from paper_2103_02309_b200.tetmesh import encode
+
+    raw, soup = build_box_fixture(6, occluders=[(0, 3, (1, 1), (5, 5))])
+    mesh = encode(raw, "tet16", soup)
+    o, d, st = interior_rays(mesh, 256 * 64, 9)
+    exp = REF.cast_rays(mesh, o, d, st)
+
+    def one(i):
+        sl = slice(256 * i, 256 * (i + 1))
+        return K.cast_rays(mesh, o[sl], d[sl], st[sl])
+
+    with ThreadPoolExecutor(max_workers=16) as pool:
+        parts = list(pool.map(one, range(64)))
+    for k in range(4):
+        assert np.array_equal(np.concatenate([p[k] for p in parts]), exp[k])
+    from paper_2103_02309_b200 import device
+
+    device.invalidate(mesh)
