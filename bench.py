@@ -64,14 +64,18 @@ CONFIGS = {
     4: dict(grid=55, width=4096, height=4096, layout="tet16", scheme="hilbert", secondaries=True,
             desc="cfg4: blob GRID=55, 16.7M diffuse secondaries from 4096x4096 primary hits, TetMesh-16"),
     # config 5 names no layout (BASELINE.json configs[4]); with 180 GB of HBM the
-    # 1 GB TetMesh-20 beats the 0.8 GB TetMesh-16 (r01 A/B: 825 vs 707 Mrays/s)
-    5: dict(kuhn=203, width=7680, height=4320, layout="tet20", scheme="none", sample_stride=64,
+    # 1.6 GB TetMesh-32 (46.5 SASS per step) beats the 1 GB TetMesh-20 (53.75)
+    # and the 0.8 GB TetMesh-16 (r02 A/B, profiles/r02_layouts.jsonl: 855 / 827 /
+    # 720 Mrays/s)
+    5: dict(kuhn=203, width=7680, height=4320, layout="tet32", scheme="none", sample_stride=64,
             desc="cfg5: Kuhn box n=203 (50,192,562 tets) stretched 4x in z with thin strip occluders "
-                 "(long thin triangles), 7680x4320 primary rays, TetMesh-20"),
+                 "(long thin triangles), 7680x4320 primary rays, TetMesh-32"),
 }
 L2_FLUSH_BYTES = 256 << 20
 FALLBACK_HBM_GBS = 6650.0
 LAYOUT_BYTES = {"tet32": 32, "tet20": 20, "tet16": 16, "tet80": 80}
+# layouts built on the device from the side tables (the host mesh stays Tet32)
+DEVICE_BUILT = ("tet80",)
 
 
 def log(*a):
@@ -250,7 +254,7 @@ def ref_scene(cfg):
     from tetray.cli import load_compact
     from tetray.tetmesh import LAYOUT_DTYPES, CompactMesh, SceneTriangleSoup, relayout
 
-    layout = "tet32" if cfg["layout"] == "tet80" else cfg["layout"]
+    layout = "tet32" if cfg["layout"] in DEVICE_BUILT else cfg["layout"]
     if "grid" in cfg:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import make_ref_scene
@@ -378,7 +382,7 @@ def build_scene(cfg):
     if "kuhn" in cfg:
         sc = kuhn_strip_scene(cfg["kuhn"], layout=cfg["layout"], scheme=cfg["scheme"])
     else:
-        host_layout = "tet32" if cfg["layout"] == "tet80" else cfg["layout"]
+        host_layout = "tet32" if cfg["layout"] in DEVICE_BUILT else cfg["layout"]
         sc = blob_scene(cfg["grid"], layout=host_layout, scheme=cfg["scheme"], check=False)
     log(f"[bench] scene {sc.name}: {sc.mesh.n_tets} tets, {sc.mesh.n_points} points, "
         f"{sc.mesh.n_constrained} constrained faces, built in {time.perf_counter() - t0:.1f}s")
@@ -520,7 +524,7 @@ def run_ours(args, cfg):
     mesh = sc.mesh
     # tet80 has no host record dtype: the host mesh stays tet32 and the device
     # builds the 80-byte records from the side tables
-    dm = device_mesh(mesh, device=local, layout=cfg["layout"] if cfg["layout"] == "tet80" else None)
+    dm = device_mesh(mesh, device=local, layout=cfg["layout"] if cfg["layout"] in DEVICE_BUILT else None)
     sctp = cfg.get("walk") == "sctp"
     W, H = cfg["width"], cfg["height"]
     per_frame = W * H
@@ -889,7 +893,7 @@ def run_ours(args, cfg):
 
 def mesh_for_ref(mesh, cfg):
     ref_package()
-    if cfg["layout"] == "tet80":
+    if cfg["layout"] in DEVICE_BUILT:
         from paper_2103_02309_b200.tetmesh import relayout
 
         return relayout(mesh, "tet32")
@@ -939,11 +943,17 @@ def config4_secondaries(args, mesh20, stream, flush, threads, clocks):
     from paper_2103_02309_b200.trace import empty_result, locate, trace
     from paper_2103_02309_b200.workload import diffuse_secondaries
 
+    from paper_2103_02309_b200.multigpu import shard_pixels
+
     cfg = CONFIGS[4]
     dev = flush.device
     mesh = relayout(mesh20, cfg["layout"])
     dm = DeviceMesh(mesh, dev.index)
     o, d, pos = frame_rays(cfg, 0)
+    # the reference renderer traces (and spawns secondaries) per 16x16 tile
+    # (render.py:496-514, 538-541): rays in tile order, as bench.py --config 4
+    tiles = shard_pixels(cfg["width"], cfg["height"], 0, 1, 16)
+    o, d = o[tiles], d[tiles]
     cam, _ = locate(dm, torch.tensor(pos[None], dtype=torch.float64, device=dev),
                     torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))
     st = np.full(len(o), int(cam.item()), np.int32)
@@ -973,7 +983,7 @@ def config4_secondaries(args, mesh20, stream, flush, threads, clocks):
            "roofline_issue": roof, "traffic": traffic_of("cfg4/tet16"),
            "algorithmic_bytes_per_launch": algorithmic_bytes(v2, "tet16"),
            "rays_from": "diffuse hemisphere bounces of the 4096x4096 blob-camera frame's primary hits (seed 4), "
-                        "Tet16 Hilbert mesh of the same scene",
+                        "16x16-tile order (the reference renderer's), Tet16 Hilbert mesh of the same scene",
            "parity": par}
     dm.close()
     return out

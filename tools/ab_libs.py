@@ -81,6 +81,11 @@ def main():
         sc = build_scene(cfg)
         mesh = sc.mesh
         o, d, pos = frame_rays(cfg, 0)
+        if os.environ.get("AB_TILES"):  # the reference renderer's 16x16-tile ray order
+            from paper_2103_02309_b200.multigpu import shard_pixels
+
+            tiles = shard_pixels(cfg["width"], cfg["height"], 0, 1, 16)
+            o, d = o[tiles], d[tiles]
         dm = device_mesh(mesh)
         cam, _ = locate(dm, torch.tensor(pos[None], dtype=torch.float64, device=dev),
                         torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))

@@ -2,13 +2,16 @@
 """Same-process A/B of ray schedules (trace(schedule=...)) on the bench workloads.
 
     python tools/sched_ab.py [--configs 2,3,5] [--schedules lane,dynamic] [--reps 20] [--rounds 3]
-                             [--secondaries]
+                             [--secondaries] [--layouts tet20,tet32] [--tiles]
 
 Builds each bench scene once, times the trace with CUDA events (256 MiB
 written between launches to flush L2), schedules interleaved round by round,
 and checks every schedule's seven outputs equal the first's bit for bit.
 --secondaries: time the frame's diffuse bounces (config 4 semantics, seed 4)
-instead of the primaries.  One JSON line per (config, schedule).
+instead of the primaries.  --layouts: device layouts to compare (default:
+the config's own; tet80 is built on the device from the same host mesh).
+--tiles: rays in 16x16-tile order (the reference renderer's) instead of row
+major.  One JSON line per (config, layout, schedule).
 """
 
 from __future__ import annotations
@@ -40,6 +43,8 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--secondaries", action="store_true")
     ap.add_argument("--layout", default=None)
+    ap.add_argument("--layouts", default=None)
+    ap.add_argument("--tiles", action="store_true")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
@@ -48,9 +53,17 @@ def main():
         cfg = dict(CONFIGS[c])
         if a.layout:
             cfg["layout"] = a.layout
+        layouts = a.layouts.split(",") if a.layouts else [cfg["layout"]]
+        if cfg["layout"] == "tet80":
+            cfg["layout"] = "tet32"
         mesh = build_scene(cfg).mesh
-        dm = DeviceMesh(mesh, 0)
+        dm = DeviceMesh(mesh, 0, layout=layouts[0])
         o, d, pos = frame_rays(cfg, 0)
+        if a.tiles:
+            from paper_2103_02309_b200.multigpu import shard_pixels
+
+            tiles = shard_pixels(cfg["width"], cfg["height"], 0, 1, 16)
+            o, d = o[tiles], d[tiles]
         cam, _ = locate(dm, torch.tensor(pos[None], dtype=torch.float64, device=dev),
                         torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))
         st = np.full(len(o), int(cam.item()), np.int32)
@@ -60,24 +73,29 @@ def main():
                                            prim.tet.cpu().numpy(), mesh.triangle_coords(), seed=4)
             del prim
         g = [torch.from_numpy(x).to(dev) for x in (o, d, st)]
-        scheds = a.schedules.split(",")
-        outs = {s: empty_result(len(st), dev) for s in scheds}
-        ms = {s: [] for s in scheds}
+        dms = {layouts[0]: dm}
+        for lay in layouts[1:]:
+            dms[lay] = DeviceMesh(mesh, 0, layout=lay)
+        runs = [(lay, s) for lay in layouts for s in a.schedules.split(",")]
+        outs = {k: empty_result(len(st), dev) for k in runs}
+        ms = {k: [] for k in runs}
         for _ in range(a.rounds):
-            for s in scheds:
-                ms[s].extend(timed(lambda: trace(dm, *g, out=outs[s], stream=stream, schedule=s), a.reps, 3, stream,
-                                   flush).tolist())
-        ref = outs[scheds[0]]
+            for k in runs:
+                ms[k].extend(timed(lambda: trace(dms[k[0]], *g, out=outs[k], stream=stream, schedule=k[1]), a.reps, 3,
+                                   stream, flush).tolist())
+        ref = outs[runs[0]]
         vis = ref.visited.cpu().numpy()
-        for s in scheds:
-            same = all(torch.equal(getattr(outs[s], f), getattr(ref, f)) for f in FIELDS)
-            med = float(np.median(ms[s]))
-            print(json.dumps({"config": c, "layout": cfg["layout"], "secondaries": bool(a.secondaries or
-                                                                                       cfg.get("secondaries")),
-                              "schedule": s, "rays": len(st), "kernel_ms_median": med,
-                              "kernel_ms_min": float(np.min(ms[s])), "mrays_s": len(st) / med / 1e3,
+        for k in runs:
+            same = all(torch.equal(getattr(outs[k], f), getattr(ref, f)) for f in FIELDS)
+            med = float(np.median(ms[k]))
+            print(json.dumps({"config": c, "layout": k[0], "secondaries": bool(a.secondaries or
+                                                                              cfg.get("secondaries")),
+                              "order": "tiles16" if a.tiles else "row-major",
+                              "schedule": k[1], "rays": len(st), "kernel_ms_median": med,
+                              "kernel_ms_min": float(np.min(ms[k])), "mrays_s": len(st) / med / 1e3,
                               "tets_per_ray": float(vis.mean()), "equal_to_first": same}), flush=True)
-        dm.close()
+        for x in dms.values():
+            x.close()
 
 
 if __name__ == "__main__":
