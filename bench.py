@@ -424,9 +424,17 @@ def timed(fn, steps: int, warmup: int, stream, flush):
     return np.array([a.elapsed_time(b) for a, b in evs])
 
 
+# sm_100 pipe rates (B300_MICROARCH.md "Pipe rates": IADD3/LOP3/SHF/PRMT/SEL/
+# compares on the ALU pipe at one warp instruction per 2 cycles per SMSP; ncu
+# sm__inst_executed_pipe_alu of the config-2 walk = 62.6 % of that peak)
+ALU_CYCLES_PER_INST = 2
+
+
 def issue_roof(layout: str, schedule: str, walk_steps: float, kern_s: float, clk_mhz, sms: int):
-    """The walk's binding roof: SASS instructions per walk step (tools/
-    sass_steps.py, committed per build) at full issue on every scheduler."""
+    """The walk's binding roof from its SASS (tools/sass_steps.py, committed
+    per build): a warp-step needs max(SASS per step, 2 x ALU-pipe SASS per
+    step) scheduler cycles -- whichever of instruction issue and the ALU pipe
+    binds (the ALU pipe for every layout: tet20 2 x 27.5 > 53.75)."""
     sp = os.path.join(ROOT, "profiles", "sass_step_counts.json")
     if not (os.path.exists(sp) and clk_mhz):
         return None
@@ -435,13 +443,25 @@ def issue_roof(layout: str, schedule: str, walk_steps: float, kern_s: float, clk
     entry = counts.get(f"{kname}<{layout[3:]}, validated>") or counts.get(f"{kname}<{layout[3:]}, clamp>")
     if not entry:
         return None
-    per_step = (entry.get("unrolled_x4_per_step") or entry["single_step"])["total"]
-    peak_steps = sms * 4 * clk_mhz * 1e6 * 32 / per_step
+    mix = entry.get("unrolled_x4_per_step") or entry["single_step"]
+    per_step, alu = mix["total"], mix["alu"]
+    cycles = max(per_step, ALU_CYCLES_PER_INST * alu)
+    peak_steps = sms * 4 * clk_mhz * 1e6 * 32 / cycles
+    issue_peak = sms * 4 * clk_mhz * 1e6 * 32 / per_step
     ach = walk_steps / kern_s
-    return {"bound": "issue", "achieved": ach / 1e9, "peak": peak_steps / 1e9, "unit": "G ray-steps/s",
-            "frac": ach / peak_steps, "sass_per_step": per_step, "sms": sms, "sm_mhz": clk_mhz,
-            "note": "peak = SMs x 4 schedulers x SM clock x 32 lanes / SASS instructions per walk step; the gap "
-                    "is init/epilogue, SIMT divergence, issue stalls and the tail"}
+    return {"bound": "alu_pipe" if cycles > per_step else "issue", "achieved": ach / 1e9, "peak": peak_steps / 1e9,
+            "unit": "G ray-steps/s", "frac": ach / peak_steps, "sass_per_step": per_step, "alu_per_step": alu,
+            "cycles_per_warp_step": cycles, "issue_frac": ach / issue_peak, "sms": sms, "sm_mhz": clk_mhz,
+            "note": "peak = SMs x 4 schedulers x SM clock x 32 lanes / max(SASS, 2 x ALU-pipe SASS) per walk step; "
+                    "the gap is init/epilogue, SIMT divergence, latency stalls and the tail"}
+
+
+def pipes_of(key: str):
+    """ncu pipe / L1 utilisation of the walk (profiles/pipe_util.json)."""
+    pp = os.path.join(ROOT, "profiles", "pipe_util.json")
+    if os.path.exists(pp):
+        return json.load(open(pp)).get(key)
+    return None
 
 
 def traffic_of(key: str):
@@ -833,7 +853,7 @@ def run_ours(args, cfg):
                    "and is not the binding roof"}
     if roof is None:
         roof = dict(hbm)
-    roof = dict(roof, traffic=traffic, kernel=kname)
+    roof = dict(roof, traffic=traffic, kernel=kname, ncu_pipes=pipes_of(f"cfg{args.config}/{cfg['layout']}"))
     line = {
         "metric": "Mrays/s", "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -980,7 +1000,7 @@ def config4_secondaries(args, mesh20, stream, flush, threads, clocks):
     out = {"value": ns / kb / 1e3, "unit": "Mrays/s", "rays": ns, "kernel_ms": kb, "schedule": "binned",
            "one_ray_per_lane": {"value": ns / float(ms["lane"].mean()) / 1e3, "kernel_ms": float(ms["lane"].mean())},
            "tets_visited_per_ray": {"mean": float(v2.mean()), "max": int(v2.max())},
-           "roofline_issue": roof, "traffic": traffic_of("cfg4/tet16"),
+           "roofline": roof, "traffic": traffic_of("cfg4/tet16"), "ncu_pipes": pipes_of("cfg4/tet16"),
            "algorithmic_bytes_per_launch": algorithmic_bytes(v2, "tet16"),
            "rays_from": "diffuse hemisphere bounces of the 4096x4096 blob-camera frame's primary hits (seed 4), "
                         "16x16-tile order (the reference renderer's), Tet16 Hilbert mesh of the same scene",
