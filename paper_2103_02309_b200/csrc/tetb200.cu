@@ -80,9 +80,12 @@ namespace {
 
 constexpr int kBlock = 128;
 // cast_kernel block size (r01 A/B: 32 / 64 / 256 threads were 1-7 % slower)
-constexpr int kCastBlock = 128;
+#ifndef TB_CAST_BLOCK
+#define TB_CAST_BLOCK 128
+#endif
+constexpr int kCastBlock = TB_CAST_BLOCK;
 #ifndef TB_CAST_MIN_BLOCKS
-#define TB_CAST_MIN_BLOCKS 10  // cast_kernel residency target: 48 registers (r01 A/B)
+#define TB_CAST_MIN_BLOCKS (1280 / TB_CAST_BLOCK)  // cast_kernel residency target: 48 registers (r01 A/B)
 #endif
 
 struct DeviceGuard {
