@@ -178,7 +178,9 @@ __device__ __forceinline__ int init_ray(const MeshView& m, float o0, float o1, f
   float q2[8];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const float4 Q = ldg_f4(&Pp[quad[i]]);
+    // 32-bit index (ids are < n_points < 2^31): one LEA pair per address
+    // instead of a sign-extended 64-bit add + LEA pair
+    const float4 Q = ldg_f4_at(Pp, (uint32_t)quad[i]);
     q2[2 * i] = __fsub_rn(__fadd_rn(__fmul_rn(b.umax, Q.x), Q.y), b.pox);
     q2[2 * i + 1] = __fsub_rn(
         __fadd_rn(__fadd_rn(__fmul_rn(b.vmax, Q.x), __fmul_rn(b.voth, Q.y)), __fmul_rn(b.sgn, Q.z)), b.poy);
