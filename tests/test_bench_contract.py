@@ -56,3 +56,48 @@ def test_bench_rejects_short_warmup():
     out = subprocess.run([sys.executable, "bench.py", "--warmup", "2"], cwd=ROOT, capture_output=True, text=True,
                          timeout=120)
     assert out.returncode != 0 and "warmup" in out.stderr
+
+
+def test_roofline_is_the_binding_pipe_of_the_committed_sass():
+    """`roofline` = achieved walk steps against max(issue, 2 x ALU-pipe SASS)
+    per warp-step from profiles/sass_step_counts.json (regenerated per build);
+    the ALU pipe binds for every 2-D walk layout."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    for layout in ("tet16", "tet20", "tet32"):
+        r = bench.issue_roof(layout, "lane", walk_steps=1e9, kern_s=1e-3, clk_mhz=1965.0, sms=148)
+        assert r["bound"] == "alu_pipe", (layout, r)
+        assert r["cycles_per_warp_step"] == 2 * r["alu_per_step"] > r["sass_per_step"]
+        peak = 148 * 4 * 1965e6 * 32 / r["cycles_per_warp_step"]
+        assert r["frac"] == pytest.approx(1e12 / peak)
+        assert r["issue_frac"] < r["frac"]
+    assert bench.issue_roof("tet20", "lane", 1e9, 1e-3, None, 148) is None  # no clock sample: no roof
+
+
+def test_profiles_carry_traffic_and_pipes_for_every_bench_config():
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    for c, cfg in bench.CONFIGS.items():
+        assert bench.traffic_of(f"cfg{c}/{cfg['layout']}"), c
+    for key in ("cfg2/tet20", "cfg3/tet16", "cfg4/tet16", "cfg5/tet32"):
+        p = bench.pipes_of(key)
+        assert p and 0 < p["alu_pipe_pct"] <= 100 and 0 < p["l1tex_lsu_wavefronts_pct"] <= 100, key
+
+
+def test_hits_mismatch_holds_t_to_the_contract_only_off_the_pinned_numpy(monkeypatch):
+    import numpy as np
+
+    import refpkg
+
+    a = [np.arange(4, dtype=np.int32)] * 5 + [np.array([1.0, np.inf, 2.0, 3.0])] + [np.arange(4, dtype=np.int32)]
+    b = [x.copy() for x in a]
+    b[5][2] = 2.0 * (1 + 4e-6)  # 4e-6 relative: an einsum-order ulp drift is far smaller
+    assert refpkg.hits_mismatch(a, b)["t"] == 1  # pinned numpy: bit-exact required
+    monkeypatch.setattr(refpkg, "EINSUM_PINNED_NUMPY", "0.0.")
+    assert refpkg.hits_mismatch(a, b)["t"] == 0  # other numpy: within 1e-5 relative
+    b[5][3] = 3.1
+    assert refpkg.hits_mismatch(a, b)["t"] == 1
+    b[1] = b[1] + 1
+    assert refpkg.hits_mismatch(a, b)["cf"] == 4  # every other array stays bit-exact
