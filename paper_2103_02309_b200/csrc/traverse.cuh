@@ -136,6 +136,48 @@ __device__ __forceinline__ void project(const Basis& b, float qx, float qy, floa
       b.poy);
 }
 
+// project() on a point already in (mx, ot, mn) order: same operations, same order.
+//
+// sm_100 issues two fp32 multiplies (or adds) per instruction (FMUL2 / FADD2,
+// PTX mul/sub.rn.f32x2 on register pairs).  The walk step is issue bound, so
+// the projection pairs (vmax*q.x, voth*q.y) -- the point copy's first two
+// words are already a register pair -- and the final (x1 - pox, y2 - poy):
+// 7 FMA-pipe instructions instead of 9.  Products and sums are each rounded
+// exactly as before.  Caution: ptxas contracts a single-use f32x2 product
+// into a following f32x2 add (FFMA2) even under -fmad=false; here every
+// f32x2 product feeds scalar adds or compares only, and tools/sass_steps.py
+// fails the build check if an FFMA/FFMA2 appears in a walk loop.
+#ifndef TB_NO_F32X2
+#define TB_F32X2 1
+#endif
+__device__ __forceinline__ void project_perm(const Basis& b, const float4& q, float& x, float& y) {
+#ifdef TB_F32X2
+  asm("{\n\t"
+      ".reg .b64 s, c, m;\n\t"
+      ".reg .f32 m0, m1, ux, x1, y1, sc, y2;\n\t"
+      "mov.b64 s, {%2, %3};\n\t"
+      "mov.b64 c, {%6, %7};\n\t"
+      "mul.rn.f32x2 m, s, c;\n\t"   // (vmax*q.x, voth*q.y)
+      "mov.b64 {m0, m1}, m;\n\t"
+      "mul.rn.f32 ux, %5, %2;\n\t"  // umax*q.x
+      "add.rn.f32 x1, ux, %3;\n\t"  // + q.y
+      "add.rn.f32 y1, m0, m1;\n\t"
+      "mul.rn.f32 sc, %8, %4;\n\t"  // sgn*q.z
+      "add.rn.f32 y2, y1, sc;\n\t"
+      "mov.b64 s, {x1, y2};\n\t"
+      "mov.b64 c, {%9, %10};\n\t"
+      "sub.rn.f32x2 m, s, c;\n\t"   // (x1 - pox, y2 - poy)
+      "mov.b64 {%0, %1}, m;\n\t"
+      "}"
+      : "=f"(x), "=f"(y)
+      : "f"(q.x), "f"(q.y), "f"(q.z), "f"(b.umax), "f"(b.vmax), "f"(b.voth), "f"(b.sgn), "f"(b.pox), "f"(b.poy));
+#else
+  x = __fsub_rn(__fadd_rn(__fmul_rn(b.umax, q.x), q.y), b.pox);
+  y = __fsub_rn(__fadd_rn(__fadd_rn(__fmul_rn(b.vmax, q.x), __fmul_rn(b.voth, q.y)), __fmul_rn(b.sgn, q.z)),
+                b.poy);
+#endif
+}
+
 // Algorithm 1, _kernels.pyx:94-102: index of the window point replaced by p3.
 __device__ __forceinline__ int exit_face(float px, float py, const float (&p)[6]) {
   const float a0 = __fmul_rn(px, p[1]), b0 = __fmul_rn(py, p[0]);
@@ -181,9 +223,7 @@ __device__ __forceinline__ int init_ray(const MeshView& m, float o0, float o1, f
     // 32-bit index (ids are < n_points < 2^31): one LEA pair per address
     // instead of a sign-extended 64-bit add + LEA pair
     const float4 Q = ldg_f4_at(Pp, (uint32_t)quad[i]);
-    q2[2 * i] = __fsub_rn(__fadd_rn(__fmul_rn(b.umax, Q.x), Q.y), b.pox);
-    q2[2 * i + 1] = __fsub_rn(
-        __fadd_rn(__fadd_rn(__fmul_rn(b.vmax, Q.x), __fmul_rn(b.voth, Q.y)), __fmul_rn(b.sgn, Q.z)), b.poy);
+    project_perm(b, Q, q2[2 * i], q2[2 * i + 1]);
   }
   // sign of the fp64 orientation rho of the sorted quad (_kernels.pyx:133-147),
   // precomputed per tet at upload (orient_kernel, identical arithmetic)
@@ -353,12 +393,6 @@ __device__ __forceinline__ const float4* ray_points(const MeshView& m, const Bas
   return m.pts + (size_t)perm_index(b.mx, b.ot) * (size_t)m.n_points;
 }
 
-// project() on a point already in (mx, ot, mn) order: same operations, same order.
-__device__ __forceinline__ void project_perm(const Basis& b, const float4& q, float& x, float& y) {
-  x = __fsub_rn(__fadd_rn(__fmul_rn(b.umax, q.x), q.y), b.pox);
-  y = __fsub_rn(__fadd_rn(__fadd_rn(__fmul_rn(b.vmax, q.x), __fmul_rn(b.voth, q.y)), __fmul_rn(b.sgn, q.z)),
-                b.poy);
-}
 
 // ----------------------------------------------------------------------------
 // The decision half of a step in PTX: Algorithm 1 (_kernels.pyx:94-102), the
@@ -376,17 +410,36 @@ __device__ __forceinline__ void project_perm(const Basis& b, const float4& q, fl
 //
 // Operands: %0 nref; %1-%3 idx (in/out); %4-%9 p (in/out); %10 qx; %11 qy;
 // %12 i3; %13.. layout words.
-#define TB_STEP_HEAD                                   \
-  "{\n\t"                                              \
-  ".reg .pred c0, c1, c2, f1, f2, g, q0, q1;\n\t"      \
-  ".reg .f32 a0, a1, a2, e0, e1, e2;\n\t"              \
-  ".reg .b32 fi, rk, t, lo, hi;\n\t"                   \
+// The six products of Algorithm 1 as three FMUL2: (qx, qy) * (p[2k+1], p[2k])
+// = (a_k, e_k); the window pair (y_k, x_k) stays one aligned register pair.
+#ifdef TB_F32X2
+#define TB_STEP_PRODUCTS                               \
+  ".reg .b64 Q2, W2, A2;\n\t"                          \
+  "mov.b64 Q2, {%10, %11};\n\t"                        \
+  "mov.b64 W2, {%5, %4};\n\t"                          \
+  "mul.rn.f32x2 A2, Q2, W2;\n\t"                       \
+  "mov.b64 {a0, e0}, A2;\n\t"                          \
+  "mov.b64 W2, {%9, %8};\n\t"                          \
+  "mul.rn.f32x2 A2, Q2, W2;\n\t"                       \
+  "mov.b64 {a2, e2}, A2;\n\t"                          \
+  "mov.b64 W2, {%7, %6};\n\t"                          \
+  "mul.rn.f32x2 A2, Q2, W2;\n\t"                       \
+  "mov.b64 {a1, e1}, A2;\n\t"
+#else
+#define TB_STEP_PRODUCTS                               \
   "mul.rn.f32 a0, %10, %5;\n\t"                        \
   "mul.rn.f32 e0, %11, %4;\n\t"                        \
   "mul.rn.f32 a2, %10, %9;\n\t"                        \
   "mul.rn.f32 e2, %11, %8;\n\t"                        \
   "mul.rn.f32 a1, %10, %7;\n\t"                        \
-  "mul.rn.f32 e1, %11, %6;\n\t"                        \
+  "mul.rn.f32 e1, %11, %6;\n\t"
+#endif
+#define TB_STEP_HEAD                                   \
+  "{\n\t"                                              \
+  ".reg .pred c0, c1, c2, f1, f2, g, q0, q1;\n\t"      \
+  ".reg .f32 a0, a1, a2, e0, e1, e2;\n\t"              \
+  ".reg .b32 fi, rk, t, lo, hi;\n\t"                   \
+  TB_STEP_PRODUCTS                                     \
   "setp.lt.f32 c0, a0, e0;\n\t"                        \
   "setp.ge.f32 c2, a2, e2;\n\t"                        \
   "setp.lt.f32 c1, a1, e1;\n\t"                        \

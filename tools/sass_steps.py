@@ -28,7 +28,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 ALU = ("ISETP", "FSETP", "DSETP", "LOP3", "LOP", "SEL", "FSEL", "PLOP3", "IMNMX", "VIMNMX", "FMNMX", "LEA",
        "SHF", "PRMT", "IADD3", "VIADD", "FLO", "POPC", "BREV", "IABS", "P2R", "R2P", "ISCADD", "SGXT", "BMSK")
-FMA = ("FMUL", "FADD", "FFMA", "IMAD", "IMUL", "FMNMX3")
+FMA = ("FMUL", "FADD", "FFMA", "IMAD", "IMUL", "FMNMX3", "FMUL2", "FADD2", "FFMA2")
 LSU = ("LDG", "STG", "LDS", "STS", "LDL", "STL", "LD", "ST", "ATOM", "ATOMS", "RED", "LDC")
 CBU = ("BRA", "EXIT", "BSSY", "BSYNC", "BAR", "WARPSYNC", "RET", "CALL", "BREAK", "JMP")
 
@@ -113,6 +113,15 @@ def main(argv):
             continue
         one = loops[0]
         n_ld = sum(re.sub(r"^@!?U?P\w+\s+", "", x).startswith("LDG") for _, x in one)
+        # exactness guard: the walk's fp32 arithmetic is mul/add with explicit
+        # rounding; a contracted FFMA / FFMA2 in a walk step breaks bit-exactness.
+        # Checked on the single-step loop of every cast walk and the unrolled
+        # loop of cast_kernel (the shadow / ScTP steps and the compact kernels'
+        # refill hold IEEE divisions, whose expansions use FFMA legitimately).
+        checked = [one] + ([loops[-1]] if key.startswith("cast_kernel") else [])
+        fused = [x for body in checked for _, x in body if re.search(r"\bFFMA2?\b", x)]
+        if fused and key.startswith("cast"):
+            raise SystemExit(f"{key}: contracted FFMA in the walk loop: {fused[:3]}")
         entry = {"single_step": mix_of(one)}
         big = loops[-1]
         k = sum(re.sub(r"^@!?U?P\w+\s+", "", x).startswith("LDG") for _, x in big) // max(n_ld, 1)
