@@ -87,6 +87,19 @@ constexpr int kCastBlock = TB_CAST_BLOCK;
 #ifndef TB_CAST_MIN_BLOCKS
 #define TB_CAST_MIN_BLOCKS (1280 / TB_CAST_BLOCK)  // cast_kernel residency target: 48 registers (r01 A/B)
 #endif
+// Residency per walk (r02 A/B, tools/gpu_r02k.sh): coherent Tet16 / Tet20 walks
+// issue best at 10 blocks per SM (48 registers: 12 blocks spill into the step
+// and lose 2 %); walks bound by gather latency -- Tet32's 32 B records on the
+// 50 M-tet mesh, and every direction-binned (kGather) secondary batch -- gain
+// from 12 blocks (40 registers, the epilogue's ray reloaded after the walk):
+// config 5 +5 %, config 4 +2.6 %.
+#ifndef TB_CAST_MIN_BLOCKS_LATENCY
+#define TB_CAST_MIN_BLOCKS_LATENCY (1536 / TB_CAST_BLOCK)
+#endif
+template <int L, bool kGather>
+constexpr int cast_min_blocks() {
+  return (L == 32 || kGather) ? TB_CAST_MIN_BLOCKS_LATENCY : TB_CAST_MIN_BLOCKS;
+}
 
 struct DeviceGuard {
   int prev = -1;
@@ -275,11 +288,43 @@ __device__ __forceinline__ void load_xyz_warp(const float* __restrict__ a, int64
 
 // ----------------------------------------------------------------------------
 // Shared termination + fused epilogue (batch.py:57-71).
-__device__ __forceinline__ void write_result(const MeshView& m, int64_t r, uint8_t st, uint32_t ref,
-                                             uint32_t cur, int vis, float o0, float o1, float o2,
-                                             float d0, float d1, float d2, uint8_t* status, int32_t* cf,
-                                             int32_t* tet, int32_t* visited, int32_t* triangle,
-                                             double* t, int32_t* tet_back) {
+//
+// Ray origin / direction for the epilogue's fp64 t.  Kept live through the
+// walk they cost six registers (plus the 64-bit ray index) across the whole
+// loop; device-resident rays are instead re-read -- only for hits -- after the
+// walk, which frees the registers for the loop (r02 A/B: +0.9 ... +1.5 %;
+// -DTB_NO_RELOAD_RAY restores the register copy).  The
+// loads are volatile so the front end cannot merge them with the init loads
+// and keep the values live after all.
+struct RayRef {
+  const float* o;
+  const float* d;
+  int64_t q;
+  __device__ __forceinline__ static float ld(const float* a) {
+    float v;
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(a));
+    return v;
+  }
+  __device__ __forceinline__ double mt(const MeshView& m, int32_t tri) const {
+    const float* po = o + 3 * q;
+    const float* pd = d + 3 * q;
+    return mt_t((double)ld(po), (double)ld(po + 1), (double)ld(po + 2), (double)ld(pd), (double)ld(pd + 1),
+                (double)ld(pd + 2), m.tri + 9 * (int64_t)tri);
+  }
+};
+// The ray's values kept in registers (host-mapped rays, the other walks).
+struct RayVal {
+  float o0, o1, o2, d0, d1, d2;
+  __device__ __forceinline__ double mt(const MeshView& m, int32_t tri) const {
+    return mt_t((double)o0, (double)o1, (double)o2, (double)d0, (double)d1, (double)d2, m.tri + 9 * (int64_t)tri);
+  }
+};
+
+template <class Ray>
+__device__ __forceinline__ void write_result_ray(const MeshView& m, int64_t r, uint8_t st, uint32_t ref,
+                                                 uint32_t cur, int vis, const Ray& ray, uint8_t* status,
+                                                 int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle,
+                                                 double* t, int32_t* tet_back) {
   if (status != nullptr) status[r] = st;
   const int32_t cfi = (st == kHit) ? (int32_t)(ref & kPayload) : -1;
   cf[r] = cfi;
@@ -293,9 +338,7 @@ __device__ __forceinline__ void write_result(const MeshView& m, int64_t r, uint8
     // n_cf, as the reference's batch epilogue does (batch.py:63).
     if (cfi >= 0 && cfi < m.n_cf) {
       tri = __ldg(&m.cf_tri[cfi]);
-      if (t != nullptr && (uint32_t)tri < (uint64_t)m.n_tri)
-        tt = mt_t((double)o0, (double)o1, (double)o2, (double)d0, (double)d1, (double)d2,
-                  m.tri + 9 * (int64_t)tri);
+      if (t != nullptr && (uint32_t)tri < (uint64_t)m.n_tri) tt = ray.mt(m, tri);
       const int2 ct = __ldg(&m.cf_tets[cfi]);
       back = (ct.x == (int32_t)cur) ? ct.y : ct.x;
     }
@@ -303,6 +346,15 @@ __device__ __forceinline__ void write_result(const MeshView& m, int64_t r, uint8
     if (t != nullptr) t[r] = tt;
     if (tet_back != nullptr) tet_back[r] = back;
   }
+}
+
+__device__ __forceinline__ void write_result(const MeshView& m, int64_t r, uint8_t st, uint32_t ref,
+                                             uint32_t cur, int vis, float o0, float o1, float o2,
+                                             float d0, float d1, float d2, uint8_t* status, int32_t* cf,
+                                             int32_t* tet, int32_t* visited, int32_t* triangle,
+                                             double* t, int32_t* tet_back) {
+  write_result_ray(m, r, st, ref, cur, vis, RayVal{o0, o1, o2, d0, d1, d2}, status, cf, tet, visited, triangle,
+                   t, tet_back);
 }
 
 // Batch epilogue alone (batch.py:57-71) from stored cf / tet: the multi-GPU
@@ -379,7 +431,11 @@ __device__ __forceinline__ bool long_walk(const MeshView& m, const float4* __res
 // cycle guard.  On return `cur` is the terminating tet, `ref` the exit
 // reference, `vis` the visited count and `st` the status.  Shared by the
 // launch-per-128-rays kernel and the dynamically scheduled one.
-constexpr int kUnroll = 4;
+#ifndef TB_UNROLL
+#define TB_UNROLL 8  // r02 A/B: 8 vs 4 -- loop bookkeeping per step 1.25 -> 0.6 SASS (+0.5 ... +2 %)
+#endif
+constexpr int kUnroll = TB_UNROLL;
+static_assert(kUnroll == 4 || kUnroll == 8, "the unrolled walk body is written out for 4 or 8 steps");
 
 template <int L, bool kClamp>
 __device__ __forceinline__ void walk_ray(const MeshView& m, float o0, float o1, float o2, float d0, float d1,
@@ -403,24 +459,22 @@ __device__ __forceinline__ void walk_ray(const MeshView& m, float o0, float o1, 
   // only runs while all kUnroll steps fit under fast_limit; the exact
   // single-step loop below finishes the walk.
   // (The early exits add their own step count, so no per-step counter.)
-  static_assert(kUnroll == 4, "the unrolled body below is written out for 4 steps");
   while (ref < n_tets && vis + kUnroll <= (int)fast_limit) {
-    uint32_t nxt = ref;
-    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
-    cur = nxt;
-    if (ref >= n_tets) { vis += 1; break; }
+    uint32_t nxt;
+#define TB_WALK_STEP(k)                                   \
+    nxt = ref;                                            \
+    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);  \
+    cur = nxt;                                            \
+    if (ref >= n_tets) { vis += (k); break; }
+    TB_WALK_STEP(1) TB_WALK_STEP(2) TB_WALK_STEP(3)
+#if TB_UNROLL == 8
+    TB_WALK_STEP(4) TB_WALK_STEP(5) TB_WALK_STEP(6) TB_WALK_STEP(7)
+#endif
+#undef TB_WALK_STEP
     nxt = ref;
     ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
     cur = nxt;
-    if (ref >= n_tets) { vis += 2; break; }
-    nxt = ref;
-    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
-    cur = nxt;
-    if (ref >= n_tets) { vis += 3; break; }
-    nxt = ref;
-    ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
-    cur = nxt;
-    vis += 4;
+    vis += kUnroll;
   }
   while (ref < n_tets) {
     const uint32_t nxt = ref;
@@ -456,7 +510,7 @@ __device__ __forceinline__ void walk_ray(const MeshView& m, float o0, float o1, 
 // binning pass writes only the 8-byte permutation; with kScatter its results
 // go back to oidx[r] (oidx == ridx: the ray's own slot).
 template <int L, bool kClamp, bool kHostRays, bool kScatter, bool kGather = false>
-__global__ void __launch_bounds__(kCastBlock, TB_CAST_MIN_BLOCKS) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
+__global__ void __launch_bounds__(kCastBlock, (cast_min_blocks<L, kGather>())) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
                                                       const float* __restrict__ d,
                                                       const int32_t* __restrict__ start,
                                                       uint8_t* __restrict__ status, int32_t* __restrict__ cf,
@@ -507,6 +561,13 @@ __global__ void __launch_bounds__(kCastBlock, TB_CAST_MIN_BLOCKS) cast_kernel(Me
       return;
     }
   }
+#ifndef TB_NO_RELOAD_RAY
+  if constexpr (!kHostRays) {
+    const int64_t q = kGather ? __ldg(ridx + r) : r;
+    write_result_ray(m, w, st, ref, cur, vis, RayRef{o, d, q}, status, cf, tet, visited, triangle, t, tet_back);
+    return;
+  }
+#endif
   write_result(m, w, st, ref, cur, vis, o0, o1, o2, d0, d1, d2, status, cf, tet, visited, triangle, t,
                tet_back);
 }
