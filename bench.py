@@ -443,7 +443,7 @@ def issue_roof(layout: str, schedule: str, walk_steps: float, kern_s: float, clk
     entry = counts.get(f"{kname}<{layout[3:]}, validated>") or counts.get(f"{kname}<{layout[3:]}, clamp>")
     if not entry:
         return None
-    mix = entry.get("unrolled_x4_per_step") or entry["single_step"]
+    mix = next((v for k, v in entry.items() if k.startswith("unrolled_x")), None) or entry["single_step"]
     per_step, alu = mix["total"], mix["alu"]
     cycles = max(per_step, ALU_CYCLES_PER_INST * alu)
     peak_steps = sms * 4 * clk_mhz * 1e6 * 32 / cycles

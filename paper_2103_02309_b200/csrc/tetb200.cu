@@ -202,7 +202,11 @@ __global__ void validate_kernel(int layout, const int4* __restrict__ sv, const u
       if ((int64_t)other >= n_tets || (int64_t)other == t) { ok = false; break; }
       u = (uint32_t)other;  // then the face-sharing check below, expecting the tagged ref back
     } else if (u >= (uint64_t)n_tets) {
-      continue;  // boundary (or a corrupt plain ref): the walk stops there
+      // the boundary sentinel: the walk stops there.  Any other plain ref past
+      // the table is corrupt and keeps the clamped walk, so on a validated
+      // mesh "ref < n_tets" and "ref < kBoundary" agree (walk_ray's loop test)
+      if (u != kBoundary) { ok = false; break; }
+      continue;
     }
     if ((int64_t)u == t) { ok = false; break; }
     const uint32_t back = (nn[j] & kConstrained) ? nn[j] : (uint32_t)t;
@@ -452,20 +456,24 @@ __device__ __forceinline__ void walk_ray(const MeshView& m, float o0, float o1, 
   // Every plain tet reference is < n_tets; the boundary sentinel
   // (0x7FFFFFFF) and constrained refs (bit 31) are >= n_tets, so one
   // unsigned compare per step decides "keep walking" (corrupt refs also land
-  // outside and are classified below).
+  // outside and are classified below).  On a validated mesh every plain ref
+  // is < n_tets and every terminal one is >= kBoundary (validate_kernel), so
+  // the test is against the immediate kBoundary: no register and no per-step
+  // copy of n_tets (ptxas re-read it from a uniform register every step).
+  const uint32_t live = kClamp ? n_tets : kBoundary;
   const uint32_t fast_limit = n_tets < kCycleCheckAfter ? n_tets : kCycleCheckAfter;
   // Unrolled fast loop: the visited count and its threshold test once per
   // kUnroll steps (saves ~2.5 ALU-pipe ops per step, r01 A/B +1.5-3 %).  It
   // only runs while all kUnroll steps fit under fast_limit; the exact
   // single-step loop below finishes the walk.
   // (The early exits add their own step count, so no per-step counter.)
-  while (ref < n_tets && vis + kUnroll <= (int)fast_limit) {
+  while (ref < live && vis + kUnroll <= (int)fast_limit) {
     uint32_t nxt;
 #define TB_WALK_STEP(k)                                   \
     nxt = ref;                                            \
     ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);  \
     cur = nxt;                                            \
-    if (ref >= n_tets) { vis += (k); break; }
+    if (ref >= live) { vis += (k); break; }
     TB_WALK_STEP(1) TB_WALK_STEP(2) TB_WALK_STEP(3)
 #if TB_UNROLL == 8
     TB_WALK_STEP(4) TB_WALK_STEP(5) TB_WALK_STEP(6) TB_WALK_STEP(7)
@@ -476,7 +484,7 @@ __device__ __forceinline__ void walk_ray(const MeshView& m, float o0, float o1, 
     cur = nxt;
     vis += kUnroll;
   }
-  while (ref < n_tets) {
+  while (ref < live) {
     const uint32_t nxt = ref;
     ref = advance<L, kClamp>(m, P, b, idx, p, nxt, cur);
     cur = nxt;

@@ -229,6 +229,55 @@ __device__ __forceinline__ int init_ray(const MeshView& m, float o0, float o1, f
   // precomputed per tet at upload (orient_kernel, identical arithmetic)
   const bool rho_pos = __ldg(&m.orient[start]) != 0;
 
+#ifndef TB_INIT_LEGACY
+  // Start-face selection (_kernels.pyx:153-186), branch-free over the tet's
+  // six edges.  Face j's edge functions are 2-D cross products of its
+  // corners: unswapped (a, b, c) = (i < k < l) gives (d0, d1, d2) =
+  // (E_ik, E_kl, -E_il) with E_ik = q_i x q_k, and the swapped winding
+  // (i, l, k) gives (-d2, -d1, -d0) of that.  fl(u - v) = -fl(v - u) and
+  // products commute, so q_k x q_i is exactly -E_ik: six cross products
+  // instead of twelve, the same IEEE values (a zero may change sign, which
+  // no comparison below can see).  min(d0, d1, d2) keeps the reference's
+  // sequential "if d < m" NaN behaviour: NaN iff d0 is NaN.
+  float E[6];  // (0,1) (0,2) (0,3) (1,2) (1,3) (2,3)
+  {
+    const int ei[6] = {0, 0, 0, 1, 1, 2}, ek[6] = {1, 2, 3, 2, 3, 3};
+#pragma unroll
+    for (int e = 0; e < 6; ++e)
+      E[e] = __fsub_rn(__fmul_rn(q2[2 * ei[e]], q2[2 * ek[e] + 1]), __fmul_rn(q2[2 * ei[e] + 1], q2[2 * ek[e]]));
+  }
+  int sel = -1, best_j = -1;
+  float best_m = -3.4e38f;
+#pragma unroll
+  for (int j = 3; j >= 0; --j) {  // reversed: the first accepting face wins
+    // corners i < k < l of face j (SLOT_A/B/C, _kernels.pyx:105-111)
+    const int eik = (j == 0) ? 3 : ((j == 1) ? 1 : 0);  // (1,2) / (0,2) / (0,1) / (0,1)
+    const int ekl = (j == 0) ? 5 : ((j == 1) ? 5 : ((j == 2) ? 4 : 3));  // (2,3) (2,3) (1,3) (1,2)
+    const int eil = (j == 0) ? 4 : ((j == 1) ? 2 : ((j == 2) ? 2 : 1));  // (1,3) (0,3) (0,3) (0,2)
+    const bool sw = ((j & 1) == 0) != rho_pos;
+    const float A = E[eik], B = E[ekl], C = E[eil];
+    const float dd0 = sw ? C : A;
+    const float dd1 = sw ? -B : B;
+    const float dd2 = sw ? -A : -C;
+    const float mm = (dd0 != dd0) ? dd0 : fminf(fminf(dd0, dd1), dd2);
+    const bool acc = mm >= 0.0f && fmaxf(fmaxf(dd0, dd1), dd2) > 0.0f;
+    if (acc) sel = j;
+  }
+  // no accepting face: the first face of largest min (strictly greater)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int eik = (j == 0) ? 3 : ((j == 1) ? 1 : 0);
+    const int ekl = (j == 0) ? 5 : ((j == 1) ? 5 : ((j == 2) ? 4 : 3));
+    const int eil = (j == 0) ? 4 : ((j == 1) ? 2 : ((j == 2) ? 2 : 1));
+    const bool sw = ((j & 1) == 0) != rho_pos;
+    const float A = E[eik], B = E[ekl], C = E[eil];
+    const float dd0 = sw ? C : A;
+    const float dd1 = sw ? -B : B;
+    const float dd2 = sw ? -A : -C;
+    const float mm = (dd0 != dd0) ? dd0 : fminf(fminf(dd0, dd1), dd2);
+    if (mm > best_m) { best_m = mm; best_j = j; }
+  }
+#else
   int sel = -1, best_j = -1;
   float best_m = -3.4e38f;
 #pragma unroll
@@ -257,6 +306,7 @@ __device__ __forceinline__ int init_ray(const MeshView& m, float o0, float o1, f
       }
     }
   }
+#endif
   if (sel < 0) sel = best_j;
   // All-NaN windows (degenerate rays) leave best_j = -1; the reference reads
   // SLOT_A[-1] there (undefined behaviour).  Pin it to slot 0, the choice of
