@@ -142,11 +142,14 @@ __device__ __forceinline__ void project(const Basis& b, float qx, float qy, floa
 // PTX mul/sub.rn.f32x2 on register pairs).  The walk step is issue bound, so
 // the projection pairs (vmax*q.x, voth*q.y) -- the point copy's first two
 // words are already a register pair -- and the final (x1 - pox, y2 - poy):
-// 7 FMA-pipe instructions instead of 9.  Products and sums are each rounded
-// exactly as before.  Caution: ptxas contracts a single-use f32x2 product
-// into a following f32x2 add (FFMA2) even under -fmad=false; here every
-// f32x2 product feeds scalar adds or compares only, and tools/sass_steps.py
-// fails the build check if an FFMA/FFMA2 appears in a walk loop.
+// and (y1 + sgn*q.z) is one FFMA: sgn is +-1, so its product is exact and
+// the fused add rounds once, exactly like the separate multiply and add.
+// 6 FMA-pipe instructions instead of 9; every other product and sum is
+// rounded exactly as before.  Caution: ptxas contracts a single-use f32x2
+// product into a following f32x2 add (FFMA2) even under -fmad=false; here
+// every f32x2 product feeds scalar adds or compares only, and
+// tools/sass_steps.py fails the build check if a walk loop holds an FFMA2 or
+// more FFMA than these sign-fused adds.
 #ifndef TB_NO_F32X2
 #define TB_F32X2 1
 #endif
@@ -154,7 +157,7 @@ __device__ __forceinline__ void project_perm(const Basis& b, const float4& q, fl
 #ifdef TB_F32X2
   asm("{\n\t"
       ".reg .b64 s, c, m;\n\t"
-      ".reg .f32 m0, m1, ux, x1, y1, sc, y2;\n\t"
+      ".reg .f32 m0, m1, ux, x1, y1, y2;\n\t"
       "mov.b64 s, {%2, %3};\n\t"
       "mov.b64 c, {%6, %7};\n\t"
       "mul.rn.f32x2 m, s, c;\n\t"   // (vmax*q.x, voth*q.y)
@@ -162,8 +165,7 @@ __device__ __forceinline__ void project_perm(const Basis& b, const float4& q, fl
       "mul.rn.f32 ux, %5, %2;\n\t"  // umax*q.x
       "add.rn.f32 x1, ux, %3;\n\t"  // + q.y
       "add.rn.f32 y1, m0, m1;\n\t"
-      "mul.rn.f32 sc, %8, %4;\n\t"  // sgn*q.z
-      "add.rn.f32 y2, y1, sc;\n\t"
+      "fma.rn.f32 y2, %8, %4, y1;\n\t"  // y1 + sgn*q.z: sgn = +-1, the product is exact
       "mov.b64 s, {x1, y2};\n\t"
       "mov.b64 c, {%9, %10};\n\t"
       "sub.rn.f32x2 m, s, c;\n\t"   // (x1 - pox, y2 - poy)

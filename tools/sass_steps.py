@@ -118,10 +118,16 @@ def main(argv):
         # Checked on the single-step loop of every cast walk and the unrolled
         # loop of cast_kernel (the shadow / ScTP steps and the compact kernels'
         # refill hold IEEE divisions, whose expansions use FFMA legitimately).
+        # The one intended FFMA per step is project_perm's y1 + sgn * q.z (an
+        # exact product): a step with more, or any FFMA2, was contracted.
         checked = [one] + ([loops[-1]] if key.startswith("cast_kernel") else [])
-        fused = [x for body in checked for _, x in body if re.search(r"\bFFMA2?\b", x)]
-        if fused and key.startswith("cast"):
-            raise SystemExit(f"{key}: contracted FFMA in the walk loop: {fused[:3]}")
+        for body in checked:
+            steps = max(1, sum(re.sub(r"^@!?U?P\w+\s+", "", x).startswith("LDG") for _, x in body) //
+                        max(1, sum(re.sub(r"^@!?U?P\w+\s+", "", x).startswith("LDG") for _, x in one)))
+            ffma = [x for _, x in body if re.search(r"\bFFMA\b", x)]
+            ffma2 = [x for _, x in body if re.search(r"\bFFMA2\b", x)]
+            if key.startswith("cast") and (ffma2 or len(ffma) > steps):
+                raise SystemExit(f"{key}: contracted FFMA in the walk loop: {(ffma2 + ffma)[:3]}")
         entry = {"single_step": mix_of(one)}
         big = loops[-1]
         k = sum(re.sub(r"^@!?U?P\w+\s+", "", x).startswith("LDG") for _, x in big) // max(n_ld, 1)
