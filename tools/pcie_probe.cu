@@ -27,3 +27,194 @@ extern "C" int pcie_move(const void* in, int64_t in_bytes, void* out, int64_t ou
                                                     (uint4*)sink);
   return (int)cudaGetLastError();
 }
+
+// TMA bulk reads of pinned host memory (cp.async.bulk global -> shared, one
+// elected thread, mbarrier completion), 4-stage ring of 8 KB per block, plus
+// the same 16 B-per-lane zero-copy writes.  Asks whether the TMA engine's
+// PCIe read requests are cheaper on the upstream link than the SMs' 128 B
+// line reads (the zero-copy path's bidirectional floor, r01: 78.9 GB/s vs the
+// copy engines' 96).
+constexpr int kStage = 8192, kStages = 4;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__global__ void zc_bulk_move(const uint8_t* __restrict__ in, int64_t n_in, uint4* __restrict__ out, int64_t n_out,
+                             uint4* __restrict__ sink) {
+  __shared__ alignas(128) uint8_t buf[kStages][kStage];
+  __shared__ alignas(8) uint64_t bar[kStages];
+  const int64_t chunks = (n_in + kStage - 1) / kStage;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t c, int s) {
+    const int64_t off = c * kStage;
+    const uint32_t bytes = (uint32_t)((n_in - off) < kStage ? (n_in - off) : kStage);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(&buf[s][0])),
+                 "l"(in + off), "r"(bytes), "r"(smem_u32(&bar[s]))
+                 : "memory");
+  };
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  int k = 0;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kStages; ++s)
+      if (blockIdx.x + (int64_t)s * gridDim.x < chunks) issue(blockIdx.x + (int64_t)s * gridDim.x, s);
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x, ++k) {
+    const int s = k % kStages;
+    const uint32_t parity = (uint32_t)((k / kStages) & 1);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W%=;\n\t}" ::"r"(
+            smem_u32(&bar[s])),
+        "r"(parity)
+        : "memory");
+    const uint4* v = reinterpret_cast<const uint4*>(buf[s]);
+    for (int i = threadIdx.x; i < kStage / 16; i += blockDim.x) {
+      const uint4 x = v[i];
+      acc.x ^= x.x; acc.y ^= x.y; acc.z ^= x.z; acc.w ^= x.w;
+    }
+    __syncthreads();
+    const int64_t nxt = c + (int64_t)kStages * gridDim.x;
+    if (threadIdx.x == 0 && nxt < chunks) issue(nxt, s);
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_out; i += stride)
+    out[i] = make_uint4((uint32_t)i, acc.x, 0u, 0u);
+  if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x9E3779B9u) *sink = acc;
+}
+
+// Reads and writes interleaved per chunk (bulk reads of chunk c, 16 B writes of
+// the matching output range) so both link directions are busy throughout.
+__global__ void zc_bulk_both(const uint8_t* __restrict__ in, int64_t n_in, uint4* __restrict__ out, int64_t n_out,
+                             uint4* __restrict__ sink) {
+  __shared__ alignas(128) uint8_t buf[kStages][kStage];
+  __shared__ alignas(8) uint64_t bar[kStages];
+  const int64_t chunks = (n_in + kStage - 1) / kStage;
+  const int64_t out_per_chunk = (n_out / 16 + chunks - 1) / chunks;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t c, int s) {
+    const int64_t off = c * kStage;
+    const uint32_t bytes = (uint32_t)((n_in - off) < kStage ? (n_in - off) : kStage);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(&buf[s][0])),
+                 "l"(in + off), "r"(bytes), "r"(smem_u32(&bar[s]))
+                 : "memory");
+  };
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  int k = 0;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kStages; ++s)
+      if (blockIdx.x + (int64_t)s * gridDim.x < chunks) issue(blockIdx.x + (int64_t)s * gridDim.x, s);
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x, ++k) {
+    const int s = k % kStages;
+    const uint32_t parity = (uint32_t)((k / kStages) & 1);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W%=;\n\t}" ::"r"(
+            smem_u32(&bar[s])),
+        "r"(parity)
+        : "memory");
+    const uint4* v = reinterpret_cast<const uint4*>(buf[s]);
+    for (int i = threadIdx.x; i < kStage / 16; i += blockDim.x) {
+      const uint4 x = v[i];
+      acc.x ^= x.x; acc.y ^= x.y; acc.z ^= x.z; acc.w ^= x.w;
+    }
+    const int64_t o0 = c * out_per_chunk, o1 = (o0 + out_per_chunk < n_out / 16) ? o0 + out_per_chunk : n_out / 16;
+    for (int64_t i = o0 + threadIdx.x; i < o1; i += blockDim.x) out[i] = make_uint4((uint32_t)i, acc.x, 0u, 0u);
+    __syncthreads();
+    const int64_t nxt = c + (int64_t)kStages * gridDim.x;
+    if (threadIdx.x == 0 && nxt < chunks) issue(nxt, s);
+  }
+  if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x9E3779B9u) *sink = acc;
+}
+
+extern "C" int pcie_bulk(const void* in, int64_t in_bytes, void* out, int64_t out_bytes, void* sink, int grid,
+                         int block, int both, void* stream) {
+  if (both)
+    zc_bulk_both<<<grid, block, 0, (cudaStream_t)stream>>>((const uint8_t*)in, in_bytes, (uint4*)out, out_bytes,
+                                                           (uint4*)sink);
+  else
+    zc_bulk_move<<<grid, block, 0, (cudaStream_t)stream>>>((const uint8_t*)in, in_bytes, (uint4*)out, out_bytes,
+                                                           (uint4*)sink);
+  return (int)cudaGetLastError();
+}
+
+// TMA bulk writes (cp.async.bulk shared -> global, bulk_group completion) of
+// 8 KB chunks from shared memory to pinned host memory, optionally with the
+// bulk reads above in the same loop (mode 1 = write only, 2 = read + write).
+__global__ void zc_bulk_write(const uint8_t* __restrict__ in, int64_t n_in, uint8_t* __restrict__ out,
+                              int64_t n_out, uint4* __restrict__ sink, int with_reads) {
+  __shared__ alignas(128) uint8_t buf[kStages][kStage];
+  __shared__ alignas(128) uint8_t obuf[kStage];
+  __shared__ alignas(8) uint64_t bar[kStages];
+  const int64_t ochunks = (n_out + kStage - 1) / kStage;
+  const int64_t chunks = with_reads ? (n_in + kStage - 1) / kStage : 0;
+  for (int i = threadIdx.x; i < kStage / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(obuf)[i] = i;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  auto issue = [&](int64_t c, int s) {
+    const int64_t off = c * kStage;
+    const uint32_t bytes = (uint32_t)((n_in - off) < kStage ? (n_in - off) : kStage);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(&buf[s][0])),
+                 "l"(in + off), "r"(bytes), "r"(smem_u32(&bar[s]))
+                 : "memory");
+  };
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kStages; ++s)
+      if (blockIdx.x + (int64_t)s * gridDim.x < chunks) issue(blockIdx.x + (int64_t)s * gridDim.x, s);
+  const int64_t iters = chunks > ochunks ? chunks : ochunks;
+  int k = 0;
+  for (int64_t c = blockIdx.x; c < iters; c += gridDim.x, ++k) {
+    if (c < chunks) {
+      const int s = k % kStages;
+      const uint32_t parity = (uint32_t)((k / kStages) & 1);
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tW%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W%=;\n\t}" ::"r"(
+              smem_u32(&bar[s])),
+          "r"(parity)
+          : "memory");
+      const uint4* v = reinterpret_cast<const uint4*>(buf[s]);
+      for (int i = threadIdx.x; i < kStage / 16; i += blockDim.x) {
+        const uint4 x = v[i];
+        acc.x ^= x.x; acc.y ^= x.y; acc.z ^= x.z; acc.w ^= x.w;
+      }
+    }
+    if (threadIdx.x == 0 && c < ochunks) {
+      const int64_t off = c * kStage;
+      const uint32_t bytes = (uint32_t)((n_out - off) < kStage ? (n_out - off) : kStage);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + off),
+                   "r"(smem_u32(obuf)), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t nxt = c + (int64_t)kStages * gridDim.x;
+    if (threadIdx.x == 0 && nxt < chunks) issue(nxt, k % kStages);
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x9E3779B9u) *sink = acc;
+}
+
+extern "C" int pcie_bulk_write(const void* in, int64_t in_bytes, void* out, int64_t out_bytes, void* sink, int grid,
+                               int block, int with_reads, void* stream) {
+  zc_bulk_write<<<grid, block, 0, (cudaStream_t)stream>>>((const uint8_t*)in, in_bytes, (uint8_t*)out, out_bytes,
+                                                          (uint4*)sink, with_reads);
+  return (int)cudaGetLastError();
+}

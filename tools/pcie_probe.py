@@ -32,6 +32,9 @@ def build() -> ctypes.CDLL:
     lib = ctypes.CDLL(so)
     lib.pcie_move.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                               ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+    for f in (lib.pcie_bulk, lib.pcie_bulk_write):
+        f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                      ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
     return lib
 
 
@@ -54,6 +57,8 @@ def main():
     ap.add_argument("--in-mb", type=float, default=2_073_600 * 28 / 1e6)
     ap.add_argument("--out-mb", type=float, default=2_073_600 * 29 / 1e6)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--bulk", choices=("off", "device", "host"), default="off",
+                    help="TMA bulk-copy probes on device buffers (a self-check) or on pinned host buffers")
     args = ap.parse_args()
     lib = build()
     dev = torch.device("cuda", 0)
@@ -74,6 +79,22 @@ def main():
         rows.append(row)
         print(json.dumps(row), flush=True)
 
+    if args.bulk != "off":
+        src, dst = (din, dout) if args.bulk == "device" else (hin, hout)
+        g = sms * 2
+        for name, fn, nb in (
+                ("bulk_read", lambda: lib.pcie_bulk(src.data_ptr(), nin, None, 0, sink.data_ptr(), g, 256, 0,
+                                                    s.cuda_stream), nin),
+                ("bulk_read_zc_write", lambda: lib.pcie_bulk(src.data_ptr(), nin, dst.data_ptr(), nout,
+                                                             sink.data_ptr(), g, 256, 1, s.cuda_stream), nin + nout),
+                ("bulk_write", lambda: lib.pcie_bulk_write(None, 0, dst.data_ptr(), nout, sink.data_ptr(), g, 256, 0,
+                                                           s.cuda_stream), nout),
+                ("bulk_read_bulk_write", lambda: lib.pcie_bulk_write(src.data_ptr(), nin, dst.data_ptr(), nout,
+                                                                     sink.data_ptr(), g, 256, 1, s.cuda_stream),
+                 nin + nout)):
+            rec(name, timed(fn, args.reps, s), nb, memory=args.bulk, grid=g, block=256)
+        torch.cuda.synchronize()
+        return
     for grid_mul, block in ((1, 256), (4, 256), (8, 256), (16, 256), (8, 128), (8, 512)):
         g = sms * grid_mul
         tag = {"grid": g, "block": block}
