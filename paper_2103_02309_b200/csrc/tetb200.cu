@@ -96,9 +96,16 @@ constexpr int kCastBlock = TB_CAST_BLOCK;
 #ifndef TB_CAST_MIN_BLOCKS_LATENCY
 #define TB_CAST_MIN_BLOCKS_LATENCY (1536 / TB_CAST_BLOCK)
 #endif
+// ... except the binned Tet20 walk, whose 20 B records (two loads) do not fit
+// 40 registers without spilling into the step: 10 blocks, r02 A/B config-2
+// frame secondaries 2237 -> 2487 Mrays/s, config-4 rays on Tet20 3200 -> 3385.
+#ifndef TB_GATHER20_MIN_BLOCKS
+#define TB_GATHER20_MIN_BLOCKS TB_CAST_MIN_BLOCKS
+#endif
 template <int L, bool kGather>
 constexpr int cast_min_blocks() {
-  return (L == 32 || kGather) ? TB_CAST_MIN_BLOCKS_LATENCY : TB_CAST_MIN_BLOCKS;
+  return (L == 20 && kGather) ? TB_GATHER20_MIN_BLOCKS
+                              : ((L == 32 || kGather) ? TB_CAST_MIN_BLOCKS_LATENCY : TB_CAST_MIN_BLOCKS);
 }
 
 struct DeviceGuard {

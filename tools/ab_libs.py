@@ -78,6 +78,8 @@ def main():
     stream = torch.cuda.current_stream(dev)
     for c in [int(x) for x in args.configs.split(",")]:
         cfg = CONFIGS[c]
+        if os.environ.get("AB_LAYOUT"):  # this config's scene and rays on another record layout
+            cfg = dict(cfg, layout=os.environ["AB_LAYOUT"])
         sc = build_scene(cfg)
         mesh = sc.mesh
         o, d, pos = frame_rays(cfg, 0)
@@ -91,7 +93,7 @@ def main():
                         torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))
         st = np.full(len(o), int(cam.item()), np.int32)
         sched = 1
-        if cfg.get("secondaries"):
+        if cfg.get("secondaries") or os.environ.get("AB_SECONDARIES"):
             from paper_2103_02309_b200.scenes import diffuse_secondaries
 
             prim = trace(dm, *(torch.from_numpy(x).to(dev) for x in (o, d, st)))
