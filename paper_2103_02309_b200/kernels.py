@@ -13,10 +13,29 @@ host (batch.py:57-71).
 
 from __future__ import annotations
 
+import ctypes
+import os
+
 import numpy as np
 
-from ._lib import addr, check, lib
+from ._lib import TetB200Error, addr, check, lib
 from .device import device_mesh
+
+# Per-tile fast path (csrc/fastcall.c): the same tb_cast_rays_host call with
+# the argument handling in C and the GIL released -- the reference renderer
+# calls cast_rays per 16x16 tile from a thread pool, where the backend's
+# GIL-held time is what limits it.  Built with the library (make); without
+# it every call takes the ctypes path below (same kernel, same results).
+try:
+    from . import _fastcall
+
+    if os.environ.get("TETB200_NO_FASTCALL"):  # A/B knob: the ctypes path only
+        raise ImportError
+except ImportError:  # pragma: no cover - the Makefile builds it with the library
+    _fastcall = None
+else:
+    _fastcall.bind(ctypes.cast(lib.tb_cast_rays_host, ctypes.c_void_p).value,
+                   ctypes.cast(lib.tb_last_error, ctypes.c_void_p).value, TetB200Error)
 
 BACKEND_NAME = "cuda"
 
@@ -96,6 +115,12 @@ def cast_rays(mesh, o32, d32, start, visits_sink=None):
     ``batch.cast_rays_visits`` consumes (batch.py:101-114).
     """
     if visits_sink is None:
+        if _fastcall is not None:
+            dm = device_mesh(mesh)
+            r = _fastcall.cast4(dm.handle.value or 0, mesh.n_tets, o32, d32, start)
+            if r is not None:
+                _check_cf(dm, mesh, r[0], r[1])
+                return r
         status, cf, tet, visited, *_ = _cast_plain(mesh, o32, d32, start)
         return status, cf, tet, visited
     status, cf, tet, visited, seq, offsets = cast_rays_csr(mesh, o32, d32, start)

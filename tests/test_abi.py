@@ -187,3 +187,40 @@ def test_multi_gpu_entry_points_validate_arguments():
     assert lib.tb_mesh_replicate(None, 0, ctypes.byref(out)) == -1
     assert b"NULL" in lib.tb_last_error()
     assert lib.tb_cast_epilogue(None, 1, *(None,) * 7, None) == -1
+
+
+def test_fastcall_extension_is_built_and_bound():
+    """The per-tile fast path of kernels.cast_rays (csrc/fastcall.c) is built
+    with the library and bound to the same libtetb200.so the ctypes path uses."""
+    from paper_2103_02309_b200 import kernels
+
+    assert kernels._fastcall is not None
+    assert kernels._fastcall.__file__.startswith(str(ROOT / "paper_2103_02309_b200"))
+
+
+def test_fastcall_declines_other_layouts_and_checks_arguments():
+    """cast4 returns None (the caller takes the general path) for anything but
+    contiguous float32 (n, 3) / int32 (n,) inputs, and raises what the ctypes
+    path raises: ValueError on a length mismatch, IndexError on a start tet
+    outside the mesh, TetB200Error from the C ABI (here: a NULL mesh handle)."""
+    import numpy as np
+
+    from paper_2103_02309_b200 import kernels
+    from paper_2103_02309_b200._lib import TetB200Error
+
+    f = kernels._fastcall.cast4
+    o = np.zeros((4, 3), np.float32)
+    d = np.ones((4, 3), np.float32)
+    st = np.zeros(4, np.int32)
+    assert f(0, 10, o.astype(np.float64), d, st) is None
+    assert f(0, 10, o, d[::2].repeat(2, 0)[:, :2], st) is None
+    assert f(0, 10, o, d, st.astype(np.int64)) is None
+    assert f(0, 10, np.asfortranarray(np.zeros((4, 3), np.float32)), d, st) is None  # F-order
+    with pytest.raises(ValueError, match="length mismatch"):
+        f(0, 10, o[:3], d, st)
+    with pytest.raises(IndexError, match=r"start\[2\] = 10"):
+        f(0, 10, o, d, np.array([0, 1, 10, 2], np.int32))
+    with pytest.raises(TetB200Error, match="NULL"):
+        f(0, 10, o, d, st)
+    status, cf, tet, visited = f(0, 10, o[:0], d[:0], st[:0])
+    assert status.dtype == np.uint8 and cf.dtype == tet.dtype == visited.dtype == np.int32 and len(status) == 0

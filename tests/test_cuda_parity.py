@@ -663,3 +663,22 @@ def test_cast_epilogue_equals_fused_epilogue(golden):
         assert int((full.status == 1).sum()) > 0 and int((full.status == 0).sum()) >= 0
         for k in ("triangle", "t", "tet_back"):
             assert torch.equal(getattr(out, k), getattr(full, k)), (layout, k)
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_fastcall_equals_ctypes_path(golden, digests, K, name):
+    """kernels.cast_rays' C fast path (csrc/fastcall.c, the per-tile call the
+    reference renderer makes) and the general ctypes path return identical
+    arrays, equal to the reference's digest; tile-sized calls too."""
+    assert K._fastcall is not None
+    m = golden_mesh(golden, name, "tet20")
+    o, d, st = _rays(m, name)
+    fast = K.cast_rays(m, o, d, st)
+    plain = K._cast_plain(m, o, d, st)[:4]
+    assert digest(*fast) == digests[f"{name}/tet20/cast10k"]
+    for a, b in zip(fast, plain):
+        assert a.dtype == b.dtype and np.array_equal(a, b)
+    for a0 in range(0, 2048, 256):
+        tile = K.cast_rays(m, o[a0:a0 + 256], d[a0:a0 + 256], st[a0:a0 + 256])
+        for a, b in zip(tile, plain):
+            assert np.array_equal(a, b[a0:a0 + 256])
