@@ -576,8 +576,7 @@ __device__ __forceinline__ uint32_t decide<16>(const Record<16>& rec, uint32_t (
       "selp.b32 lo, %14, %13, q0;\n\t"
       "selp.b32 hi, 0, %15, q0;\n\t"
       "selp.b32 lo, hi, lo, q1;\n\t"
-      "xor.b32 %0, %16, rk;\n\t"
-      "xor.b32 %0, %0, lo;\n\t" TB_STEP_TAIL
+      "lop3.b32 %0, %16, rk, lo, 0x96;\n\t" TB_STEP_TAIL  // prev ^ nx[rank] ^ nx[order_a], one LOP3
       : TB_STEP_OUTS
       : "f"(qx), "f"(qy), "r"(i3), "r"(rec.r.y), "r"(rec.r.z), "r"(rec.r.w), "r"(prev));
   return nref;
