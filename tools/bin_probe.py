@@ -51,6 +51,11 @@ def main():
                   torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))
     W = H = args.size
     o, d = camera_rays(cam["position"], cam["look_at"], cam["up"], cam["fov"], W, H)
+    if os.environ.get("BIN_TILES"):  # the reference renderer's 16x16-tile ray order (bench.py config 4)
+        from paper_2103_02309_b200.multigpu import shard_pixels
+
+        tiles = shard_pixels(W, H, 0, 1, 16)
+        o, d = o[tiles], d[tiles]
     st = np.full(len(o), int(c.item()), np.int32)
     prim = trace(dm, *(torch.from_numpy(a).to(dev) for a in (o, d, st)))
     torch.cuda.synchronize()
@@ -78,6 +83,12 @@ def main():
         if k in (2, 4):
             for shift in (8, 12, 16):
                 keys[f"cube{k},start>>{shift}"] = (keys[f"cube{k}"] << 40) | (start >> shift)
+    # the production order (schedule "binned"): stable by (256 K-ray segment, cube4 cell),
+    # and the same with a spatial sub-key inside each cell: the start tet's Hilbert id
+    seg = torch.arange(n, device=dev, dtype=torch.long) >> 18
+    keys["seg,cube4"] = (seg << 50) | (keys["cube4"] << 40)
+    for shift in (6, 8, 10, 12, 14):
+        keys[f"seg,cube4,start>>{shift}"] = (seg << 50) | (keys["cube4"] << 40) | (start >> shift)
     ref = None
     only = os.environ.get("BIN_KEYS")
     for name, key in keys.items():
