@@ -606,7 +606,9 @@ def run_ours(args, cfg):
                     frs = [frame_rays(cfg, f)[:2] for f in range(world)]
                     root_rays = tuple(torch.from_numpy(np.ascontiguousarray(np.concatenate([fr[i] for fr in frs])))
                                       .to(dev) for i in (0, 1))
-            pg = multigpu.PeerFrameGather(W, H, world, rank, world, dev, root_rays=root_rays, index=idx)
+            # pipelined: rank 0's whole-job epilogue of step k overlaps step k+1's trace
+            pg = multigpu.PeerFrameGather(W, H, world, rank, world, dev, root_rays=root_rays, index=idx,
+                                          pipelined=lean)
             gather_mode = "p2p"
 
             def step():  # noqa: F811  (the N > 1 step: fused trace + frame assembly)
@@ -637,6 +639,8 @@ def run_ours(args, cfg):
     for _ in range(args.warmup):
         flush.zero_()
         step()
+    if pg is not None:
+        pg.finish()
     torch.cuda.synchronize()
     if pg is not None and rank == 0:
         # p2p: this rank's hits live in the root's frame
@@ -713,6 +717,12 @@ def run_ours(args, cfg):
             evs[i][0].record(stream)
             step()
             evs[i][1].record(stream)
+        if pg is not None and pg.pipelined:
+            # the last step's pipelined root epilogue belongs to the timed work
+            evs.append((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)))
+            evs[-1][0].record(stream)
+            pg.finish()
+            evs[-1][1].record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
         clocks.mark("t_end")
@@ -724,6 +734,8 @@ def run_ours(args, cfg):
         # N > 1: the assembled frame set of the last step, checked on rank 0
         try:
             full = step()
+            if pg is not None:
+                full = pg.finish()
             torch.cuda.synchronize()
             if full is not None:
                 gather_check = {"rays_in_frame": int((full["visited"] > 0).sum().item())}
@@ -781,6 +793,8 @@ def run_ours(args, cfg):
             # each rank: its rays host -> HBM, the fused trace + frame assembly
             # into rank 0, and rank 0 copies the assembled job back to the host
             full0 = step()  # every rank (the step may hold collectives); rank 0 gets the frame set
+            if pg is not None:
+                full0 = pg.finish()
             fr_host = None
             if rank == 0:
                 fr_host = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in full0.items()}
@@ -790,6 +804,8 @@ def run_ours(args, cfg):
                 gd.copy_(hd, non_blocking=True)
                 gs.copy_(hs, non_blocking=True)
                 full = step()
+                if pg is not None:
+                    full = pg.finish()  # this step's frame set, complete
                 if rank == 0:
                     for k2, v2 in full.items():
                         fr_host[k2].copy_(v2, non_blocking=True)

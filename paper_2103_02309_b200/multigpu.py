@@ -270,9 +270,19 @@ class PeerFrameGather:
     cf / triangle / tet / tet_back -1, t +inf, visited 0) written once at
     setup.
 
-    Two frame buffers alternate between steps, so a rank that runs ahead into
-    step k+1 writes the other buffer while the root still reads step k's
-    (every rank passes step k's closing barrier before any starts k+2).
+    Two frame buffers alternate between steps (three when pipelined), so a
+    rank that runs ahead into step k+1 writes another buffer while the root
+    still reads the frame it returned (every rank passes step k's closing
+    barrier before any starts k+2).
+
+    ``pipelined`` (lean assembly): the root's whole-job epilogue of step k
+    runs on a side stream during step k+1 -- concurrently with the root's own
+    trace of step k+1, which writes the other buffer -- and is joined before
+    step k+1's closing barrier, so no rank touches buffer k again before it is
+    finished.  Without it the epilogue follows the barrier and every rank
+    waits for it (at N GPUs it covers N frames, while each rank traces one).
+    ``step`` then returns the most recent *completed* frame set (step k's
+    after step k+1); ``finish()`` completes the last one.
 
     ``root_rays``: lean assembly.  Every rank passes it -- the root the job's
     full (origins, dirs) device tensors in global ray order, the others
@@ -283,10 +293,10 @@ class PeerFrameGather:
     pass this step's rays (``root_rays=``) when they change between steps.
     """
 
-    BUFFERS = 2
+    BUFFERS = 2  # 3 when pipelined (the frame returned by step k+1 is step k's)
 
     def __init__(self, width, height, world, rank, frames, device, root=0, group=None, tile=16, root_rays=None,
-                 index=None):
+                 index=None, pipelined=False):
         import ctypes
 
         import torch
@@ -297,6 +307,12 @@ class PeerFrameGather:
         self.world, self.rank, self.root, self.group = world, rank, root, group
         self.lean = root_rays is not None
         self.root_rays = root_rays if (self.lean and rank == root) else None
+        self.pipelined = bool(pipelined) and self.lean
+        # pipelined, step k+1 returns step k's frame; a rank running ahead into
+        # step k+2 must not touch it, hence a third buffer
+        self.buffers = self.BUFFERS + (1 if self.pipelined else 0)
+        self.pending = None  # (buffer, rays) whose root epilogue has not run yet
+        self.epi_stream = None
         self.device = torch.device(device)
         self.total = width * height * frames
         shard = shard_pixels(width, height, rank, world, tile, frames) if index is None else np.asarray(index)
@@ -309,7 +325,7 @@ class PeerFrameGather:
             self.offsets.append(off)
             off += (size * self.total + 255) // 256 * 256
         self.frame_bytes = off
-        self.bytes = off * self.BUFFERS
+        self.bytes = off * self.buffers
         self.base = None
         self.remote = None
         self.steps = 0
@@ -351,13 +367,13 @@ class PeerFrameGather:
                 self.base = None
             raise RuntimeError(f"peer frame assembly unavailable: {failed[0] if failed else 'no IPC handle'}")
         dest = self.base if rank == root else self.remote
-        self.ptrs = [[dest + b * self.frame_bytes + o for o in self.offsets] for b in range(self.BUFFERS)]
+        self.ptrs = [[dest + b * self.frame_bytes + o for o in self.offsets] for b in range(self.buffers)]
         self.frames = None
         if rank == root:
             fills = {"status": 0, "cf": -1, "tet": -1, "visited": 0, "triangle": -1, "t": float("inf"),
                      "tet_back": -1}
             self.frames = []
-            for b in range(self.BUFFERS):
+            for b in range(self.buffers):
                 fr = {name: torch.as_tensor(_CudaArray(self.base + b * self.frame_bytes + o, self.total, ts),
                                             device=self.device)
                       for (name, ts, _), o in zip(_OUTPUTS, self.offsets)}
@@ -372,7 +388,32 @@ class PeerFrameGather:
         """The root's most recently completed frame (None on other ranks)."""
         if self.frames is None:
             return None
-        return self.frames[(self.steps - 1) % self.BUFFERS if self.steps else 0]
+        done = self.steps - (1 if self.pending is not None else 0)
+        return self.frames[(done - 1) % self.buffers if done else 0]
+
+    def _epilogue(self, ptrs, rays, stream):
+        from ._lib import addr, check, lib
+
+        ro, rd = rays
+        if ro.shape[0] != self.total or rd.shape[0] != self.total:
+            raise ValueError(f"root_rays must hold the job's {self.total} rays")
+        check(lib.tb_cast_epilogue(self._dm.handle, self.total, addr(ro), addr(rd), ptrs[1], ptrs[2], ptrs[4],
+                                   ptrs[5], ptrs[6], stream.cuda_stream), "tb_cast_epilogue")
+
+    def finish(self):
+        """Complete a pipelined step's pending root epilogue; returns the
+        root's latest frame (None on other ranks)."""
+        import torch
+
+        if self.pending is not None:
+            ptrs, rays, evs = self.pending
+            s = torch.cuda.current_stream(self.device)
+            for ev in evs:
+                s.wait_event(ev)
+            self._epilogue(ptrs, rays, s)
+            s.synchronize()
+            self.pending = None
+        return self.frame
 
     def step(self, dm, origins, dirs, start, stream=None, *, schedule="lane", sctp=False, root_rays=None):
         """Trace this rank's rays into the root's frame; returns the frame on
@@ -389,7 +430,16 @@ class PeerFrameGather:
             raise ValueError(f"this rank traces {n} rays (its index), got {origins.shape[0]} origins, "
                              f"{dirs.shape[0]} dirs, {start.numel()} starts")
         s = stream or torch.cuda.current_stream(self.device)
-        ptrs = self.ptrs[self.steps % self.BUFFERS]
+        ptrs = self.ptrs[self.steps % self.buffers]
+        self._dm = dm
+        epi = None
+        if self.pending is not None:  # pipelined: the previous step's root epilogue, beside this trace
+            if self.epi_stream is None:
+                self.epi_stream = torch.cuda.Stream(self.device)
+            epi = self.pending
+            for ev in epi[2]:  # the rays were produced in the caller's stream order
+                self.epi_stream.wait_event(ev)
+            self._epilogue(epi[0], epi[1], self.epi_stream)
         # _OUTPUTS order: status, cf, tet, visited, triangle, t, tet_back
         outs = ptrs[:4] + [None, None, None] if self.lean else ptrs
         if sctp:
@@ -401,15 +451,25 @@ class PeerFrameGather:
                                                  addr(self.idx), *outs, mode, s.cuda_stream),
                   "tb_cast_rays_scatter_sched")
         s.synchronize()  # this rank's stores have landed in the root's memory
+        if epi is not None:
+            self.epi_stream.synchronize()  # buffer k is finished before anyone passes this barrier
+            self.pending = None
         dist.barrier(group=self.group)
         self.steps += 1
         if self.rank == self.root and self.lean:
-            ro, rd = root_rays if root_rays is not None else self.root_rays
-            if ro.shape[0] != self.total or rd.shape[0] != self.total:
+            rays = root_rays if root_rays is not None else self.root_rays
+            if rays[0].shape[0] != self.total or rays[1].shape[0] != self.total:
                 raise ValueError(f"root_rays must hold the job's {self.total} rays")
-            check(lib.tb_cast_epilogue(dm.handle, self.total, addr(ro), addr(rd), ptrs[1], ptrs[2], ptrs[4], ptrs[5],
-                                       ptrs[6], s.cuda_stream), "tb_cast_epilogue")
-            s.synchronize()
+            if self.pipelined:
+                evs = []
+                for st in {s, torch.cuda.current_stream(self.device)}:
+                    ev = torch.cuda.Event()
+                    ev.record(st)
+                    evs.append(ev)
+                self.pending = (ptrs, rays, evs)
+            else:
+                self._epilogue(ptrs, rays, s)
+                s.synchronize()
         return self.frame
 
     def close(self):
@@ -417,6 +477,7 @@ class PeerFrameGather:
 
         from ._lib import lib
 
+        self.pending = None  # a pipelined step's unfinished epilogue dies with the frames
         if self.remote is not None:
             lib.tb_ipc_close(self.remote)
             self.remote = None

@@ -25,6 +25,8 @@ def _free_port():
 
 def _worker(rank, world, port, result_path, mode="full"):
     """mode: "full" (29 B per ray stored), "lean" (13 B, root epilogue),
+    "pipelined" (lean, the root epilogue of step k run beside step k+1;
+    each step returns the previous job's frame, finish() the last one),
     "binned" (the binned walk's permutation composed with the scatter
     index), "sctp" (the ScTP walk scattering), "partial" (each rank traces
     a data-dependent subset -- like diffuse secondaries of primary hits --
@@ -61,8 +63,8 @@ def _worker(rank, world, port, result_path, mode="full"):
                 st_all.append(np.full(len(o), cam[0], np.int32))
             return [np.concatenate(a) for a in (o_all, d_all, st_all)]
 
-        jobs = [job(0.0), job(0.13)]
-        lean = mode == "lean"
+        jobs = [job(0.0), job(0.13)] + ([job(0.21)] if mode == "pipelined" else [])
+        lean = mode in ("lean", "pipelined")
         index = None
         if mode == "partial":  # drop every third ray of this rank's shard
             shard = multigpu.shard_pixels(W, H, rank, world, 16, frames)
@@ -70,14 +72,25 @@ def _worker(rank, world, port, result_path, mode="full"):
         root_rays = None
         if lean:
             root_rays = tuple(torch.from_numpy(a).to(dev) for a in jobs[0][:2]) if rank == 0 else True
-        pg = multigpu.PeerFrameGather(W, H, world, rank, frames, dev, root_rays=root_rays, index=index)
+        pg = multigpu.PeerFrameGather(W, H, world, rank, frames, dev, root_rays=root_rays, index=index,
+                                      pipelined=mode == "pipelined")
         idx = pg.idx.cpu().numpy()
         dm = device_mesh(mesh, device=0)
         schedule = "binned" if mode in ("binned", "partial") else "lane"
-        for o_all, d_all, st_all in jobs:  # reusable frame after frame, rays changing
+        names = ("status", "cf", "tet", "visited", "triangle", "t", "tet_back")
+        lagged_ok = True
+        for k, (o_all, d_all, st_all) in enumerate(jobs):  # reusable frame after frame, rays changing
             g = [torch.from_numpy(np.ascontiguousarray(a[idx])).to(dev) for a in (o_all, d_all, st_all)]
             rr = tuple(torch.from_numpy(a).to(dev) for a in (o_all, d_all)) if (lean and rank == 0) else None
             frame = pg.step(dm, *g, schedule=schedule, sctp=mode == "sctp", root_rays=rr)
+            if mode == "pipelined" and rank == 0 and k >= 1:  # step k returns job k-1, complete
+                prev = pyoracle.cast_rays_full(mesh, *jobs[k - 1], n_threads=1)
+                bad = [nm for nm, e in zip(names, prev) if not np.array_equal(frame[nm].cpu().numpy(), e)]
+                if bad:
+                    lagged_ok = False
+                    print(f"pipelined step {k}: lagged frame differs in {bad}", flush=True)
+        if mode == "pipelined":
+            frame = pg.finish()
         with pytest.raises(ValueError):  # the ray count must match the rank's index
             pg.step(dm, g[0][:-1], g[1][:-1], g[2][:-1])
         if rank == 0:
@@ -90,8 +103,10 @@ def _worker(rank, world, port, result_path, mode="full"):
                     traced[sh[np.arange(len(sh)) % 3 != 1]] = True
                 for e, fill in zip(exp, (0, -1, -1, 0, -1, np.inf, -1)):
                     e[~traced] = fill
-            ok = all(np.array_equal(frame[k].cpu().numpy(), e) for k, e in
-                     zip(("status", "cf", "tet", "visited", "triangle", "t", "tet_back"), exp))
+            bad = [k for k, e in zip(names, exp) if not np.array_equal(frame[k].cpu().numpy(), e)]
+            if bad:
+                print(f"{mode}: final frame differs in {bad}", flush=True)
+            ok = lagged_ok and not bad
             with open(result_path, "w") as fh:
                 fh.write("ok" if ok else "mismatch")
         pg.close()
@@ -100,7 +115,7 @@ def _worker(rank, world, port, result_path, mode="full"):
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("mode", ("full", "lean", "binned", "sctp", "partial"))
+@pytest.mark.parametrize("mode", ("full", "lean", "pipelined", "binned", "sctp", "partial"))
 def test_p2p_frame_assembly_two_ranks(tmp_path, mode):
     """Two ranks (sharing cuda:0 here) assemble the frame set on rank 0 by P2P
     stores, in every mode (see _worker); the frame equals the oracle."""
