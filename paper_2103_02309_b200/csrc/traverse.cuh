@@ -624,7 +624,16 @@ __device__ __forceinline__ uint32_t advance(const MeshView& m, const float4* __r
                                             uint32_t (&idx)[3], float (&p)[6], uint32_t nxt, uint32_t prev) {
   Record<L> rec;
   rec.load(m, nxt);
+#ifndef TB_NO_XOR_EARLY
+  // idx0 ^ idx1 ^ idx2 formed before the record arrives (opaque to ptxas,
+  // which otherwise folds vx in first): one LOP3 between the vx load and the
+  // point address instead of two (r02 A/B +0.4 ... +1.5 %)
+  uint32_t wx;
+  asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(wx) : "r"(idx[0]), "r"(idx[1]), "r"(idx[2]));
+  uint32_t i3 = wx ^ rec.vxw();
+#else
   uint32_t i3 = idx[0] ^ idx[1] ^ idx[2] ^ rec.vxw();
+#endif
   float qx, qy;
   if constexpr (L != 80) {
     if (kClamp) i3 = min(i3, (uint32_t)m.n_points - 1u);  // corrupt record: stay in bounds

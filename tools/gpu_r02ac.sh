@@ -1,0 +1,10 @@
+#!/bin/bash
+# round-2: window xor formed before the record arrives (one LOP3 on the load chain) -- parity + A/B
+TAG=${1:-r02ac}; OUT=gpurun_out/$TAG; mkdir -p $OUT
+cp varlibs/xe.so paper_2103_02309_b200/libtetb200.so
+timeout 900 python -m pytest tests/test_cuda_parity.py tests/test_cuda_edge_cases.py tests/test_full_size_parity.py -m gpu -q -x > $OUT/pytest.log 2>&1; echo "rc=$?" >> $OUT/pytest.log
+L="varlibs/base3.so varlibs/xe.so"
+AB_TILES=1 timeout 1200 python tools/ab_libs.py $L --configs 2,3,5 --reps 10 --rounds 3 > $OUT/ab.jsonl 2> $OUT/ab.err
+AB_TILES=1 AB_SCHED=6 timeout 900 python tools/ab_libs.py $L --configs 4 --reps 5 --rounds 3 >> $OUT/ab.jsonl 2>> $OUT/ab.err
+AB_TILES=1 AB_SCHED=6 AB_SECONDARIES=1 timeout 900 python tools/ab_libs.py $L --configs 2 --reps 10 --rounds 3 >> $OUT/ab.jsonl 2>> $OUT/ab.err
+echo done
