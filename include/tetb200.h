@@ -171,6 +171,25 @@ int tb_cast_rays(tb_mesh* mesh, int64_t n, const float* o, const float* d, const
 int tb_cast_rays_sched(tb_mesh* mesh, int64_t n, const float* o, const float* d, const int32_t* start,
                        uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle,
                        double* t, int32_t* tet_back, int schedule, void* stream);
+/* Rays per block of the cast kernels (the unit of tb_cast_rays_ordered). */
+int tb_cast_block_size(void);
+/* tb_cast_rays with a caller-chosen launch order of whole blocks: launch slot
+ * b walks the tb_cast_block_size() rays of block block_order[b] (a
+ * permutation of the n_blocks = ceil(n / block) blocks); rays are read and
+ * results written in place, so outputs equal tb_cast_rays' bit for bit.  A
+ * renderer tracing frame after frame orders a frame's blocks longest first by
+ * the previous frame's walk lengths (visited), which removes most of the
+ * launch's SM-idle tail (profiles/r02_experiments.md).  No reference
+ * counterpart: the reference's tile pool (render.py:538-541) takes tiles in
+ * order. */
+int tb_cast_rays_ordered(tb_mesh* mesh, int64_t n, const float* o, const float* d, const int32_t* start,
+                         const int32_t* block_order, int64_t n_blocks, uint8_t* status, int32_t* cf, int32_t* tet,
+                         int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back, void* stream);
+/* block_order for tb_cast_rays_ordered from a previous similar batch's
+ * per-ray visited counts (n rays, device memory): the batch's n_blocks
+ * blocks, longest walk first (a block's key is its largest visited count,
+ * bucketed at 4095), stream-ordered, no host round trip. */
+int tb_block_order(int64_t n, const int32_t* visited, int32_t* order, int64_t n_blocks, void* stream);
 /* tb_cast_rays whose ray r writes its seven results to index out_index[r]
  * (int64, device) of the output arrays: the multi-GPU frame assembly with
  * no separate collective -- every rank traces its image tiles and its trace

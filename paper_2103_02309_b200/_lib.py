@@ -44,6 +44,9 @@ _SIGS = {
     "tb_trace_multi": (c_int, [c_int, P, c_int64, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),
     "tb_cast_rays": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),
     "tb_cast_rays_sched": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_int, c_void_p]),
+    "tb_cast_block_size": (c_int, []),
+    "tb_block_order": (c_int, [c_int64, P, P, c_int64, c_void_p]),
+    "tb_cast_rays_ordered": (c_int, [c_void_p, c_int64, P, P, P, P, c_int64, P, P, P, P, P, P, P, c_void_p]),
     "tb_cast_rays_scatter": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, P, c_void_p]),
     "tb_cast_rays_scatter_sched": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, P, c_int, c_void_p]),
     "tb_sctp_cast_rays_scatter": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, P, c_void_p]),

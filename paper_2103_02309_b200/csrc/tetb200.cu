@@ -524,7 +524,7 @@ __device__ __forceinline__ void walk_ray(const MeshView& m, float o0, float o1, 
 // walks the rays in binned order straight from the caller's arrays, so the
 // binning pass writes only the 8-byte permutation; with kScatter its results
 // go back to oidx[r] (oidx == ridx: the ray's own slot).
-template <int L, bool kClamp, bool kHostRays, bool kScatter, bool kGather = false>
+template <int L, bool kClamp, bool kHostRays, bool kScatter, bool kGather = false, bool kBlockMap = false>
 __global__ void __launch_bounds__(kCastBlock, (cast_min_blocks<L, kGather>())) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
                                                       const float* __restrict__ d,
                                                       const int32_t* __restrict__ start,
@@ -533,8 +533,13 @@ __global__ void __launch_bounds__(kCastBlock, (cast_min_blocks<L, kGather>())) c
                                                       int32_t* __restrict__ triangle, double* __restrict__ t,
                                                       int32_t* __restrict__ tet_back,
                                                       const int64_t* __restrict__ oidx,
-                                                      const int64_t* __restrict__ ridx) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+                                                      const int64_t* __restrict__ ridx,
+                                                      const int32_t* __restrict__ bmap) {
+  // kBlockMap: block b walks the rays of block bmap[b] (a caller-chosen launch
+  // order of whole 128-ray blocks, e.g. longest first by a previous frame's
+  // walk lengths -- tb_cast_rays_ordered); rays and results stay in place
+  const int64_t blk = kBlockMap ? (int64_t)__ldg(bmap + blockIdx.x) : (int64_t)blockIdx.x;
+  const int64_t r = blk * (int64_t)blockDim.x + threadIdx.x;
   float o0, o1, o2, d0, d1, d2;
   uint32_t cur;
   if constexpr (kHostRays) {
@@ -1252,20 +1257,32 @@ struct CastL {
     const int64_t* none = nullptr;
     if (oidx != nullptr) {  // scattered outputs (device rays only)
       if (nc)
-        cast_kernel<L, false, false, true><<<g, kCastBlock, 0, s>>>(a..., oidx, none);
+        cast_kernel<L, false, false, true><<<g, kCastBlock, 0, s>>>(a..., oidx, none, nullptr);
       else
-        cast_kernel<L, true, false, true><<<g, kCastBlock, 0, s>>>(a..., oidx, none);
+        cast_kernel<L, true, false, true><<<g, kCastBlock, 0, s>>>(a..., oidx, none, nullptr);
     } else if (host_rays) {
       if (nc)
-        cast_kernel<L, false, true, false><<<g, kCastBlock, 0, s>>>(a..., oidx, none);
+        cast_kernel<L, false, true, false><<<g, kCastBlock, 0, s>>>(a..., oidx, none, nullptr);
       else
-        cast_kernel<L, true, true, false><<<g, kCastBlock, 0, s>>>(a..., oidx, none);
+        cast_kernel<L, true, true, false><<<g, kCastBlock, 0, s>>>(a..., oidx, none, nullptr);
     } else {
       if (nc)
-        cast_kernel<L, false, false, false><<<g, kCastBlock, 0, s>>>(a..., oidx, none);
+        cast_kernel<L, false, false, false><<<g, kCastBlock, 0, s>>>(a..., oidx, none, nullptr);
       else
-        cast_kernel<L, true, false, false><<<g, kCastBlock, 0, s>>>(a..., oidx, none);
+        cast_kernel<L, true, false, false><<<g, kCastBlock, 0, s>>>(a..., oidx, none, nullptr);
     }
+  }
+};
+// Caller-ordered blocks (device rays, in-place results).
+template <int L>
+struct CastOrderedL {
+  template <typename... A>
+  static void launch(unsigned g, cudaStream_t s, bool safe, const int32_t* bmap, A... a) {
+    const int64_t* none = nullptr;
+    if (safe && L != 80)
+      cast_kernel<L, false, false, false, false, true><<<g, kCastBlock, 0, s>>>(a..., none, none, bmap);
+    else
+      cast_kernel<L, true, false, false, false, true><<<g, kCastBlock, 0, s>>>(a..., none, none, bmap);
   }
 };
 // Binned walk: rays read through perm; results stored through widx (perm
@@ -1275,9 +1292,9 @@ struct CastBinnedL {
   template <typename... A>
   static void launch(unsigned g, cudaStream_t s, bool safe, const int64_t* perm, const int64_t* widx, A... a) {
     if (safe && L != 80)
-      cast_kernel<L, false, false, true, true><<<g, kCastBlock, 0, s>>>(a..., widx, perm);
+      cast_kernel<L, false, false, true, true><<<g, kCastBlock, 0, s>>>(a..., widx, perm, nullptr);
     else
-      cast_kernel<L, true, false, true, true><<<g, kCastBlock, 0, s>>>(a..., widx, perm);
+      cast_kernel<L, true, false, true, true><<<g, kCastBlock, 0, s>>>(a..., widx, perm, nullptr);
   }
 };
 
@@ -2073,6 +2090,131 @@ int tb_cast_rays_sched(tb_mesh* m, int64_t n, const float* o, const float* d, co
   if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
   return cast_dispatch(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, (cudaStream_t)stream,
                        schedule == 0 ? sched_mode() : schedule);
+}
+
+int tb_cast_block_size(void) { return kCastBlock; }
+
+}  // extern "C"
+
+namespace {
+
+// Launch order of a batch's blocks, longest walk first, from a previous
+// similar batch's per-ray visited counts (tb_block_order).  A block's key is
+// its largest visited count (a block holds its slot until its slowest warp
+// ends), bucketed in kOrderBuckets log-spaced classes.  Pass 1: one warp per
+// block takes the key and adds it to the bucket histogram (warp-aggregated
+// atomics); pass 2: every CTA scans the small histogram in shared memory and
+// scatters its blocks, longest bucket first, through per-bucket atomic
+// cursors.  The order inside a bucket follows the atomics: it decides where a
+// block runs, never what it computes.
+constexpr int kOrderBuckets = 64;
+
+__device__ __forceinline__ int order_bucket(int v) {
+  // 0..15 exact, then 4 classes per power of two, descending ids for longer walks
+  int b;
+  if (v < 16) {
+    b = v;
+  } else {
+    const int e = 31 - __clz(v);               // >= 4
+    b = 16 + (e - 4) * 4 + ((v >> (e - 2)) & 3);
+  }
+  return kOrderBuckets - 1 - min(b, kOrderBuckets - 1);
+}
+
+__global__ void block_key_kernel(const int32_t* __restrict__ visited, int64_t n, int64_t nb,
+                                 uint8_t* __restrict__ key, int* __restrict__ hist) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nb) return;
+  int mx = 0;
+  for (int k = lane; k < kCastBlock; k += 32) {
+    const int64_t r = w * kCastBlock + k;
+    if (r < n) mx = max(mx, __ldg(visited + r));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) {
+    const int b = order_bucket(mx);
+    key[w] = (uint8_t)b;
+    atomicAdd(hist + b, 1);
+  }
+}
+
+__global__ void block_scatter_kernel(const uint8_t* __restrict__ key, int64_t nb, const int* __restrict__ hist,
+                                     int* __restrict__ cursor, int32_t* __restrict__ order) {
+  __shared__ int base[kOrderBuckets];
+  if (threadIdx.x < 32) {  // exclusive scan of the histogram, 2 buckets per lane
+    const int a = hist[2 * threadIdx.x], c = hist[2 * threadIdx.x + 1];
+    int pre = a + c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, pre, o);
+      if ((int)threadIdx.x >= o) pre += v;
+    }
+    base[2 * threadIdx.x] = pre - a - c;
+    base[2 * threadIdx.x + 1] = pre - c;
+  }
+  __syncthreads();
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const int k = key[b];
+  // warp-aggregated cursor bumps: one atomic per distinct bucket in the warp
+  const unsigned peers = __match_any_sync(__activemask(), k);
+  const int leader = __ffs(peers) - 1;
+  const int rank = __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
+  int pos = 0;
+  if ((int)(threadIdx.x & 31) == leader) pos = atomicAdd(cursor + k, __popc(peers));
+  pos = __shfl_sync(peers, pos, leader);
+  order[base[k] + pos + rank] = (int32_t)b;
+}
+}  // namespace
+
+extern "C" {
+
+int tb_block_order(int64_t n, const int32_t* visited, int32_t* order, int64_t n_blocks, void* stream) {
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  const int64_t nb = (n + kCastBlock - 1) / kCastBlock;
+  if (n_blocks != nb) return set_error(TB_E_ARG, "order must hold the %lld blocks of %d rays", (long long)nb,
+                                       kCastBlock);
+  if (nb == 0) return TB_OK;
+  if (!visited || !order) return set_error(TB_E_ARG, "NULL buffer");
+  if (nb > (int64_t)INT32_MAX) return set_error(TB_E_ARG, "too many blocks");
+  int dev = 0;
+  TB_CUDA(cudaGetDevice(&dev));
+  const cudaStream_t s = (cudaStream_t)stream;
+  // scratch: keys + histogram + cursors, from the per-device pool that keeps its memory
+  const size_t kb = ((size_t)nb + 255) / 256 * 256, hb = 2 * kOrderBuckets * sizeof(int);
+  char* scratch = nullptr;
+  if (int e = scratch_alloc(dev, kb + hb, s, &scratch)) return e;
+  uint8_t* key = reinterpret_cast<uint8_t*>(scratch);
+  int* hist = reinterpret_cast<int*>(scratch + kb);
+  int* cursor = hist + kOrderBuckets;
+  cudaMemsetAsync(hist, 0, hb, s);
+  block_key_kernel<<<grid_for(nb * 32, 256), 256, 0, s>>>(visited, n, nb, key, hist);
+  block_scatter_kernel<<<grid_for(nb, 256), 256, 0, s>>>(key, nb, hist, cursor, order);
+  const cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(scratch, s);
+  TB_CUDA(e);
+  return TB_OK;
+}
+
+int tb_cast_rays_ordered(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,
+                         const int32_t* block_order, int64_t n_blocks, uint8_t* status, int32_t* cf, int32_t* tet,
+                         int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back, void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (n < 0) return set_error(TB_E_ARG, "negative ray count");
+  if (n == 0) return TB_OK;
+  if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
+  const int64_t nb = (n + kCastBlock - 1) / kCastBlock;
+  if (!block_order || n_blocks != nb)
+    return set_error(TB_E_ARG, "block_order must list the %lld blocks of %d rays (got %lld)", (long long)nb,
+                     kCastBlock, (long long)n_blocks);
+  DeviceGuard g(m->device);
+  // the order is a permutation of [0, nb) (the caller's contract; an entry
+  // out of range only reads past the rays' blocks, which r >= n guards)
+  int e = launch_layout<CastOrderedL>(m->layout, (unsigned)nb, (cudaStream_t)stream, m->safe, block_order, m->view(),
+                                      n, o, d, start, status, cf, tet, visited, triangle, t, tet_back);
+  if (e) return e;
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
 }
 
 int tb_sctp_cast_rays(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start,

@@ -224,3 +224,11 @@ def test_fastcall_declines_other_layouts_and_checks_arguments():
         f(0, 10, o, d, st)
     status, cf, tet, visited = f(0, 10, o[:0], d[:0], st[:0])
     assert status.dtype == np.uint8 and cf.dtype == tet.dtype == visited.dtype == np.int32 and len(status) == 0
+
+
+def test_ordered_cast_validates_arguments():
+    from paper_2103_02309_b200._lib import lib
+
+    assert lib.tb_cast_block_size() == 128
+    rc = lib.tb_cast_rays_ordered(None, 1, None, None, None, None, 1, None, None, None, None, None, None, None, None)
+    assert rc != 0 and b"NULL" in lib.tb_last_error()

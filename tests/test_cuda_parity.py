@@ -682,3 +682,46 @@ def test_fastcall_equals_ctypes_path(golden, digests, K, name):
         tile = K.cast_rays(m, o[a0:a0 + 256], d[a0:a0 + 256], st[a0:a0 + 256])
         for a, b in zip(tile, plain):
             assert np.array_equal(a, b[a0:a0 + 256])
+
+
+def test_block_order_launch_equals_plain_trace(golden, K):
+    """trace(block_order=...) launches whole blocks in a caller-chosen order
+    (tb_cast_rays_ordered); results stay in place and equal the plain launch
+    bit for bit -- for longest_first of the batch's own walk lengths, a random
+    permutation and a ragged last block.  Bad orders fail loudly."""
+    import torch
+
+    from paper_2103_02309_b200._lib import TetB200Error
+    from paper_2103_02309_b200.trace import block_size, longest_first, trace
+
+    dev = torch.device("cuda", 0)
+    m = golden_mesh(golden, "model", "tet20")
+    o, d, st = _rays(m, "model", n=10000 + 37)
+    g = [torch.from_numpy(a).to(dev) for a in (o, d, st)]
+    ref = trace(m, *g)
+    nb = (len(st) + block_size() - 1) // block_size()
+    lf = longest_first(ref.visited)  # tb_block_order: a permutation, block maxima non-increasing
+    assert sorted(lf.cpu().tolist()) == list(range(nb))
+    v = torch.zeros(nb * block_size(), dtype=torch.int32, device=dev)
+    v[:len(st)] = ref.visited
+    keys = v.view(nb, -1).max(dim=1).values[lf.long()].cpu().numpy()
+
+    def bucket(x):  # tb_block_order's classes: exact below 16, then 4 per power of two
+        if x < 16:
+            return int(x)
+        e = int(x).bit_length() - 1
+        return min(16 + (e - 4) * 4 + ((int(x) >> (e - 2)) & 3), 63)
+
+    classes = [bucket(k) for k in keys]
+    assert all(a >= b for a, b in zip(classes, classes[1:]))  # longest class first
+    gen = torch.Generator(device="cpu").manual_seed(5)
+    for order in (longest_first(ref.visited), torch.randperm(nb, generator=gen).to(torch.int32).to(dev)):
+        got = trace(m, *g, block_order=order)
+        for k in NAMES7:
+            assert torch.equal(getattr(got, k), getattr(ref, k)), k
+    with pytest.raises(TetB200Error, match="block_order"):
+        trace(m, *g, block_order=torch.arange(nb - 1, dtype=torch.int32, device=dev))
+    with pytest.raises(ValueError):
+        trace(m, *g, block_order=torch.arange(nb, dtype=torch.int64, device=dev))
+    with pytest.raises(ValueError):
+        trace(m, *g, block_order=torch.arange(nb, dtype=torch.int32, device=dev), sctp=True)
