@@ -585,8 +585,17 @@ def run_ours(args, cfg):
     # ray schedule: one ray per lane for primaries; incoherent secondaries
     # (config 4) are binned by direction cell first (96 cube-map cells) and
     # walked in binned order (r01: 3.36 vs 2.37 Grays/s one ray per lane).
-    schedule = args.schedule or ("auto" if os.environ.get("TETB200_SCHED") else
-                                 ("binned" if cfg.get("secondaries") else "lane"))
+    # ray schedule: incoherent secondaries (config 4) are binned by direction
+    # cell first (96 cube-map cells) and walked in binned order (r01: 3.36 vs
+    # 2.37 Grays/s one ray per lane); primaries take "auto": the sampled
+    # longest-first block order for launches of <= 16 waves (config 2), one
+    # ray per lane beyond (tb_auto_schedule)
+    schedule = args.schedule or ("binned" if cfg.get("secondaries") else "auto")
+    if schedule == "auto" and world == 1 and not sctp:
+        from paper_2103_02309_b200._lib import SCHEDULES
+
+        resolved = int(lib.tb_auto_schedule(local, n))
+        schedule = next(k for k, v in SCHEDULES.items() if v == resolved)
 
     def step():
         trace(dm, go, gd, gs, out=res, stream=stream, sctp=sctp, schedule=schedule)
@@ -858,7 +867,10 @@ def run_ours(args, cfg):
     kname = (f"sctp_kernel<{cfg['layout'][3:]}>" if sctp else
              f"{'cast_compact_kernel' if schedule in ('compact', 'compact512') else 'cast_kernel'}"
              f"<{cfg['layout'][3:]}>" + (" after bin_count/bin_seg_scan/bin_scatter (direction binning, inside "
-                                          "the events)" if schedule == "binned" else ""))
+                                          "the events)" if schedule == "binned" else
+                                          " with its blocks launched longest first, after block_probe/"
+                                          "block_scatter (a capped one-ray-per-block pre-pass, inside the events)"
+                                          if schedule == "sampled" else ""))
     hbm = {"bound": "hbm", "achieved": alg / kern_s / 1e9, "peak": peak, "unit": "GB/s", "peak_source": peak_src,
            "algorithmic_bytes_per_launch": alg,
            "frac": alg / kern_s / 1e9 / peak,
@@ -895,7 +907,8 @@ def run_ours(args, cfg):
                         if (not sctp and cfg["layout"] != "tet80" and not args.no_l2_probe) else None),
         "clocks": dict(clk, window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
         "gpu_launches": args.steps * ((1 if fg is None else sum(1 for a, b in fg.my_pieces() if b > a))
-                                      * (4 if schedule == "binned" else 1)  # binned: count, scan, scatter, walk
+                                      * (4 if schedule == "binned" else (3 if schedule == "sampled" else 1))
+                                      # binned: count, scan, scatter, walk; sampled: probe, scatter, walk
                                       + (1 if (pg is not None and schedule == "binned") else 0)  # compose
                                       + (1 if pg is not None and pg.lean else 0)),  # lean p2p: root epilogue
         "parity": parity,
@@ -1126,7 +1139,8 @@ def main():
     ap.add_argument("--gather", choices=("p2p", "nccl"), default="p2p",
                     help="N > 1 frame assembly: fused P2P stores (default) or the chunked NCCL gather")
     ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1 NCCL gather: trace/gather pipeline depth")
-    ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512", "dynamic", "binned"),
+    ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512", "dynamic", "binned",
+                                                          "sampled"),
                     help="ray-to-lane schedule of the timed trace (default: binned for secondaries, else lane)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-l2-probe", action="store_true", help="skip the L2 gather-roof probe (roofline_l2)")

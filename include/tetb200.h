@@ -173,6 +173,10 @@ int tb_cast_rays_sched(tb_mesh* mesh, int64_t n, const float* o, const float* d,
                        double* t, int32_t* tet_back, int schedule, void* stream);
 /* Rays per block of the cast kernels (the unit of tb_cast_rays_ordered). */
 int tb_cast_block_size(void);
+/* The schedule "auto" (mode 0) resolves to for a device-resident batch of n
+ * rays on `device`: 7 (sampled longest-first) while the launch has at most 16
+ * waves of blocks, else 1 (one ray per lane). */
+int tb_auto_schedule(int device, int64_t n);
 /* tb_cast_rays with a caller-chosen launch order of whole blocks: launch slot
  * b walks the tb_cast_block_size() rays of block block_order[b] (a
  * permutation of the n_blocks = ceil(n / block) blocks); rays are read and
@@ -308,7 +312,12 @@ int tb_sctp_cast_rays_host(tb_mesh* mesh, int64_t n, const float* o, const float
  *   bins; stream-ordered scratch, 9 B / ray), then one ray per lane in
  *   binned order, each ray read and its results stored by index --
  *   for incoherent device-resident batches (n < 2^31; host-ray zero-copy
- *   calls run one ray per lane).  5 is unused. 
+ *   calls run one ray per lane), 5 = dynamic warp chunks (kept for
+ *   comparison), 7 = sampled longest-first: one ray per block walked at most
+ *   32 steps orders the blocks longest first, then the full walk launches
+ *   them in that order (tb_cast_rays_ordered's kernel) -- for coherent
+ *   device-resident primaries, whose launch otherwise ends on a few late
+ *   long rays.  Results are identical in every mode. 
  * Process-wide; overrides TETB200_SCHED / TETB200_ROUND.  A negative
  * argument leaves that setting unchanged. */
 int tb_set_schedule(int mode, int steps_per_round);

@@ -45,6 +45,7 @@ _SIGS = {
     "tb_cast_rays": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_void_p]),
     "tb_cast_rays_sched": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, c_int, c_void_p]),
     "tb_cast_block_size": (c_int, []),
+    "tb_auto_schedule": (c_int, [c_int, c_int64]),
     "tb_block_order": (c_int, [c_int64, P, P, c_int64, c_void_p]),
     "tb_cast_rays_ordered": (c_int, [c_void_p, c_int64, P, P, P, P, c_int64, P, P, P, P, P, P, P, c_void_p]),
     "tb_cast_rays_scatter": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, P, c_void_p]),
@@ -97,7 +98,8 @@ def check(code: int, what: str) -> None:
         raise TetB200Error(f"{what} failed ({code}): {msg.decode() if msg else 'unknown error'}")
 
 
-SCHEDULES = {"auto": 0, "lane": 1, "refill": 2, "compact": 3, "compact512": 4, "dynamic": 5, "binned": 6}
+SCHEDULES = {"auto": 0, "lane": 1, "refill": 2, "compact": 3, "compact512": 4, "dynamic": 5, "binned": 6,
+             "sampled": 7}
 
 
 def set_schedule(mode: str | int | None = None, steps_per_round: int | None = None) -> None:

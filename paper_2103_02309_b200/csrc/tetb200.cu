@@ -1380,7 +1380,7 @@ int sched_mode() {
   if (mode < 0) {
     const char* v = getenv("TETB200_SCHED");
     mode = v ? atoi(v) : 0;
-    if (mode < 0 || mode > 6) mode = 0;
+    if (mode < 0 || mode > 7) mode = 0;
     int expect = -1;
     g_sched_mode.compare_exchange_strong(expect, mode);
     mode = g_sched_mode.load();
@@ -1507,6 +1507,157 @@ __global__ void __launch_bounds__(256) gather_probe_kernel(MeshView m, int64_t n
   if (acc == 0x9E3779B9u) atomicXor(sink, acc);  // keeps the loads live; practically never stores
 }
 
+// Launch order of a batch's blocks, longest walk first, from a previous
+// similar batch's per-ray visited counts (tb_block_order).  A block's key is
+// its largest visited count (a block holds its slot until its slowest warp
+// ends), bucketed in kOrderBuckets log-spaced classes.  Pass 1: one warp per
+// block takes the key and adds it to the bucket histogram (warp-aggregated
+// atomics); pass 2: every CTA scans the small histogram in shared memory and
+// scatters its blocks, longest bucket first, through per-bucket atomic
+// cursors.  The order inside a bucket follows the atomics: it decides where a
+// block runs, never what it computes.
+constexpr int kOrderBuckets = 64;
+
+__device__ __forceinline__ int order_bucket(int v) {
+  // 0..15 exact, then 4 classes per power of two, descending ids for longer walks
+  int b;
+  if (v < 16) {
+    b = v;
+  } else {
+    const int e = 31 - __clz(v);               // >= 4
+    b = 16 + (e - 4) * 4 + ((v >> (e - 2)) & 3);
+  }
+  return kOrderBuckets - 1 - min(b, kOrderBuckets - 1);
+}
+
+__global__ void block_key_kernel(const int32_t* __restrict__ visited, int64_t n, int64_t nb,
+                                 uint8_t* __restrict__ key, int* __restrict__ hist) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nb) return;
+  int mx = 0;
+  for (int k = lane; k < kCastBlock; k += 32) {
+    const int64_t r = w * kCastBlock + k;
+    if (r < n) mx = max(mx, __ldg(visited + r));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) {
+    const int b = order_bucket(mx);
+    key[w] = (uint8_t)b;
+    atomicAdd(hist + b, 1);
+  }
+}
+
+__global__ void block_scatter_kernel(const uint8_t* __restrict__ key, int64_t nb, const int* __restrict__ hist,
+                                     int* __restrict__ cursor, int32_t* __restrict__ order) {
+  __shared__ int base[kOrderBuckets];
+  if (threadIdx.x < 32) {  // exclusive scan of the histogram, 2 buckets per lane
+    const int a = hist[2 * threadIdx.x], c = hist[2 * threadIdx.x + 1];
+    int pre = a + c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, pre, o);
+      if ((int)threadIdx.x >= o) pre += v;
+    }
+    base[2 * threadIdx.x] = pre - a - c;
+    base[2 * threadIdx.x + 1] = pre - c;
+  }
+  __syncthreads();
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const int k = key[b];
+  // warp-aggregated cursor bumps: one atomic per distinct bucket in the warp
+  const unsigned peers = __match_any_sync(__activemask(), k);
+  const int leader = __ffs(peers) - 1;
+  const int rank = __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
+  int pos = 0;
+  if ((int)(threadIdx.x & 31) == leader) pos = atomicAdd(cursor + k, __popc(peers));
+  pos = __shfl_sync(peers, pos, leader);
+  order[base[k] + pos + rank] = (int32_t)b;
+}
+
+// Sampled cost pre-pass of schedule 7 ("sampled"): one ray per block -- the
+// block's middle ray -- walked at most `cap` steps; its step count, exact
+// below kOrderBuckets, is the block's key for the longest-first order.  A
+// single ray per block, capped at 32 steps, orders a 1080p frame as well as
+// the blocks' full walk lengths do (r02 probe): the blocks that matter are
+// the ones whose rays run long, and any ray past 32 steps marks one.
+template <int L, bool kClamp>
+__global__ void __launch_bounds__(64) block_probe_kernel(MeshView m, int64_t n, const float* __restrict__ o,
+                                                         const float* __restrict__ d,
+                                                         const int32_t* __restrict__ start, int64_t nb, int cap,
+                                                         uint8_t* __restrict__ key, int* __restrict__ hist) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool in = b < nb;
+  int steps = 0;
+  if (in) {
+    int64_t r = b * kCastBlock + kCastBlock / 2;
+    if (r >= n) r = n - 1;
+    uint32_t cur = (uint32_t)__ldg(start + r);
+    Basis bs;
+    uint32_t idx[3];
+    float p[6];
+    const int j = init_ray(m, __ldg(o + 3 * r), __ldg(o + 3 * r + 1), __ldg(o + 3 * r + 2), __ldg(d + 3 * r),
+                           __ldg(d + 3 * r + 1), __ldg(d + 3 * r + 2), (int)cur, bs, idx, p);
+    uint32_t ref = pick4u(__ldg(&m.sn[cur]), j);
+    const float4* __restrict__ P = ray_points(m, bs);
+    const uint32_t live = kClamp ? (uint32_t)m.n_tets : kBoundary;
+    steps = 1;
+    while (ref < live && steps < cap) {
+      const uint32_t nxt = ref;
+      ref = advance<L, kClamp>(m, P, bs, idx, p, nxt, cur);
+      cur = nxt;
+      ++steps;
+    }
+  }
+  const int k = kOrderBuckets - 1 - min(steps, kOrderBuckets - 1);
+  if (in) key[b] = (uint8_t)k;
+  const unsigned act = __ballot_sync(0xffffffffu, in);
+  if (!in) return;
+  const unsigned peers = __match_any_sync(act, k);
+  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(hist + k, __popc(peers));
+}
+
+template <int L>
+struct BlockProbeL {
+  template <typename... A>
+  static void launch(unsigned g, cudaStream_t s, bool safe, A... a) {
+    if (safe && L != 80)
+      block_probe_kernel<L, false><<<g, 64, 0, s>>>(a...);
+    else
+      block_probe_kernel<L, true><<<g, 64, 0, s>>>(a...);
+  }
+};
+
+// Schedule 0 ("auto") for device-resident batches: the sampled longest-first
+// order (7) while the launch has at most kSampledWaves waves of blocks --
+// there the SM-idle tail of the last wave is a large share of the launch
+// (config 2, 1080p: 11 waves, +4-6 % net of its pre-pass) -- and one ray per
+// lane (1) beyond, where the tail is diluted and the pre-pass, a latency-bound
+// walk over a cold L2, costs more than it returns (config 3: 44 waves, -1.6 %;
+// config 5: 175 waves, -5.7 %; r02 A/B).  Incoherent batches ask for "binned".
+constexpr int64_t kSampledWaves = 16;
+int auto_schedule(int device, int64_t n) {
+  static std::atomic<int> sms[64];
+  if (device < 0 || device >= 64) return 1;
+  int c = sms[device].load(std::memory_order_relaxed);
+  if (c == 0) {
+    if (cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || c <= 0) c = 148;
+    sms[device].store(c, std::memory_order_relaxed);
+  }
+  const int64_t nb = (n + kCastBlock - 1) / kCastBlock;
+  const int64_t wave = (int64_t)c * TB_CAST_MIN_BLOCKS;
+  return nb <= kSampledWaves * wave ? 7 : 1;
+}
+
+int probe_cap() {
+  static const int cap = [] {
+    const char* v = getenv("TETB200_PROBE_CAP");  // experiment knob
+    const int c = v ? atoi(v) : 24;
+    return c < 2 ? 2 : (c > 63 ? 63 : c);
+  }();
+  return cap;
+}
+
 int check_mesh(const tb_mesh* m) {
   if (m == nullptr) return set_error(TB_E_ARG, "mesh handle is NULL");
   return TB_OK;
@@ -1523,6 +1674,7 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
   // binned walk (its permutation composed with oidx); the compaction and
   // refill schedules have no scatter variant and run one ray per lane.
   if (oidx != nullptr && mode != 6) mode = 1;
+  if (mode == 0 && !host_rays) mode = auto_schedule(m->device, n);
   if ((mode == 3 || mode == 4) && n < (int64_t)1 << 32) {
     e = mode == 3 ? launch_compact<256>(m->layout, m->safe, n, s, v, n, o, d, start, status, cf, tet, visited,
                                         triangle, t, tet_back)
@@ -1560,6 +1712,29 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
     if (oidx) compose_index_kernel<<<grid_for(n, 256), 256, 0, s>>>(perm, oidx, n, widx);
     e = launch_layout<CastBinnedL>(m->layout, grid_for(n, kCastBlock), s, m->safe, perm, widx, v, n, o, d, start,
                                    status, cf, tet, visited, triangle, t, tet_back);
+    cudaFreeAsync(scratch, s);
+  } else if (mode == 7 && !host_rays && oidx == nullptr) {
+    // sampled longest-first: a capped walk of one ray per block orders the
+    // blocks (block_probe_kernel -> block_scatter_kernel), then the full walk
+    // launches them in that order, rays and results in place
+    const int64_t nb = (n + kCastBlock - 1) / kCastBlock;
+    const size_t kb = ((size_t)nb + 255) / 256 * 256, hb = 2 * kOrderBuckets * sizeof(int);
+    char* scratch = nullptr;
+    if (int e2 = scratch_alloc(m->device, kb + hb + (size_t)nb * 4, s, &scratch)) return e2;
+    uint8_t* key = reinterpret_cast<uint8_t*>(scratch);
+    int* hist = reinterpret_cast<int*>(scratch + kb);
+    int32_t* order = reinterpret_cast<int32_t*>(scratch + kb + hb);
+    if (cudaError_t me = cudaMemsetAsync(hist, 0, hb, s)) {
+      cudaFreeAsync(scratch, s);
+      return set_error(TB_E_CUDA, "sampled schedule memset: %s", cudaGetErrorString(me));
+    }
+    e = launch_layout<BlockProbeL>(m->layout, grid_for(nb, 64), s, m->safe, v, n, o, d, start, nb, probe_cap(), key,
+                                   hist);
+    if (!e) {
+      block_scatter_kernel<<<grid_for(nb, 256), 256, 0, s>>>(key, nb, hist, hist + kOrderBuckets, order);
+      e = launch_layout<CastOrderedL>(m->layout, (unsigned)nb, s, m->safe, (const int32_t*)order, v, n, o, d, start,
+                                      status, cf, tet, visited, triangle, t, tet_back);
+    }
     cudaFreeAsync(scratch, s);
   } else if (mode == 5 && !host_rays) {
     char* scratch = nullptr;
@@ -1840,9 +2015,10 @@ int tb_cast_rays(tb_mesh* m, int64_t n, const float* o, const float* d, const in
   if (n < 0) return set_error(TB_E_ARG, "negative ray count");
   if (n == 0) return TB_OK;
   if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
-  // device pointers: auto = one ray per lane (deciding coherence would need
-  // a host round trip; callers that know their batch is incoherent select
-  // compaction with tb_set_schedule)
+  // device pointers: auto = tb_auto_schedule (sampled longest-first for
+  // launches of few waves, else one ray per lane; deciding coherence would
+  // need a host round trip -- callers that know their batch is incoherent
+  // select "binned")
   return cast_dispatch(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, (cudaStream_t)stream,
                        sched_mode());
 }
@@ -1864,7 +2040,7 @@ int tb_cast_rays_scatter_sched(tb_mesh* m, int64_t n, const float* o, const floa
                                int32_t* triangle, double* t, int32_t* tet_back, int schedule, void* stream) {
   if (int e = check_mesh(m)) return e;
   if (n < 0) return set_error(TB_E_ARG, "negative ray count");
-  if (schedule < 0 || schedule > 6) return set_error(TB_E_ARG, "schedule %d not in 0..6", schedule);
+  if (schedule < 0 || schedule > 7) return set_error(TB_E_ARG, "schedule %d not in 0..7", schedule);
   if (n == 0) return TB_OK;
   if (!o || !d || !start || !out_index || !status || !cf || !tet || !visited)
     return set_error(TB_E_ARG, "NULL ray buffer");
@@ -2085,7 +2261,7 @@ int tb_cast_rays_sched(tb_mesh* m, int64_t n, const float* o, const float* d, co
                        int32_t* tet_back, int schedule, void* stream) {
   if (int e = check_mesh(m)) return e;
   if (n < 0) return set_error(TB_E_ARG, "negative ray count");
-  if (schedule < 0 || schedule > 6) return set_error(TB_E_ARG, "schedule %d not in 0..6", schedule);
+  if (schedule < 0 || schedule > 7) return set_error(TB_E_ARG, "schedule %d not in 0..7", schedule);
   if (n == 0) return TB_OK;
   if (!o || !d || !start || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL ray buffer");
   return cast_dispatch(m, n, o, d, start, status, cf, tet, visited, triangle, t, tet_back, (cudaStream_t)stream,
@@ -2094,80 +2270,7 @@ int tb_cast_rays_sched(tb_mesh* m, int64_t n, const float* o, const float* d, co
 
 int tb_cast_block_size(void) { return kCastBlock; }
 
-}  // extern "C"
-
-namespace {
-
-// Launch order of a batch's blocks, longest walk first, from a previous
-// similar batch's per-ray visited counts (tb_block_order).  A block's key is
-// its largest visited count (a block holds its slot until its slowest warp
-// ends), bucketed in kOrderBuckets log-spaced classes.  Pass 1: one warp per
-// block takes the key and adds it to the bucket histogram (warp-aggregated
-// atomics); pass 2: every CTA scans the small histogram in shared memory and
-// scatters its blocks, longest bucket first, through per-bucket atomic
-// cursors.  The order inside a bucket follows the atomics: it decides where a
-// block runs, never what it computes.
-constexpr int kOrderBuckets = 64;
-
-__device__ __forceinline__ int order_bucket(int v) {
-  // 0..15 exact, then 4 classes per power of two, descending ids for longer walks
-  int b;
-  if (v < 16) {
-    b = v;
-  } else {
-    const int e = 31 - __clz(v);               // >= 4
-    b = 16 + (e - 4) * 4 + ((v >> (e - 2)) & 3);
-  }
-  return kOrderBuckets - 1 - min(b, kOrderBuckets - 1);
-}
-
-__global__ void block_key_kernel(const int32_t* __restrict__ visited, int64_t n, int64_t nb,
-                                 uint8_t* __restrict__ key, int* __restrict__ hist) {
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= nb) return;
-  int mx = 0;
-  for (int k = lane; k < kCastBlock; k += 32) {
-    const int64_t r = w * kCastBlock + k;
-    if (r < n) mx = max(mx, __ldg(visited + r));
-  }
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) {
-    const int b = order_bucket(mx);
-    key[w] = (uint8_t)b;
-    atomicAdd(hist + b, 1);
-  }
-}
-
-__global__ void block_scatter_kernel(const uint8_t* __restrict__ key, int64_t nb, const int* __restrict__ hist,
-                                     int* __restrict__ cursor, int32_t* __restrict__ order) {
-  __shared__ int base[kOrderBuckets];
-  if (threadIdx.x < 32) {  // exclusive scan of the histogram, 2 buckets per lane
-    const int a = hist[2 * threadIdx.x], c = hist[2 * threadIdx.x + 1];
-    int pre = a + c;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, pre, o);
-      if ((int)threadIdx.x >= o) pre += v;
-    }
-    base[2 * threadIdx.x] = pre - a - c;
-    base[2 * threadIdx.x + 1] = pre - c;
-  }
-  __syncthreads();
-  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (b >= nb) return;
-  const int k = key[b];
-  // warp-aggregated cursor bumps: one atomic per distinct bucket in the warp
-  const unsigned peers = __match_any_sync(__activemask(), k);
-  const int leader = __ffs(peers) - 1;
-  const int rank = __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
-  int pos = 0;
-  if ((int)(threadIdx.x & 31) == leader) pos = atomicAdd(cursor + k, __popc(peers));
-  pos = __shfl_sync(peers, pos, leader);
-  order[base[k] + pos + rank] = (int32_t)b;
-}
-}  // namespace
-
-extern "C" {
+int tb_auto_schedule(int device, int64_t n) { return n < 0 ? -1 : auto_schedule(device, n); }
 
 int tb_block_order(int64_t n, const int32_t* visited, int32_t* order, int64_t n_blocks, void* stream) {
   if (n < 0) return set_error(TB_E_ARG, "negative ray count");
@@ -2740,7 +2843,7 @@ int tb_shadow_rays_host(tb_mesh* m, int64_t n, const double* p, const double* li
 }
 
 int tb_set_schedule(int mode, int steps_per_round) {
-  if (mode > 6) return set_error(TB_E_ARG, "schedule mode %d not in 0..6", mode);
+  if (mode > 7) return set_error(TB_E_ARG, "schedule mode %d not in 0..7", mode);
   if (steps_per_round == 0) return set_error(TB_E_ARG, "steps_per_round must be >= 1");
   if (mode >= 0) g_sched_mode.store(mode);
   if (steps_per_round > 0) g_round_steps.store(steps_per_round);

@@ -394,7 +394,7 @@ def test_schedules_cycle_guard(digests, K, O, schedule, mode):
         assert np.array_equal(a, b), k
 
 
-@pytest.mark.parametrize("schedule", ("lane", "refill", "compact", "compact512", "binned"))
+@pytest.mark.parametrize("schedule", ("lane", "refill", "compact", "compact512", "binned", "sampled"))
 def test_trace_schedule_argument(golden, K, O, schedule):
     """trace(schedule=...) on device tensors (tb_cast_rays_sched) equals the
     oracle for an incoherent batch larger than one wave of blocks."""
@@ -618,7 +618,7 @@ def test_binned_many_segments_matches_lane(golden):
         assert torch.equal(getattr(a, k), getattr(b, k)), k
 
 
-@pytest.mark.parametrize("schedule", ("lane", "binned", "compact"))
+@pytest.mark.parametrize("schedule", ("lane", "binned", "compact", "sampled"))
 def test_schedules_without_epilogue(golden, O, schedule):
     """trace(epilogue=False): triangle / t / tet_back are not computed (NULL in
     the C call) under every schedule; status / cf / tet / visited still equal
@@ -725,3 +725,43 @@ def test_block_order_launch_equals_plain_trace(golden, K):
         trace(m, *g, block_order=torch.arange(nb, dtype=torch.int64, device=dev))
     with pytest.raises(ValueError):
         trace(m, *g, block_order=torch.arange(nb, dtype=torch.int32, device=dev), sctp=True)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS4)
+def test_sampled_schedule_matches_lane(golden, digests, K, layout):
+    """schedule="sampled" (a capped one-ray-per-block pre-pass orders the
+    blocks longest first, then the full walk in that order) equals one ray per
+    lane for every ray: golden fixtures at full digest, ragged sizes (1 ray,
+    less than a block, a ragged last block), every layout, and the lattice
+    camera whose rays trip the cycle guard."""
+    import torch
+
+    from paper_2103_02309_b200.scenes import camera_rays
+    from paper_2103_02309_b200.tetmesh import encode
+    from paper_2103_02309_b200.trace import trace
+
+    dev = torch.device("cuda", 0)
+    for name in ("pane4", "model"):
+        base = golden_mesh(golden, name, "tet20" if layout == "tet80" else layout)
+        o, d, st = _rays(base, name)
+        g = [torch.from_numpy(a).to(dev) for a in (o, d, st)]
+        got = trace(base, *g, schedule="sampled", layout=layout)
+        ref_layout = "tet32" if layout == "tet80" else layout
+        assert digest(*(getattr(got, k).cpu().numpy() for k in ("status", "cf", "tet", "visited"))) == \
+            digests[f"{name}/{ref_layout}/cast10k"]
+        for n in (1, 33, 129, 4099):
+            a = trace(base, *(x[:n] for x in g), schedule="sampled", layout=layout)
+            b = trace(base, *(x[:n] for x in g), schedule="lane", layout=layout)
+            for k in NAMES7:
+                assert torch.equal(getattr(a, k), getattr(b, k)), (name, n, k)
+    if layout == "tet20":  # the lattice camera: exact ties, cycle-guard rays (status 2)
+        from paper_2103_02309_b200.ingestion import build_box_fixture
+
+        raw, soup = build_box_fixture(8, occluders=[(0, 4, (2, 2), (6, 6))])
+        m = encode(raw, "tet20", soup)
+        o, d = camera_rays((4.0, 4.0, 0.5), (4.0, 4.0, 8.0), (0.0, 1.0, 0.0), 68.0, 1024, 1024)
+        st = np.full(len(o), digests["lattice8/cam_tet"], np.int32)
+        g = [torch.from_numpy(a).to(dev) for a in (o, d, st)]
+        a = trace(m, *g, schedule="sampled")
+        assert digest(*(getattr(a, k).cpu().numpy() for k in ("status", "cf", "tet", "visited"))) == \
+            digests["lattice8/cast"]

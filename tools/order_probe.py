@@ -75,9 +75,22 @@ def main():
         return v.view(nb, BLOCK).max(dim=1).values, r
 
     own, ref = costs(g)
+    v_own = torch.zeros(nb * BLOCK, dtype=torch.int32, device=dev)
+    v_own[:n] = ref.visited
+    one_ray = v_own.view(nb, BLOCK)[:, BLOCK // 2]      # one sampled ray per block
+    stride8 = v_own.view(nb, BLOCK)[:, ::16].max(dim=1).values  # 8 sampled rays per block
     moved, _ = costs(frame(args.move))
-    orders = {"as given": torch.arange(nb, device=dev),
+    ar = torch.arange(nb, device=dev)
+    orders = {"as given": ar,
+              "reversed": torch.flip(ar, [0]),
+              "interleaved (b x 7919 mod B)": torch.argsort((ar * 7919) % nb),
+              "interleaved by 148 (SM-strided)": torch.argsort((ar % 148) * nb + ar),
+              "random": torch.randperm(nb, device=dev, generator=torch.Generator(device=dev).manual_seed(1)),
               "longest first, own costs (bound)": torch.argsort(own, descending=True, stable=True),
+              "longest first, one sampled ray per block": torch.argsort(one_ray, descending=True, stable=True),
+              "longest first, 8 sampled rays per block": torch.argsort(stride8, descending=True, stable=True),
+              **{f"longest first, one sampled ray capped at {k} steps":
+                 torch.argsort(one_ray.clamp(max=k), descending=True, stable=True) for k in (16, 32, 48, 96)},
               f"longest first, costs of the frame moved by {args.move}": torch.argsort(moved, descending=True,
                                                                                        stable=True)}
     for name, bo in orders.items():
