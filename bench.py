@@ -1141,7 +1141,7 @@ def main():
     ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1 NCCL gather: trace/gather pipeline depth")
     ap.add_argument("--schedule", default=None, choices=("auto", "lane", "refill", "compact", "compact512", "dynamic", "binned",
                                                           "sampled"),
-                    help="ray-to-lane schedule of the timed trace (default: binned for secondaries, else lane)")
+                    help="ray-to-lane schedule of the timed trace (default: binned for secondaries, else auto)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-l2-probe", action="store_true", help="skip the L2 gather-roof probe (roofline_l2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
