@@ -1604,6 +1604,21 @@ __global__ void __launch_bounds__(64) block_probe_kernel(MeshView m, int64_t n, 
     steps = 1;
     while (ref < live && steps < cap) {
       const uint32_t nxt = ref;
+#ifndef TB_PROBE_NO_PREFETCH
+      if constexpr (L == 20) {
+        // the walk here is a lone latency chain over a cold L2: the tet's
+        // neighbours are the next step's only candidates, so their records go
+        // to L2 while this step decides (one DRAM round trip per step, not two)
+        const uint4 nb4 = __ldg(&m.rec4[nxt]);
+        const uint32_t nbs[4] = {nb4.x, nb4.y, nb4.z, nb4.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (nbs[k] < (uint32_t)m.n_tets) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(m.vx + nbs[k]));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(m.rec4 + nbs[k]));
+          }
+      }
+#endif
       ref = advance<L, kClamp>(m, P, bs, idx, p, nxt, cur);
       cur = nxt;
       ++steps;

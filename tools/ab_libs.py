@@ -92,7 +92,7 @@ def main():
         cam, _ = locate(dm, torch.tensor(pos[None], dtype=torch.float64, device=dev),
                         torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))
         st = np.full(len(o), int(cam.item()), np.int32)
-        sched = 1
+        sched = int(os.environ.get("AB_PRIMARY_SCHED", "1"))
         if cfg.get("secondaries") or os.environ.get("AB_SECONDARIES"):
             from paper_2103_02309_b200.scenes import diffuse_secondaries
 
