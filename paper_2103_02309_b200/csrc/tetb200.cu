@@ -1667,7 +1667,7 @@ int auto_schedule(int device, int64_t n) {
 int probe_cap() {
   static const int cap = [] {
     const char* v = getenv("TETB200_PROBE_CAP");  // experiment knob
-    const int c = v ? atoi(v) : 24;
+    const int c = v ? atoi(v) : 32;
     return c < 2 ? 2 : (c > 63 ? 63 : c);
   }();
   return cap;

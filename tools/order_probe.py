@@ -90,7 +90,11 @@ def main():
               "longest first, one sampled ray per block": torch.argsort(one_ray, descending=True, stable=True),
               "longest first, 8 sampled rays per block": torch.argsort(stride8, descending=True, stable=True),
               **{f"longest first, one sampled ray capped at {k} steps":
-                 torch.argsort(one_ray.clamp(max=k), descending=True, stable=True) for k in (16, 32, 48, 96)},
+                 torch.argsort(one_ray.clamp(max=k), descending=True, stable=True) for k in (16, 24, 32, 48, 96)},
+              **{f"longest first, one sampled ray capped at {k} steps, ties shuffled":
+                 torch.argsort(one_ray.clamp(max=k).to(torch.float64) * 4 + torch.rand(nb, device=dev,
+                               generator=torch.Generator(device=dev).manual_seed(3), dtype=torch.float64),
+                               descending=True) for k in (24, 32)},
               f"longest first, costs of the frame moved by {args.move}": torch.argsort(moved, descending=True,
                                                                                        stable=True)}
     for name, bo in orders.items():
