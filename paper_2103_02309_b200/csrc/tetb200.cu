@@ -1606,16 +1606,34 @@ __global__ void __launch_bounds__(64) block_probe_kernel(MeshView m, int64_t n, 
       const uint32_t nxt = ref;
 #ifndef TB_PROBE_NO_PREFETCH
       if constexpr (L == 20) {
-        // the walk here is a lone latency chain over a cold L2: the tet's
-        // neighbours are the next step's only candidates, so their records go
-        // to L2 while this step decides (one DRAM round trip per step, not two)
+        // The walk here is a lone latency chain over a cold L2.  The tet's four
+        // neighbours are the next step's only candidates: their records go to
+        // L2 while this step decides, and -- from their vx words, prefetched one
+        // step earlier and so L2 hits now -- so do the point copies of the
+        // vertex each would add (vx[n_k] ^ vx[t] ^ v_k, v_k the tet's k-th
+        // smallest vertex, across from n_k).  Each step then finds its record
+        // and its point in L2 instead of two DRAM round trips.
         const uint4 nb4 = __ldg(&m.rec4[nxt]);
+        const uint32_t vt = __ldg(&m.vx[nxt]);
+        const uint32_t a[4] = {idx[0], idx[1], idx[2], idx[0] ^ idx[1] ^ idx[2] ^ vt};
+        uint32_t v[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          int r = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) r += (a[j] < a[i]) ? 1 : 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[k] = (r == k) ? a[i] : v[k];
+        }
         const uint32_t nbs[4] = {nb4.x, nb4.y, nb4.z, nb4.w};
+        const uint32_t last_point = (uint32_t)m.n_points - 1u;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           if (nbs[k] < (uint32_t)m.n_tets) {
             asm volatile("prefetch.global.L2 [%0];" ::"l"(m.vx + nbs[k]));
             asm volatile("prefetch.global.L2 [%0];" ::"l"(m.rec4 + nbs[k]));
+            const uint32_t nv = min(__ldg(&m.vx[nbs[k]]) ^ vt ^ v[k], last_point);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(P + nv));
           }
       }
 #endif
