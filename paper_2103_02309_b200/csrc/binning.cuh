@@ -44,6 +44,26 @@ __device__ __forceinline__ int dir_bin(const float* __restrict__ d, int64_t r) {
   return ((2 * a + (m < 0.f)) * kBinFace + cu) * kBinFace + cv;
 }
 
+// Lanes of the (full) warp holding the same bin id (< 128, kBins included):
+// seven ballots over the id's bits instead of __match_any_sync, whose
+// MATCH.ANY is slow enough to matter once a pass matches twice per ray (r02:
+// config 4, a two-barrier scatter variant with two matches per ray +53 us per
+// step with MATCH.ANY, +0 with ballots; see profiles/r02_experiments.md).
+__device__ __forceinline__ unsigned bin_peers(int bin) {
+#ifdef TB_BIN_MATCH_ANY
+  return __match_any_sync(0xffffffffu, bin);
+#else
+  static_assert(kBins < 128, "bin ids (and the dead-lane id kBins) fit 7 bits");
+  unsigned m = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < 7; ++b) {
+    const unsigned v = __ballot_sync(0xffffffffu, (bin >> b) & 1);
+    m &= ((bin >> b) & 1) ? v : ~v;
+  }
+  return m;
+#endif
+}
+
 // Histogram index of (bin b, tile t): global sort (S == 0) bin-major over
 // all tiles; tile-local sort (S = tiles per segment) segment-major, then
 // bin, then the tile within the segment -- so one exclusive scan per segment
@@ -65,7 +85,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(const float* __r
     const int64_t r = base + i;
     const int bin = r < n ? dir_bin(d, r) : kBins;
     if (r < n) bins[r] = (uint8_t)bin;
-    const unsigned peers = __match_any_sync(0xffffffffu, bin);  // one shared-memory atomic per bin per warp
+    const unsigned peers = bin_peers(bin);  // one shared-memory atomic per bin per warp
     if (bin < kBins && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&cnt[bin], __popc(peers));
   }
   __syncthreads();
@@ -153,11 +173,11 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(int32_t* __restrict__ hi
 
 // Stable scatter of the permutation: perm[start of bin b + offset of the
 // tile within bin b + rank of ray r among the tile's bin-b rays, in caller
-// order] = r.  Ranks within a warp come from __match_any_sync peers.
+// order] = r.  Ranks within a warp come from bin_peers().
 __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint8_t* __restrict__ bins, int64_t n,
                                                                   const int32_t* __restrict__ offs,
                                                                   const int32_t* __restrict__ totals, int n_tiles,
-                                                                  int S, int64_t* __restrict__ perm) {
+                                                                  int S, int32_t* __restrict__ perm) {
   __shared__ int warp_cnt[kBinThreads / 32][kBins];
   __shared__ int running[kBins];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -178,14 +198,14 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint8_t*
     const int64_t r = base + round * kBinThreads + threadIdx.x;
     const bool live = r < n;
     const int bin = live ? (int)__ldg(bins + r) : kBins;
-    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    const unsigned peers = bin_peers(bin);
     const int rank = __popc(peers & ((1u << lane) - 1u));
     if (live && rank == 0) warp_cnt[warp][bin] = __popc(peers);
     __syncthreads();
     if (live) {
       int pos = running[bin] + rank;
       for (int w = 0; w < warp; ++w) pos += warp_cnt[w][bin];
-      perm[pos] = r;
+      perm[pos] = (int32_t)r;
     }
     __syncthreads();
     for (int b = threadIdx.x; b < kBins; b += kBinThreads) {
@@ -199,7 +219,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint8_t*
 
 // Scatter target of a binned walk whose results go to a caller's index
 // (multi-GPU frame assembly): widx[r] = oidx[perm[r]].
-__global__ void compose_index_kernel(const int64_t* __restrict__ perm, const int64_t* __restrict__ oidx, int64_t n,
+__global__ void compose_index_kernel(const int32_t* __restrict__ perm, const int64_t* __restrict__ oidx, int64_t n,
                                      int64_t* __restrict__ widx) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r < n) widx[r] = __ldg(oidx + __ldg(perm + r));

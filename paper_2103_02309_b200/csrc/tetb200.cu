@@ -522,8 +522,8 @@ __device__ __forceinline__ void walk_ray(const MeshView& m, float o0, float o1, 
 // ray's result is stored there by the epilogue the moment its walk ends.
 // kGather: ray r is read from index ridx[r] -- the direction-binned schedule
 // walks the rays in binned order straight from the caller's arrays, so the
-// binning pass writes only the 8-byte permutation; with kScatter its results
-// go back to oidx[r] (oidx == ridx: the ray's own slot).
+// binning pass writes only the 4-byte permutation; with kScatter its results
+// go back to oidx[r], or to ridx[r] (the ray's own slot) when oidx is null.
 template <int L, bool kClamp, bool kHostRays, bool kScatter, bool kGather = false, bool kBlockMap = false>
 __global__ void __launch_bounds__(kCastBlock, (cast_min_blocks<L, kGather>())) cast_kernel(MeshView m, int64_t n, const float* __restrict__ o,
                                                       const float* __restrict__ d,
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kCastBlock, (cast_min_blocks<L, kGather>())) c
                                                       int32_t* __restrict__ triangle, double* __restrict__ t,
                                                       int32_t* __restrict__ tet_back,
                                                       const int64_t* __restrict__ oidx,
-                                                      const int64_t* __restrict__ ridx,
+                                                      const int32_t* __restrict__ ridx,
                                                       const int32_t* __restrict__ bmap) {
   // kBlockMap: block b walks the rays of block bmap[b] (a caller-chosen launch
   // order of whole 128-ray blocks, e.g. longest first by a previous frame's
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kCastBlock, (cast_min_blocks<L, kGather>())) c
     cur = (uint32_t)__ldg(start + r);
   } else {
     if (r >= n) return;
-    const int64_t q = kGather ? __ldg(ridx + r) : r;
+    const int64_t q = kGather ? (int64_t)__ldg(ridx + r) : r;
     cur = (uint32_t)__ldg(start + q);
     o0 = __ldg(o + 3 * q); o1 = __ldg(o + 3 * q + 1); o2 = __ldg(o + 3 * q + 2);
     d0 = __ldg(d + 3 * q); d1 = __ldg(d + 3 * q + 1); d2 = __ldg(d + 3 * q + 2);
@@ -559,10 +559,10 @@ __global__ void __launch_bounds__(kCastBlock, (cast_min_blocks<L, kGather>())) c
   uint8_t st;
   walk_ray<L, kClamp>(m, o0, o1, o2, d0, d1, d2, cur, ref, vis, st);
   // kGather alone reads through ridx and stores in place; the binned walk
-  // stores back through its permutation (oidx == ridx: the index already
+  // stores back through its permutation (oidx null: the index already
   // loaded) or through a composed one (multi-GPU scatter of a binned batch)
   int64_t w = r;
-  if constexpr (kScatter) w = (kGather && oidx == ridx) ? __ldg(ridx + r) : __ldg(oidx + r);
+  if constexpr (kScatter) w = (kGather && oidx == nullptr) ? (int64_t)__ldg(ridx + r) : __ldg(oidx + r);
   if constexpr (kHostRays) {
     // Zero-copy outputs cross PCIe as the warps' stores: every array gets
     // >= 128 B per warp store except the 1-byte status (32 B per warp).  A
@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(kCastBlock, (cast_min_blocks<L, kGather>())) c
   }
 #ifndef TB_NO_RELOAD_RAY
   if constexpr (!kHostRays) {
-    const int64_t q = kGather ? __ldg(ridx + r) : r;
+    const int64_t q = kGather ? (int64_t)__ldg(ridx + r) : r;
     write_result_ray(m, w, st, ref, cur, vis, RayRef{o, d, q}, status, cf, tet, visited, triangle, t, tet_back);
     return;
   }
@@ -1254,7 +1254,7 @@ struct CastL {
   template <typename... A>
   static void launch(unsigned g, cudaStream_t s, bool safe, bool host_rays, const int64_t* oidx, A... a) {
     const bool nc = safe && L != 80;  // validated mesh: no per-step index clamp
-    const int64_t* none = nullptr;
+    const int32_t* none = nullptr;
     if (oidx != nullptr) {  // scattered outputs (device rays only)
       if (nc)
         cast_kernel<L, false, false, true><<<g, kCastBlock, 0, s>>>(a..., oidx, none, nullptr);
@@ -1279,10 +1279,11 @@ struct CastOrderedL {
   template <typename... A>
   static void launch(unsigned g, cudaStream_t s, bool safe, const int32_t* bmap, A... a) {
     const int64_t* none = nullptr;
+    const int32_t* no_gather = nullptr;
     if (safe && L != 80)
-      cast_kernel<L, false, false, false, false, true><<<g, kCastBlock, 0, s>>>(a..., none, none, bmap);
+      cast_kernel<L, false, false, false, false, true><<<g, kCastBlock, 0, s>>>(a..., none, no_gather, bmap);
     else
-      cast_kernel<L, true, false, false, false, true><<<g, kCastBlock, 0, s>>>(a..., none, none, bmap);
+      cast_kernel<L, true, false, false, false, true><<<g, kCastBlock, 0, s>>>(a..., none, no_gather, bmap);
   }
 };
 // Binned walk: rays read through perm; results stored through widx (perm
@@ -1290,7 +1291,7 @@ struct CastOrderedL {
 template <int L>
 struct CastBinnedL {
   template <typename... A>
-  static void launch(unsigned g, cudaStream_t s, bool safe, const int64_t* perm, const int64_t* widx, A... a) {
+  static void launch(unsigned g, cudaStream_t s, bool safe, const int32_t* perm, const int64_t* widx, A... a) {
     if (safe && L != 80)
       cast_kernel<L, false, false, true, true><<<g, kCastBlock, 0, s>>>(a..., widx, perm, nullptr);
     else
@@ -1724,12 +1725,12 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
     const size_t hist_b = ((hist_n + kBins) * 4 + 255) & ~(size_t)255;
     char* scratch = nullptr;
     const size_t widx_b = oidx ? (size_t)n * 8 : 0;  // perm composed with the caller's scatter index
-    if (int e2 = scratch_alloc(m->device, hist_b + (size_t)n * 8 + widx_b + (size_t)n, s, &scratch)) return e2;
+    if (int e2 = scratch_alloc(m->device, hist_b + widx_b + (size_t)n * 4 + (size_t)n, s, &scratch)) return e2;
     int32_t* hist = reinterpret_cast<int32_t*>(scratch);
     int32_t* totals = hist + hist_n;
-    int64_t* perm = reinterpret_cast<int64_t*>(scratch + hist_b);
-    int64_t* widx = oidx ? reinterpret_cast<int64_t*>(scratch + hist_b + (size_t)n * 8) : perm;
-    uint8_t* bins = reinterpret_cast<uint8_t*>(scratch + hist_b + (size_t)n * 8 + widx_b);
+    int64_t* widx = oidx ? reinterpret_cast<int64_t*>(scratch + hist_b) : nullptr;  // null: results to perm[r]
+    int32_t* perm = reinterpret_cast<int32_t*>(scratch + hist_b + widx_b);
+    uint8_t* bins = reinterpret_cast<uint8_t*>(scratch + hist_b + widx_b + (size_t)n * 4);
     if (S) {
       if (cudaError_t me = cudaMemsetAsync(hist, 0, hist_n * 4, s)) {  // the ragged segment's missing tiles count 0
         cudaFreeAsync(scratch, s);
@@ -2113,25 +2114,26 @@ struct ShardKey {
   }
 };
 std::mutex g_shard_mu;
-std::map<ShardKey, std::pair<int64_t*, int64_t>> g_shards;  // device index arrays, kept for the process
+std::map<ShardKey, std::pair<int32_t*, int64_t>> g_shards;  // device index arrays, kept for the process
 
-int shard_indices(int device, int64_t W, int64_t H, int parts, int part, const int64_t** idx, int64_t* count) {
+int shard_indices(int device, int64_t W, int64_t H, int parts, int part, const int32_t** idx, int64_t* count) {
   std::lock_guard<std::mutex> lk(g_shard_mu);
   const ShardKey key{device, W, H, parts, part};
   auto it = g_shards.find(key);
   if (it == g_shards.end()) {
-    std::vector<int64_t> h;
+    if (W * H > INT32_MAX) return set_error(TB_E_ARG, "frame of %lld pixels: pixel indices exceed int32", (long long)(W * H));
+    std::vector<int32_t> h;
     const int64_t tx = (W + 15) / 16, ty = (H + 15) / 16;
     for (int64_t k = part; k < tx * ty; k += parts) {
       const int64_t x0 = (k % tx) * 16, y0 = (k / tx) * 16;
       for (int64_t y = y0; y < std::min(H, y0 + 16); ++y)
-        for (int64_t x = x0; x < std::min(W, x0 + 16); ++x) h.push_back(y * W + x);
+        for (int64_t x = x0; x < std::min(W, x0 + 16); ++x) h.push_back((int32_t)(y * W + x));
     }
-    int64_t* dptr = nullptr;
+    int32_t* dptr = nullptr;
     if (!h.empty()) {
       DeviceGuard g(device);
-      TB_CUDA(cudaMalloc((void**)&dptr, h.size() * sizeof(int64_t)));
-      TB_CUDA(cudaMemcpy(dptr, h.data(), h.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+      TB_CUDA(cudaMalloc((void**)&dptr, h.size() * sizeof(int32_t)));
+      TB_CUDA(cudaMemcpy(dptr, h.data(), h.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     it = g_shards.emplace(key, std::make_pair(dptr, (int64_t)h.size())).first;
   }
@@ -2192,7 +2194,7 @@ int tb_trace_multi(int n_meshes, tb_mesh* const* meshes, int64_t width, int64_t 
   std::vector<cudaEvent_t> done;
   for (int k = 0; k < n_meshes && err == TB_OK; ++k) {
     tb_mesh* m = meshes[k];
-    const int64_t* idx = nullptr;
+    const int32_t* idx = nullptr;
     int64_t count = 0;
     if ((err = shard_indices(m->device, width, height, n_meshes, k, &idx, &count)) != TB_OK || count == 0) continue;
     DeviceGuard g(m->device);
@@ -2215,7 +2217,7 @@ int tb_trace_multi(int n_meshes, tb_mesh* const* meshes, int64_t width, int64_t 
       err = set_error(TB_E_CUDA, "cross-device wait failed");
       break;
     }
-    if ((err = launch_layout<CastBinnedL>(m->layout, grid_for(count, kCastBlock), sk, m->safe, idx, idx, m->view(), count, o,
+    if ((err = launch_layout<CastBinnedL>(m->layout, grid_for(count, kCastBlock), sk, m->safe, idx, nullptr, m->view(), count, o,
                                           d, start, status, cf, tet, visited, triangle, t, tet_back)) != TB_OK)
       break;
     if (sk != s0) {
