@@ -582,20 +582,19 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
 
-    # ray schedule: one ray per lane for primaries; incoherent secondaries
-    # (config 4) are binned by direction cell first (96 cube-map cells) and
-    # walked in binned order (r01: 3.36 vs 2.37 Grays/s one ray per lane).
     # ray schedule: incoherent secondaries (config 4) are binned by direction
     # cell first (96 cube-map cells) and walked in binned order (r01: 3.36 vs
     # 2.37 Grays/s one ray per lane); primaries take "auto": the sampled
-    # longest-first block order for launches of <= 16 waves (config 2), one
-    # ray per lane beyond (tb_auto_schedule)
+    # longest-first block order, split so its pre-pass hides under the head of
+    # the launch, for launches of 6-48 waves (configs 2 and 3), one ray per
+    # lane otherwise (tb_auto_schedule)
     schedule = args.schedule or ("binned" if cfg.get("secondaries") else "auto")
     if schedule == "auto" and world == 1 and not sctp:
         from paper_2103_02309_b200._lib import SCHEDULES
 
         resolved = int(lib.tb_auto_schedule(local, n))
         schedule = next(k for k, v in SCHEDULES.items() if v == resolved)
+    split = schedule == "sampled" and world == 1 and int(lib.tb_sampled_head_blocks(local, n)) > 0
 
     def step():
         trace(dm, go, gd, gs, out=res, stream=stream, sctp=sctp, schedule=schedule)
@@ -868,8 +867,12 @@ def run_ours(args, cfg):
              f"{'cast_compact_kernel' if schedule in ('compact', 'compact512') else 'cast_kernel'}"
              f"<{cfg['layout'][3:]}>" + (" after bin_count/bin_seg_scan/bin_scatter (direction binning, inside "
                                           "the events)" if schedule == "binned" else
-                                          " with its blocks launched longest first, after block_probe/"
-                                          "block_scatter (a capped one-ray-per-block pre-pass, inside the events)"
+                                          (" with its tail's blocks launched longest first: the head walks in "
+                                           "launch order while block_probe/block_scatter (a capped one-ray-per-block "
+                                           "pre-pass) order the tail on a high-priority side stream, all inside the "
+                                           "events" if split else
+                                           " with its blocks launched longest first, after block_probe/"
+                                           "block_scatter (a capped one-ray-per-block pre-pass, inside the events)")
                                           if schedule == "sampled" else ""))
     hbm = {"bound": "hbm", "achieved": alg / kern_s / 1e9, "peak": peak, "unit": "GB/s", "peak_source": peak_src,
            "algorithmic_bytes_per_launch": alg,
@@ -907,8 +910,10 @@ def run_ours(args, cfg):
                         if (not sctp and cfg["layout"] != "tet80" and not args.no_l2_probe) else None),
         "clocks": dict(clk, window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
         "gpu_launches": args.steps * ((1 if fg is None else sum(1 for a, b in fg.my_pieces() if b > a))
-                                      * (4 if schedule == "binned" else (3 if schedule == "sampled" else 1))
+                                      * (4 if schedule == "binned" else
+                                         ((4 if split else 3) if schedule == "sampled" else 1))
                                       # binned: count, scan, scatter, walk; sampled: probe, scatter, walk
+                                      # (+ the head's walk when split)
                                       + (1 if (pg is not None and schedule == "binned") else 0)  # compose
                                       + (1 if pg is not None and pg.lean else 0)),  # lean p2p: root epilogue
         "parity": parity,

@@ -174,9 +174,15 @@ int tb_cast_rays_sched(tb_mesh* mesh, int64_t n, const float* o, const float* d,
 /* Rays per block of the cast kernels (the unit of tb_cast_rays_ordered). */
 int tb_cast_block_size(void);
 /* The schedule "auto" (mode 0) resolves to for a device-resident batch of n
- * rays on `device`: 7 (sampled longest-first) while the launch has at most 16
- * waves of blocks, else 1 (one ray per lane). */
+ * rays on `device`: 7 (sampled longest-first) for launches of 6 to 48 waves
+ * of blocks (a wave = SMs x 10 blocks), else 1 (one ray per lane). */
 int tb_auto_schedule(int device, int64_t n);
+/* Schedule 7's split for n rays on `device`: the number of leading blocks
+ * that walk in launch order while the pre-pass orders the rest (0: no split,
+ * every block ordered after the pre-pass).  At least 3 waves, the rest
+ * ~65 % of the launch and at most 16 waves; TETB200_ORDER_TAIL (percent)
+ * overrides.  Lets a caller count the launches (4 kernels split, 3 not). */
+int64_t tb_sampled_head_blocks(int device, int64_t n);
 /* tb_cast_rays with a caller-chosen launch order of whole blocks: launch slot
  * b walks the tb_cast_block_size() rays of block block_order[b] (a
  * permutation of the n_blocks = ceil(n / block) blocks); rays are read and
@@ -317,7 +323,11 @@ int tb_sctp_cast_rays_host(tb_mesh* mesh, int64_t n, const float* o, const float
  *   32 steps orders the blocks longest first, then the full walk launches
  *   them in that order (tb_cast_rays_ordered's kernel) -- for coherent
  *   device-resident primaries, whose launch otherwise ends on a few late
- *   long rays.  Results are identical in every mode. 
+ *   long rays.  Split launches (tb_sampled_head_blocks > 0): the leading
+ *   blocks walk in launch order on the caller's stream while a
+ *   high-priority internal stream probes, orders and launches the rest; the
+ *   caller's stream waits for it before the call's later work.  Results are
+ *   identical in every mode. 
  * Process-wide; overrides TETB200_SCHED / TETB200_ROUND.  A negative
  * argument leaves that setting unchanged. */
 int tb_set_schedule(int mode, int steps_per_round);

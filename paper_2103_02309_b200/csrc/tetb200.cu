@@ -1550,7 +1550,7 @@ __global__ void block_key_kernel(const int32_t* __restrict__ visited, int64_t n,
 }
 
 __global__ void block_scatter_kernel(const uint8_t* __restrict__ key, int64_t nb, const int* __restrict__ hist,
-                                     int* __restrict__ cursor, int32_t* __restrict__ order) {
+                                     int* __restrict__ cursor, int32_t* __restrict__ order, int64_t b0 = 0) {
   __shared__ int base[kOrderBuckets];
   if (threadIdx.x < 32) {  // exclusive scan of the histogram, 2 buckets per lane
     const int a = hist[2 * threadIdx.x], c = hist[2 * threadIdx.x + 1];
@@ -1573,7 +1573,7 @@ __global__ void block_scatter_kernel(const uint8_t* __restrict__ key, int64_t nb
   int pos = 0;
   if ((int)(threadIdx.x & 31) == leader) pos = atomicAdd(cursor + k, __popc(peers));
   pos = __shfl_sync(peers, pos, leader);
-  order[base[k] + pos + rank] = (int32_t)b;
+  order[base[k] + pos + rank] = (int32_t)(b0 + b);
 }
 
 // Sampled cost pre-pass of schedule 7 ("sampled"): one ray per block -- the
@@ -1585,9 +1585,10 @@ __global__ void block_scatter_kernel(const uint8_t* __restrict__ key, int64_t nb
 template <int L, bool kClamp>
 __global__ void __launch_bounds__(64) block_probe_kernel(MeshView m, int64_t n, const float* __restrict__ o,
                                                          const float* __restrict__ d,
-                                                         const int32_t* __restrict__ start, int64_t nb, int cap,
-                                                         uint8_t* __restrict__ key, int* __restrict__ hist) {
-  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+                                                         const int32_t* __restrict__ start, int64_t b0, int64_t nb,
+                                                         int cap, uint8_t* __restrict__ key, int* __restrict__ hist) {
+  // blocks b0 .. nb-1 (the ordered tail of a split launch; b0 = 0: all)
+  const int64_t b = b0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool in = b < nb;
   int steps = 0;
   if (in) {
@@ -1644,7 +1645,7 @@ __global__ void __launch_bounds__(64) block_probe_kernel(MeshView m, int64_t n, 
     }
   }
   const int k = kOrderBuckets - 1 - min(steps, kOrderBuckets - 1);
-  if (in) key[b] = (uint8_t)k;
+  if (in) key[b - b0] = (uint8_t)k;
   const unsigned act = __ballot_sync(0xffffffffu, in);
   if (!in) return;
   const unsigned peers = __match_any_sync(act, k);
@@ -1662,25 +1663,55 @@ struct BlockProbeL {
   }
 };
 
-// Schedule 0 ("auto") for device-resident batches: the sampled longest-first
-// order (7) while the launch has at most kSampledWaves waves of blocks --
-// there the SM-idle tail of the last wave is a large share of the launch
-// (config 2, 1080p: 11 waves, +4-6 % net of its pre-pass) -- and one ray per
-// lane (1) beyond, where the tail is diluted and the pre-pass, a latency-bound
-// walk over a cold L2, costs more than it returns (config 3: 44 waves, -1.6 %;
-// config 5: 175 waves, -5.7 %; r02 A/B).  Incoherent batches ask for "binned".
-constexpr int64_t kSampledWaves = 16;
-int auto_schedule(int device, int64_t n) {
+// Blocks per wave of the walk on `device` (SMs x the 10 resident blocks of
+// the 48-register walks).
+int64_t cast_wave(int device) {
   static std::atomic<int> sms[64];
-  if (device < 0 || device >= 64) return 1;
-  int c = sms[device].load(std::memory_order_relaxed);
+  int c = device >= 0 && device < 64 ? sms[device].load(std::memory_order_relaxed) : 148;
   if (c == 0) {
     if (cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || c <= 0) c = 148;
     sms[device].store(c, std::memory_order_relaxed);
   }
+  return (int64_t)c * TB_CAST_MIN_BLOCKS;
+}
+
+// Schedule 7's split (cast_dispatch): the first head_blocks() blocks walk in
+// launch order while the pre-pass orders the rest, which then launch longest
+// first on a high-priority side stream.  The head must outlast the pre-pass
+// (~20-25 us, a lone latency chain): at least kHeadWaves waves.  The ordered
+// tail is ~65 % of the launch, at most kTailWaves waves: only the last waves'
+// order shapes the SM-idle tail, and a longer sorted stretch only trades away
+// the frame order's L2 locality.  r02 A/B (profiles/r02_experiments.md):
+// config 2 (11 waves) tail 50 / 65 / 80 % -> 0.1776 / 0.1715 / 0.1836 ms;
+// config 3 (44 waves) tail 35 / 50 / 65 % -> 0.7209 / 0.7225 / 0.7306 ms;
+// 1 M rays (5.5 waves) tail 50 / 60 % -> 0.0975 / 0.114 ms.
+// TETB200_ORDER_TAIL (percent of the blocks, experiment knob) overrides.
+constexpr int64_t kHeadWaves = 3, kTailWaves = 16;
+int64_t head_blocks(int device, int64_t nb) {
+  static const int pct = [] {
+    const char* v = getenv("TETB200_ORDER_TAIL");
+    return v ? std::min(100, std::max(1, atoi(v))) : 0;
+  }();
+  if (pct) return nb - std::max<int64_t>(1, nb * pct / 100);
+  const int64_t wave = cast_wave(device);
+  const int64_t tail = std::min(nb * 65 / 100, kTailWaves * wave);
+  const int64_t head = std::max(nb - tail, kHeadWaves * wave);
+  return head >= nb ? 0 : head;  // too short to split: order every block, pre-pass first
+}
+
+// Schedule 0 ("auto") for device-resident batches: the sampled longest-first
+// order (7) for launches of kSampledMinWaves .. kSampledMaxWaves waves, one
+// ray per lane (1) otherwise.  Short launches cannot hide the pre-pass under a
+// head (262 K / 524 K rays: lane 0.068 / 0.080 ms, sampled 0.089 / 0.098);
+// long ones have a diluted tail and lose frame-order locality (config 5, 146
+// waves: -0.6 %).  Config 2 (11 waves) +18 %, config 3 (44 waves) +2.5 %
+// (r02 A/B).  Incoherent batches ask for "binned".
+constexpr int64_t kSampledMinWaves = 6, kSampledMaxWaves = 48;
+int auto_schedule(int device, int64_t n) {
+  if (device < 0 || device >= 64) return 1;
   const int64_t nb = (n + kCastBlock - 1) / kCastBlock;
-  const int64_t wave = (int64_t)c * TB_CAST_MIN_BLOCKS;
-  return nb <= kSampledWaves * wave ? 7 : 1;
+  const int64_t wave = cast_wave(device);
+  return nb >= kSampledMinWaves * wave && nb <= kSampledMaxWaves * wave ? 7 : 1;
 }
 
 int probe_cap() {
@@ -1698,6 +1729,46 @@ int check_mesh(const tb_mesh* m) {
 }
 
 // Launch the traversal with an explicit schedule (see sched_mode).
+// Schedule 7's side stream (highest priority: once the tail's order exists,
+// its blocks take the SM slots the head's retiring blocks free, so the long
+// blocks start early and the head's remainder fills in behind them -- at
+// default priority the tail waited for the whole head: config 2 0.1959 vs
+// 0.1784 ms at a 60 % tail) and a fork / join event pair, per (host thread,
+// device).
+struct OrderSide {
+  cudaStream_t s[64] = {};
+  cudaEvent_t fork[64] = {}, join[64] = {};
+  ~OrderSide() {
+    for (int dv = 0; dv < 64; ++dv) {
+      if (!s[dv]) continue;
+      int prev = -1;
+      cudaGetDevice(&prev);
+      cudaSetDevice(dv);
+      cudaStreamSynchronize(s[dv]);
+      cudaEventDestroy(fork[dv]);
+      cudaEventDestroy(join[dv]);
+      cudaStreamDestroy(s[dv]);
+      if (prev >= 0) cudaSetDevice(prev);
+    }
+    cudaGetLastError();
+  }
+};
+int order_side(int device, cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join) {
+  static thread_local OrderSide o;
+  if (device < 0 || device >= 64) return set_error(TB_E_ARG, "device %d out of range", device);
+  if (!o.s[device]) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (cudaStreamCreateWithPriority(&o.s[device], cudaStreamNonBlocking, greatest) != cudaSuccess ||
+        cudaEventCreateWithFlags(&o.fork[device], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&o.join[device], cudaEventDisableTiming) != cudaSuccess)
+      return set_error(TB_E_CUDA, "side stream for the sampled schedule: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  *side = o.s[device];
+  *fork = o.fork[device];
+  *join = o.join[device];
+  return TB_OK;
+}
 int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start, uint8_t* status,
                   int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back,
                   cudaStream_t s, int mode, bool host_rays = false, const int64_t* oidx = nullptr) {
@@ -1750,24 +1821,48 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
   } else if (mode == 7 && !host_rays && oidx == nullptr) {
     // sampled longest-first: a capped walk of one ray per block orders the
     // blocks (block_probe_kernel -> block_scatter_kernel), then the full walk
-    // launches them in that order, rays and results in place
+    // launches them in that order, rays and results in place.  Split (b0 > 0):
+    // the head's blocks walk in launch order on the caller's stream while the
+    // side stream probes and orders the tail, which launches longest first at
+    // high priority; the caller's stream joins the side stream at the end.
     const int64_t nb = (n + kCastBlock - 1) / kCastBlock;
-    const size_t kb = ((size_t)nb + 255) / 256 * 256, hb = 2 * kOrderBuckets * sizeof(int);
+    const int64_t b0 = head_blocks(m->device, nb);  // first block of the ordered tail
+    const int64_t nt = nb - b0;
+    const size_t kb = ((size_t)nt + 255) / 256 * 256, hb = 2 * kOrderBuckets * sizeof(int);
     char* scratch = nullptr;
-    if (int e2 = scratch_alloc(m->device, kb + hb + (size_t)nb * 4, s, &scratch)) return e2;
+    if (int e2 = scratch_alloc(m->device, kb + hb + (size_t)nt * 4, s, &scratch)) return e2;
     uint8_t* key = reinterpret_cast<uint8_t*>(scratch);
     int* hist = reinterpret_cast<int*>(scratch + kb);
     int32_t* order = reinterpret_cast<int32_t*>(scratch + kb + hb);
-    if (cudaError_t me = cudaMemsetAsync(hist, 0, hb, s)) {
-      cudaFreeAsync(scratch, s);
-      return set_error(TB_E_CUDA, "sampled schedule memset: %s", cudaGetErrorString(me));
+    cudaStream_t side = s;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (b0 > 0) {  // split launch: fork the side stream off the caller's
+      if (int e2 = order_side(m->device, &side, &fork, &join)) {
+        cudaFreeAsync(scratch, s);
+        return e2;
+      }
+      if (cudaEventRecord(fork, s) != cudaSuccess || cudaStreamWaitEvent(side, fork, 0) != cudaSuccess) {
+        cudaFreeAsync(scratch, s);
+        return set_error(TB_E_CUDA, "sampled schedule fork: %s", cudaGetErrorString(cudaGetLastError()));
+      }
     }
-    e = launch_layout<BlockProbeL>(m->layout, grid_for(nb, 64), s, m->safe, v, n, o, d, start, nb, probe_cap(), key,
-                                   hist);
+    if (cudaError_t me = cudaMemsetAsync(hist, 0, hb, side)) {
+      e = set_error(TB_E_CUDA, "sampled schedule memset: %s", cudaGetErrorString(me));
+    } else {
+      e = launch_layout<BlockProbeL>(m->layout, grid_for(nt, 64), side, m->safe, v, n, o, d, start, b0, nb,
+                                     probe_cap(), key, hist);
+    }
+    if (!e && b0 > 0)  // the head, in launch order, on the caller's stream
+      e = launch_layout<CastL>(m->layout, (unsigned)b0, s, m->safe, false, (const int64_t*)nullptr, v,
+                               b0 * kCastBlock, o, d, start, status, cf, tet, visited, triangle, t, tet_back);
     if (!e) {
-      block_scatter_kernel<<<grid_for(nb, 256), 256, 0, s>>>(key, nb, hist, hist + kOrderBuckets, order);
-      e = launch_layout<CastOrderedL>(m->layout, (unsigned)nb, s, m->safe, (const int32_t*)order, v, n, o, d, start,
-                                      status, cf, tet, visited, triangle, t, tet_back);
+      block_scatter_kernel<<<grid_for(nt, 256), 256, 0, side>>>(key, nt, hist, hist + kOrderBuckets, order, b0);
+      e = launch_layout<CastOrderedL>(m->layout, (unsigned)nt, side, m->safe, (const int32_t*)order, v, n, o, d,
+                                      start, status, cf, tet, visited, triangle, t, tet_back);
+    }
+    if (b0 > 0) {  // join (also on error: nothing may stay queued on the side stream past the free)
+      const bool ok = cudaEventRecord(join, side) == cudaSuccess && cudaStreamWaitEvent(s, join, 0) == cudaSuccess;
+      if (!ok && !e) e = set_error(TB_E_CUDA, "sampled schedule join: %s", cudaGetErrorString(cudaGetLastError()));
     }
     cudaFreeAsync(scratch, s);
   } else if (mode == 5 && !host_rays) {
@@ -2306,6 +2401,10 @@ int tb_cast_rays_sched(tb_mesh* m, int64_t n, const float* o, const float* d, co
 int tb_cast_block_size(void) { return kCastBlock; }
 
 int tb_auto_schedule(int device, int64_t n) { return n < 0 ? -1 : auto_schedule(device, n); }
+
+int64_t tb_sampled_head_blocks(int device, int64_t n) {
+  return n < 0 ? -1 : head_blocks(device, (n + kCastBlock - 1) / kCastBlock);
+}
 
 int tb_block_order(int64_t n, const int32_t* visited, int32_t* order, int64_t n_blocks, void* stream) {
   if (n < 0) return set_error(TB_E_ARG, "negative ray count");

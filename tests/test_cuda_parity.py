@@ -762,6 +762,37 @@ def test_sampled_schedule_matches_lane(golden, digests, K, layout):
         o, d = camera_rays((4.0, 4.0, 0.5), (4.0, 4.0, 8.0), (0.0, 1.0, 0.0), 68.0, 1024, 1024)
         st = np.full(len(o), digests["lattice8/cam_tet"], np.int32)
         g = [torch.from_numpy(a).to(dev) for a in (o, d, st)]
+        from paper_2103_02309_b200._lib import lib
+
+        # 1 M rays = 8192 blocks: a split launch (head in launch order, the
+        # probed tail longest first on the side stream), also with a ragged tail
+        assert lib.tb_sampled_head_blocks(0, len(o)) > 0
         a = trace(m, *g, schedule="sampled")
         assert digest(*(getattr(a, k).cpu().numpy() for k in ("status", "cf", "tet", "visited"))) == \
             digests["lattice8/cast"]
+        n = len(o) - 77
+        a = trace(m, *(x[:n] for x in g), schedule="sampled")
+        b = trace(m, *(x[:n] for x in g), schedule="lane")
+        for k in NAMES7:
+            assert torch.equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_sampled_split_rule():
+    """tb_sampled_head_blocks / tb_auto_schedule: no split below 3 waves of
+    blocks, a head of >= 3 waves and a tail of <= 16 waves beyond; auto picks
+    the sampled schedule for 6-48 waves only."""
+    import torch
+
+    from paper_2103_02309_b200._lib import lib
+
+    wave = torch.cuda.get_device_properties(0).multi_processor_count * 10
+    blk = lib.tb_cast_block_size()
+    for waves in (0.5, 2, 3, 5.5, 11, 44, 146):
+        n = int(waves * wave * blk)
+        nb = -(-n // blk)
+        head = lib.tb_sampled_head_blocks(0, n)
+        if nb <= 3 * wave:
+            assert head == 0, waves
+        else:
+            assert head >= 3 * wave and nb - head <= 16 * wave and nb - head >= 1, (waves, head)
+        assert lib.tb_auto_schedule(0, n) == (7 if 6 * wave <= nb <= 48 * wave else 1), waves

@@ -88,6 +88,10 @@ def main():
 
             tiles = shard_pixels(cfg["width"], cfg["height"], 0, 1, 16)
             o, d = o[tiles], d[tiles]
+        if os.environ.get("AB_RAYS"):  # only the first N rays of the frame (small launches)
+            o, d = o[: int(os.environ["AB_RAYS"])], d[: int(os.environ["AB_RAYS"])]
+        if os.environ.get("AB_FLIP"):  # the frame's rays in reverse order (bottom-right tile first)
+            o, d = np.ascontiguousarray(o[::-1]), np.ascontiguousarray(d[::-1])
         dm = device_mesh(mesh)
         cam, _ = locate(dm, torch.tensor(pos[None], dtype=torch.float64, device=dev),
                         torch.tensor([mesh.source_tet], dtype=torch.int32, device=dev))
