@@ -866,7 +866,9 @@ def run_ours(args, cfg):
     kname = (f"sctp_kernel<{cfg['layout'][3:]}>" if sctp else
              f"{'cast_compact_kernel' if schedule in ('compact', 'compact512') else 'cast_kernel'}"
              f"<{cfg['layout'][3:]}>" + (" after bin_count/bin_seg_scan/bin_scatter (direction binning, inside "
-                                          "the events)" if schedule == "binned" else
+                                          "the events; in two pieces of whole sorting segments when "
+                                          "tb_binned_pieces says so: the second binned on a high-priority side "
+                                          "stream beside the first one's walk)" if schedule == "binned" else
                                           (" with its tail's blocks launched longest first: the head walks in "
                                            "launch order while block_probe/block_scatter (a capped one-ray-per-block "
                                            "pre-pass) order the tail on a high-priority side stream, all inside the "
@@ -910,9 +912,11 @@ def run_ours(args, cfg):
                         if (not sctp and cfg["layout"] != "tet80" and not args.no_l2_probe) else None),
         "clocks": dict(clk, window=f"{args.ramp_s:.1f}s untimed ramp + timed region"),
         "gpu_launches": args.steps * ((1 if fg is None else sum(1 for a, b in fg.my_pieces() if b > a))
-                                      * (4 if schedule == "binned" else
+                                      * (4 * (int(lib.tb_binned_pieces(n)) if pg is None else 1)
+                                         if schedule == "binned" else
                                          ((4 if split else 3) if schedule == "sampled" else 1))
-                                      # binned: count, scan, scatter, walk; sampled: probe, scatter, walk
+                                      # binned: count, scan, scatter, walk (per piece); sampled: probe,
+                                      # scatter, walk
                                       # (+ the head's walk when split)
                                       + (1 if (pg is not None and schedule == "binned") else 0)  # compose
                                       + (1 if pg is not None and pg.lean else 0)),  # lean p2p: root epilogue

@@ -183,6 +183,14 @@ int tb_auto_schedule(int device, int64_t n);
  * ~65 % of the launch and at most 16 waves; TETB200_ORDER_TAIL (percent)
  * overrides.  Lets a caller count the launches (4 kernels split, 3 not). */
 int64_t tb_sampled_head_blocks(int device, int64_t n);
+/* Schedule 6 ("binned") for n device-resident rays without a scatter index:
+ * 2 when the batch spans two or more 262144-ray sorting segments -- the
+ * segments' first half is binned and walks on the caller's stream while the
+ * second half is binned on a high-priority internal stream beside that walk
+ * and walks there (config-2 secondaries +7.6 %, config 4 neutral; the sort is
+ * segment-local, so the permutation is unchanged) -- else 1.
+ * TETB200_BIN_SPLIT=0 disables the split. */
+int tb_binned_pieces(int64_t n);
 /* tb_cast_rays with a caller-chosen launch order of whole blocks: launch slot
  * b walks the tb_cast_block_size() rays of block block_order[b] (a
  * permutation of the n_blocks = ceil(n / block) blocks); rays are read and

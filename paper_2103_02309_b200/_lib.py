@@ -47,6 +47,7 @@ _SIGS = {
     "tb_cast_block_size": (c_int, []),
     "tb_auto_schedule": (c_int, [c_int, c_int64]),
     "tb_sampled_head_blocks": (c_int64, [c_int, c_int64]),
+    "tb_binned_pieces": (c_int, [c_int64]),
     "tb_block_order": (c_int, [c_int64, P, P, c_int64, c_void_p]),
     "tb_cast_rays_ordered": (c_int, [c_void_p, c_int64, P, P, P, P, c_int64, P, P, P, P, P, P, P, c_void_p]),
     "tb_cast_rays_scatter": (c_int, [c_void_p, c_int64, P, P, P, P, P, P, P, P, P, P, P, c_void_p]),

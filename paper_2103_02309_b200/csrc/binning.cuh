@@ -76,11 +76,12 @@ __device__ __forceinline__ int64_t hist_at(int b, int t, int n_tiles, int S) {
 // (so the scatter pass reads 1 byte per ray instead of the direction).
 __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(const float* __restrict__ d, int64_t n,
                                                                 int32_t* __restrict__ hist, int n_tiles, int S,
-                                                                uint8_t* __restrict__ bins) {
+                                                                uint8_t* __restrict__ bins, int tile0 = 0) {
   __shared__ int cnt[kBins];
   for (int b = threadIdx.x; b < kBins; b += kBinThreads) cnt[b] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kBinTile;
+  const int tile = tile0 + (int)blockIdx.x;  // tile0: first tile of a chunk of segments
+  const int64_t base = (int64_t)tile * kBinTile;
   for (int i = threadIdx.x; i < kBinTile; i += kBinThreads) {  // warp-uniform trip count
     const int64_t r = base + i;
     const int bin = r < n ? dir_bin(d, r) : kBins;
@@ -89,20 +90,21 @@ __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(const float* __r
     if (bin < kBins && (peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&cnt[bin], __popc(peers));
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < kBins; b += kBinThreads) hist[hist_at(b, blockIdx.x, n_tiles, S)] = cnt[b];
+  for (int b = threadIdx.x; b < kBins; b += kBinThreads) hist[hist_at(b, tile, n_tiles, S)] = cnt[b];
 }
 
 // Segmented mode: one block per segment, exclusive scan of its kBins * S
 // counts in place, offset by the segment's first ray.
-__global__ void __launch_bounds__(1024) bin_seg_scan_kernel(int32_t* __restrict__ hist, int S) {
+__global__ void __launch_bounds__(1024) bin_seg_scan_kernel(int32_t* __restrict__ hist, int S, int seg0 = 0) {
   __shared__ int32_t warp_sum[32];
   __shared__ int32_t carry;
   const int len = kBins * S;
-  int32_t* row = hist + (int64_t)blockIdx.x * len;
+  const int seg = seg0 + (int)blockIdx.x;
+  int32_t* row = hist + (int64_t)seg * len;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  const int32_t seg_base = blockIdx.x * S * kBinTile;
+  const int32_t seg_base = seg * S * kBinTile;
   for (int base = 0; base < len; base += 1024) {
     const int i = base + threadIdx.x;
     const int32_t v = i < len ? row[i] : 0;
@@ -177,8 +179,9 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(int32_t* __restrict__ hi
 __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint8_t* __restrict__ bins, int64_t n,
                                                                   const int32_t* __restrict__ offs,
                                                                   const int32_t* __restrict__ totals, int n_tiles,
-                                                                  int S, int32_t* __restrict__ perm) {
+                                                                  int S, int32_t* __restrict__ perm, int tile0 = 0) {
   __shared__ int warp_cnt[kBinThreads / 32][kBins];
+  const int tile = tile0 + (int)blockIdx.x;
   __shared__ int running[kBins];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {  // global sort: bin starts = exclusive prefix of the 96 totals
@@ -189,8 +192,8 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint8_t*
     }
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < kBins; b += kBinThreads) running[b] += offs[hist_at(b, blockIdx.x, n_tiles, S)];
-  const int64_t base = (int64_t)blockIdx.x * kBinTile;
+  for (int b = threadIdx.x; b < kBins; b += kBinThreads) running[b] += offs[hist_at(b, tile, n_tiles, S)];
+  const int64_t base = (int64_t)tile * kBinTile;
   for (int round = 0; round < kBinTile / kBinThreads; ++round) {
     if (base + round * kBinThreads >= n) break;  // block-uniform
     for (int k = threadIdx.x; k < (kBinThreads / 32) * kBins; k += kBinThreads) (&warp_cnt[0][0])[k] = 0;

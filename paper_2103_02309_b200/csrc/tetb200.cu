@@ -1769,6 +1769,18 @@ int order_side(int device, cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* j
   *join = o.join[device];
   return TB_OK;
 }
+// TETB200_BIN_SPLIT=0 keeps the binned schedule on the caller's stream in one
+// piece (A/B; results are identical either way)
+#ifndef TB_BIN_SPLIT_DEFAULT
+#define TB_BIN_SPLIT_DEFAULT 1
+#endif
+bool bin_split() {
+  static const int v = [] {
+    const char* e = getenv("TETB200_BIN_SPLIT");
+    return e ? atoi(e) : TB_BIN_SPLIT_DEFAULT;
+  }();
+  return v > 0;
+}
 int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const int32_t* start, uint8_t* status,
                   int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back,
                   cudaStream_t s, int mode, bool host_rays = false, const int64_t* oidx = nullptr) {
@@ -1802,21 +1814,57 @@ int cast_dispatch(tb_mesh* m, int64_t n, const float* o, const float* d, const i
     int64_t* widx = oidx ? reinterpret_cast<int64_t*>(scratch + hist_b) : nullptr;  // null: results to perm[r]
     int32_t* perm = reinterpret_cast<int32_t*>(scratch + hist_b + widx_b);
     uint8_t* bins = reinterpret_cast<uint8_t*>(scratch + hist_b + widx_b + (size_t)n * 4);
-    if (S) {
-      if (cudaError_t me = cudaMemsetAsync(hist, 0, hist_n * 4, s)) {  // the ragged segment's missing tiles count 0
-        cudaFreeAsync(scratch, s);
-        return set_error(TB_E_CUDA, "binning scratch memset: %s", cudaGetErrorString(me));
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    const int seg_mid = (n_segs + 1) / 2;
+    if (S && !oidx && n_segs >= 2 && bin_split() && order_side(m->device, &side, &fork, &join) == TB_OK) {
+      // Two chunks of whole segments (the sort is segment-local): chunk 0 is
+      // binned on the caller's stream and walks there; chunk 1 is binned on the
+      // high-priority side stream beside chunk 0's walk and then walks there
+      // too, so only half of the binning passes precede any walk.
+      const int ta = std::min(seg_mid * S, n_tiles);
+      const int64_t ra = std::min<int64_t>((int64_t)ta * kBinTile, n);
+      cudaError_t ce = cudaMemsetAsync(hist, 0, hist_n * 4, s);
+      if (ce == cudaSuccess) {
+        bin_count_kernel<<<ta, kBinThreads, 0, s>>>(d, n, hist, n_tiles, S, bins, 0);
+        bin_seg_scan_kernel<<<seg_mid, 1024, 0, s>>>(hist, S, 0);
+        bin_scatter_kernel<<<ta, kBinThreads, 0, s>>>(bins, n, hist, totals, n_tiles, S, perm, 0);
+        ce = cudaEventRecord(fork, s);
       }
-      bin_count_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles, S, bins);
-      bin_seg_scan_kernel<<<n_segs, 1024, 0, s>>>(hist, S);
+      if (ce == cudaSuccess) ce = cudaStreamWaitEvent(side, fork, 0);
+      if (ce != cudaSuccess) {
+        cudaFreeAsync(scratch, s);
+        return set_error(TB_E_CUDA, "binned schedule fork: %s", cudaGetErrorString(ce));
+      }
+      bin_count_kernel<<<n_tiles - ta, kBinThreads, 0, side>>>(d, n, hist, n_tiles, S, bins, ta);
+      bin_seg_scan_kernel<<<n_segs - seg_mid, 1024, 0, side>>>(hist, S, seg_mid);
+      bin_scatter_kernel<<<n_tiles - ta, kBinThreads, 0, side>>>(bins, n, hist, totals, n_tiles, S, perm, ta);
+      e = launch_layout<CastBinnedL>(m->layout, grid_for(ra, kCastBlock), s, m->safe, (const int32_t*)perm,
+                                     (const int64_t*)nullptr, v, ra, o, d, start, status, cf, tet, visited, triangle,
+                                     t, tet_back);
+      if (!e)
+        e = launch_layout<CastBinnedL>(m->layout, grid_for(n - ra, kCastBlock), side, m->safe,
+                                       (const int32_t*)(perm + ra), (const int64_t*)nullptr, v, n - ra, o, d, start,
+                                       status, cf, tet, visited, triangle, t, tet_back);
+      const bool ok = cudaEventRecord(join, side) == cudaSuccess && cudaStreamWaitEvent(s, join, 0) == cudaSuccess;
+      if (!ok && !e) e = set_error(TB_E_CUDA, "binned schedule join: %s", cudaGetErrorString(cudaGetLastError()));
     } else {
-      bin_count_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles, 0, bins);
-      bin_scan_kernel<<<kBins, 1024, 0, s>>>(hist, n_tiles, totals);
+      if (S) {
+        if (cudaError_t me = cudaMemsetAsync(hist, 0, hist_n * 4, s)) {  // the ragged segment's missing tiles count 0
+          cudaFreeAsync(scratch, s);
+          return set_error(TB_E_CUDA, "binning scratch memset: %s", cudaGetErrorString(me));
+        }
+        bin_count_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles, S, bins);
+        bin_seg_scan_kernel<<<n_segs, 1024, 0, s>>>(hist, S);
+      } else {
+        bin_count_kernel<<<n_tiles, kBinThreads, 0, s>>>(d, n, hist, n_tiles, 0, bins);
+        bin_scan_kernel<<<kBins, 1024, 0, s>>>(hist, n_tiles, totals);
+      }
+      bin_scatter_kernel<<<n_tiles, kBinThreads, 0, s>>>(bins, n, hist, totals, n_tiles, S, perm);
+      if (oidx) compose_index_kernel<<<grid_for(n, 256), 256, 0, s>>>(perm, oidx, n, widx);
+      e = launch_layout<CastBinnedL>(m->layout, grid_for(n, kCastBlock), s, m->safe, perm, widx, v, n, o, d, start,
+                                     status, cf, tet, visited, triangle, t, tet_back);
     }
-    bin_scatter_kernel<<<n_tiles, kBinThreads, 0, s>>>(bins, n, hist, totals, n_tiles, S, perm);
-    if (oidx) compose_index_kernel<<<grid_for(n, 256), 256, 0, s>>>(perm, oidx, n, widx);
-    e = launch_layout<CastBinnedL>(m->layout, grid_for(n, kCastBlock), s, m->safe, perm, widx, v, n, o, d, start,
-                                   status, cf, tet, visited, triangle, t, tet_back);
     cudaFreeAsync(scratch, s);
   } else if (mode == 7 && !host_rays && oidx == nullptr) {
     // sampled longest-first: a capped walk of one ray per block orders the
@@ -2401,6 +2449,13 @@ int tb_cast_rays_sched(tb_mesh* m, int64_t n, const float* o, const float* d, co
 int tb_cast_block_size(void) { return kCastBlock; }
 
 int tb_auto_schedule(int device, int64_t n) { return n < 0 ? -1 : auto_schedule(device, n); }
+
+int tb_binned_pieces(int64_t n) {
+  if (n < 0) return -1;
+  const int n_tiles = (int)((n + kBinTile - 1) / kBinTile);
+  const int S = bin_tile() / kBinTile;
+  return (S && (n_tiles + S - 1) / S >= 2 && bin_split()) ? 2 : 1;
+}
 
 int64_t tb_sampled_head_blocks(int device, int64_t n) {
   return n < 0 ? -1 : head_blocks(device, (n + kCastBlock - 1) / kCastBlock);
