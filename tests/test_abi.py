@@ -97,6 +97,18 @@ def test_schedule_setter_roundtrip_and_validation():
         _lib.set_schedule(mode0, k0)
 
 
+def test_binned_pieces_rule():
+    """tb_binned_pieces: the binned schedule splits into two pieces of whole
+    262144-ray sorting segments only when the batch spans two or more of
+    them; a negative count is rejected (host logic, no GPU)."""
+    from paper_2103_02309_b200._lib import lib
+
+    seg = 262144
+    assert lib.tb_binned_pieces(-1) == -1
+    for n, want in ((0, 1), (1, 1), (seg, 1), (seg + 1, 2), (2 * seg, 2), (16_777_216, 2)):
+        assert lib.tb_binned_pieces(n) == want, n
+
+
 def test_cast_rays_sched_validates_arguments():
     from paper_2103_02309_b200._lib import lib
 
