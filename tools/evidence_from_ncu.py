@@ -29,8 +29,8 @@ def raw(path: str) -> dict:
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True,
                          check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h, u, v = rows[0], rows[1], rows[2]
-    return {k: (u[i], v[i]) for i, k in enumerate(h)}
+    h, u = rows[0], rows[1]
+    return [{k: (u[i], v[i]) for i, k in enumerate(h)} for v in rows[2:]]
 
 
 def num(m: dict, key: str) -> float:
@@ -45,7 +45,8 @@ def main(argv):
     pipes = json.load(open(pp)) if os.path.exists(pp) else {}
     traffic = json.load(open(tp)) if os.path.exists(tp) else {}
     for key, path in pairs:
-        m = raw(path)
+        ms = raw(path)  # one row per captured launch: a walk in pieces sums its launches
+        m = ms[0]
         name = m["Kernel Name"][1] if "Kernel Name" in m else "?"
         pipes[key] = {
             "kernel": name.split("(")[0].replace("void <unnamed>::", ""),
@@ -57,9 +58,12 @@ def main(argv):
             "l1_hit_pct": round(num(m, "l1tex__t_sector_hit_rate.pct"), 1),
             "l2_hit_pct": round(num(m, "lts__t_sector_hit_rate.pct"), 1),
             "issue_active_pct": round(num(m, "smsp__issue_active.avg.pct_of_peak_sustained_active"), 1),
-            "duration_us": round(num(m, "gpu__time_duration.sum"), 1),
+            "duration_us": round(sum(num(x, "gpu__time_duration.sum") for x in ms), 1),
         }
-        traffic[key] = int(round(num(m, "dram__bytes_read.sum") + num(m, "dram__bytes_write.sum"), -5))
+        if len(ms) > 1:
+            pipes[key]["launches"] = len(ms)
+        traffic[key] = int(round(sum(num(x, "dram__bytes_read.sum") + num(x, "dram__bytes_write.sum")
+                                     for x in ms), -5))
         print(key, pipes[key], traffic[key])
     pipes["_source"] = (f"ncu --set full --clock-control none of the timed walk per config (tools/gpu_r02_final.sh, "
                         f"gpurun_out/{tag}/prof_cfg*.ncu-rep), read by tools/evidence_from_ncu.py; % of peak "
