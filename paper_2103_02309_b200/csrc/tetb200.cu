@@ -331,16 +331,40 @@ struct RayVal {
   }
 };
 
+// Ray I/O cache hints: the walk's result stores, and the ray loads of walks
+// that read their rays in place, are issued evict-first (st/ld.global.cs), so
+// the streamed ray and hit arrays give way to the mesh in L2.  Same-process
+// A/B (profiles/r02_ab_stream_hints.jsonl, bit-identical): config 2 +1.0 %,
+// binned config 4 +0.3 %, frame secondaries +0.6 %, configs 3 / 5 within
+// 0.2 %.  Gathered (binned) walks keep cached loads: evict-first ray loads
+// through the permutation cost config 4 0.5 %.  TB_STREAM_HINTS=0 turns the
+// hints off (1: stores only, 2: every ray load too, 3: the default).
+#ifndef TB_STREAM_HINTS
+#define TB_STREAM_HINTS 3
+#endif
+#if TB_STREAM_HINTS >= 3
+#define TB_LDR(p) (kGather ? __ldg(p) : __ldcs(p))
+#elif TB_STREAM_HINTS >= 2
+#define TB_LDR(p) __ldcs(p)
+#else
+#define TB_LDR(p) __ldg(p)
+#endif
+#if TB_STREAM_HINTS >= 1
+#define TB_STR(p, v) __stcs((p), (v))
+#else
+#define TB_STR(p, v) (*(p) = (v))
+#endif
+
 template <class Ray>
 __device__ __forceinline__ void write_result_ray(const MeshView& m, int64_t r, uint8_t st, uint32_t ref,
                                                  uint32_t cur, int vis, const Ray& ray, uint8_t* status,
                                                  int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle,
                                                  double* t, int32_t* tet_back) {
-  if (status != nullptr) status[r] = st;
+  if (status != nullptr) TB_STR(reinterpret_cast<signed char*>(status) + r, (signed char)st);
   const int32_t cfi = (st == kHit) ? (int32_t)(ref & kPayload) : -1;
-  cf[r] = cfi;
-  tet[r] = (int32_t)cur;
-  visited[r] = vis;
+  TB_STR(cf + r, cfi);
+  TB_STR(tet + r, (int32_t)cur);
+  TB_STR(visited + r, vis);
   if (triangle != nullptr || t != nullptr || tet_back != nullptr) {
     int32_t tri = -1, back = -1;
     double tt = INFINITY;
@@ -353,9 +377,9 @@ __device__ __forceinline__ void write_result_ray(const MeshView& m, int64_t r, u
       const int2 ct = __ldg(&m.cf_tets[cfi]);
       back = (ct.x == (int32_t)cur) ? ct.y : ct.x;
     }
-    if (triangle != nullptr) triangle[r] = tri;
-    if (t != nullptr) t[r] = tt;
-    if (tet_back != nullptr) tet_back[r] = back;
+    if (triangle != nullptr) TB_STR(triangle + r, tri);
+    if (t != nullptr) TB_STR(t + r, tt);
+    if (tet_back != nullptr) TB_STR(tet_back + r, back);
   }
 }
 
@@ -550,9 +574,9 @@ __global__ void __launch_bounds__(kCastBlock, (cast_min_blocks<L, kGather>())) c
   } else {
     if (r >= n) return;
     const int64_t q = kGather ? (int64_t)__ldg(ridx + r) : r;
-    cur = (uint32_t)__ldg(start + q);
-    o0 = __ldg(o + 3 * q); o1 = __ldg(o + 3 * q + 1); o2 = __ldg(o + 3 * q + 2);
-    d0 = __ldg(d + 3 * q); d1 = __ldg(d + 3 * q + 1); d2 = __ldg(d + 3 * q + 2);
+    cur = (uint32_t)TB_LDR(start + q);
+    o0 = TB_LDR(o + 3 * q); o1 = TB_LDR(o + 3 * q + 1); o2 = TB_LDR(o + 3 * q + 2);
+    d0 = TB_LDR(d + 3 * q); d1 = TB_LDR(d + 3 * q + 1); d2 = TB_LDR(d + 3 * q + 2);
   }
   uint32_t ref;
   int vis;
