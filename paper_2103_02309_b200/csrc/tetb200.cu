@@ -334,9 +334,9 @@ struct RayVal {
 // Ray I/O cache hints: the walk's result stores, and the ray loads of walks
 // that read their rays in place, are issued evict-first (st/ld.global.cs), so
 // the streamed ray and hit arrays give way to the mesh in L2.  Same-process
-// A/B (profiles/r02_ab_stream_hints.jsonl, bit-identical): config 2 +1.0 %,
-// binned config 4 +0.3 %, frame secondaries +0.6 %, configs 3 / 5 within
-// 0.2 %.  Gathered (binned) walks keep cached loads: evict-first ray loads
+// A/B (profiles/r02_ab_stream_hints.jsonl, bit-identical): config 2 +1.0 %
+// in the A/B harness (neutral through bench.py), binned config 4 +0.3 %,
+// frame secondaries +0.6 %, configs 3 / 5 within 0.2 %.  Gathered (binned) walks keep cached loads: evict-first ray loads
 // through the permutation cost config 4 0.5 %.  TB_STREAM_HINTS=0 turns the
 // hints off (1: stores only, 2: every ray load too, 3: the default).
 #ifndef TB_STREAM_HINTS
