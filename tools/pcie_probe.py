@@ -120,6 +120,35 @@ def main():
 
     rec("ce_both", timed(both, args.reps, s), nin + nout)
 
+    # mixed: one direction by the SMs (zero copy), the other by a copy engine
+    # on a second stream, concurrently
+    g = sms * 8
+
+    def zc_read_ce_d2h():
+        ev = torch.cuda.Event()
+        ev.record(s)
+        s2.wait_event(ev)
+        lib.pcie_move(hin.data_ptr(), nin, None, 0, sink.data_ptr(), g, 256, s.cuda_stream)
+        with torch.cuda.stream(s2):
+            hout.copy_(dout, non_blocking=True)
+        ev2 = torch.cuda.Event()
+        ev2.record(s2)
+        s.wait_event(ev2)
+
+    def ce_h2d_zc_write():
+        ev = torch.cuda.Event()
+        ev.record(s)
+        s2.wait_event(ev)
+        lib.pcie_move(None, 0, hout.data_ptr(), nout, sink.data_ptr(), g, 256, s.cuda_stream)
+        with torch.cuda.stream(s2):
+            din.copy_(hin, non_blocking=True)
+        ev2 = torch.cuda.Event()
+        ev2.record(s2)
+        s.wait_event(ev2)
+
+    rec("zc_read_ce_d2h", timed(zc_read_ce_d2h, args.reps, s), nin + nout, grid=g, block=256)
+    rec("ce_h2d_zc_write", timed(ce_h2d_zc_write, args.reps, s), nin + nout, grid=g, block=256)
+
 
 if __name__ == "__main__":
     main()
