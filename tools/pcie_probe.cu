@@ -218,3 +218,66 @@ extern "C" int pcie_bulk_write(const void* in, int64_t in_bytes, void* out, int6
                                                           (uint4*)sink, with_reads);
   return (int)cudaGetLastError();
 }
+
+// Copy-engine H2D streamed into one running kernel: the copy stream moves the
+// input in chunks into HBM staging, each chunk followed by a 4-byte flag copy
+// (the copy engine finishes a copy before the next one in its stream starts,
+// so the flag lands after its data); the kernel's blocks -- laid out like the
+// trace's 128-ray blocks -- wait (acquire) for their chunk's flag, read it
+// from L2 (.cg) and write their output bytes zero-copy to pinned host memory.
+// One launch: no per-chunk kernel tails.  The spin gives up after ~2 s.
+__global__ void flag_move(const uint4* __restrict__ stage, int64_t in_per_block, uint4* __restrict__ out,
+                          int64_t out_per_block, int64_t chunk_u4, const uint32_t* flag, uint4* __restrict__ sink) {
+  const int64_t b = blockIdx.x;
+  const int64_t last = (b + 1) * in_per_block - 1;
+  const uint32_t need = (uint32_t)(last / chunk_u4) + 1;
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    const long long t0 = clock64();
+    uint32_t f;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(flag) : "memory");
+    } while (f < need && clock64() - t0 < 4000000000LL);
+    ok = f >= need;
+  }
+  __syncthreads();
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  if (ok) {
+    for (int64_t i = threadIdx.x; i < in_per_block; i += blockDim.x) {
+      const uint4 v = __ldcg(stage + b * in_per_block + i);
+      acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+    }
+  } else if (threadIdx.x == 0) {
+    sink[1] = make_uint4(0xDEADu, (uint32_t)b, need, 0u);
+  }
+  for (int64_t i = threadIdx.x; i < out_per_block; i += blockDim.x)
+    out[b * out_per_block + i] = make_uint4((uint32_t)i, acc.x, 0u, 0u);
+  if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x9E3779B9u) *sink = acc;
+}
+
+// in_bytes / out_bytes are split over n_blocks blocks (multiples of 16 B per
+// block); chunk_blocks blocks' input per chunk, each chunk as `copies` copies.
+extern "C" int pcie_flagged(const void* host_in, void* stage, int64_t in_bytes, void* host_out, int64_t out_bytes,
+                            uint32_t* flag, const uint32_t* host_vals, int64_t n_blocks, int64_t chunk_blocks,
+                            int copies, void* sink, void* ks, void* cs, void* ev_fork, void* ev_join) {
+  cudaStream_t k = (cudaStream_t)ks, c = (cudaStream_t)cs;
+  const int64_t ipb = in_bytes / 16 / n_blocks, opb = out_bytes / 16 / n_blocks;
+  cudaMemsetAsync(flag, 0, 4, k);
+  cudaEventRecord((cudaEvent_t)ev_fork, k);
+  cudaStreamWaitEvent(c, (cudaEvent_t)ev_fork, 0);
+  flag_move<<<(unsigned)n_blocks, 128, 0, k>>>((const uint4*)stage, ipb, (uint4*)host_out, opb, chunk_blocks * ipb,
+                                               flag, (uint4*)sink);
+  const int64_t chunk_bytes = chunk_blocks * ipb * 16, total = n_blocks * ipb * 16;
+  for (int64_t off = 0, ci = 0; off < total; off += chunk_bytes, ++ci) {
+    const int64_t len = (total - off < chunk_bytes) ? total - off : chunk_bytes;
+    const int64_t part = (len / copies + 15) / 16 * 16;
+    for (int64_t p = 0; p < len; p += part) {
+      const int64_t l = (len - p < part) ? len - p : part;
+      cudaMemcpyAsync((char*)stage + off + p, (const char*)host_in + off + p, l, cudaMemcpyHostToDevice, c);
+    }
+    cudaMemcpyAsync(flag, host_vals + ci, 4, cudaMemcpyHostToDevice, c);
+  }
+  cudaEventRecord((cudaEvent_t)ev_join, c);
+  cudaStreamWaitEvent(k, (cudaEvent_t)ev_join, 0);
+  return (int)cudaGetLastError();
+}

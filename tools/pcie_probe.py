@@ -32,6 +32,9 @@ def build() -> ctypes.CDLL:
     lib = ctypes.CDLL(so)
     lib.pcie_move.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                               ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+    lib.pcie_flagged.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     for f in (lib.pcie_bulk, lib.pcie_bulk_write):
         f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                       ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
@@ -147,6 +150,31 @@ def main():
         s.wait_event(ev2)
 
     rec("zc_read_ce_d2h", timed(zc_read_ce_d2h, args.reps, s), nin + nout, grid=g, block=256)
+
+    # copy-engine H2D streamed into one running kernel by per-chunk flags
+    nb = 2_073_600 // 128
+    # 28 B in / 29 B out per ray; each block's share a whole number of 16 B words
+    in_b, out_b = nb * (28 * 128 // 16) * 16, nb * (29 * 128 // 16) * 16
+    hin2 = torch.empty(in_b, dtype=torch.uint8).pin_memory()
+    hout2 = torch.empty(out_b, dtype=torch.uint8).pin_memory()
+    stage = torch.empty(in_b, dtype=torch.uint8, device=dev)
+    flag = torch.zeros(4, dtype=torch.int32, device=dev)
+    vals = torch.arange(1, 4097, dtype=torch.int32).pin_memory()
+    sinkf = torch.zeros(8, dtype=torch.int32, device=dev)
+    evf, evj = torch.cuda.Event(), torch.cuda.Event()
+    evf.record(s)
+    evj.record(s)
+    assert (in_b // 16) % nb == 0 and (out_b // 16) % nb == 0
+    for chunk_blocks in (256, 512, 1024, 2048, 4096):
+        for copies in (1, 3):
+            fn = lambda: lib.pcie_flagged(hin2.data_ptr(), stage.data_ptr(), in_b, hout2.data_ptr(), out_b,
+                                          flag.data_ptr(), vals.data_ptr(), nb, chunk_blocks, copies,
+                                          sinkf.data_ptr(), s.cuda_stream, s2.cuda_stream, evf.cuda_event,
+                                          evj.cuda_event)
+            ms = timed(fn, args.reps, s)
+            torch.cuda.synchronize()
+            rec("ce_h2d_flagged_kernel_zc_write", ms, in_b + out_b, chunk_rays=chunk_blocks * 128, copies=copies,
+                timeouts=int(sinkf[4].item()))
     rec("ce_h2d_zc_write", timed(ce_h2d_zc_write, args.reps, s), nin + nout, grid=g, block=256)
 
 
