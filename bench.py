@@ -456,6 +456,33 @@ def issue_roof(layout: str, schedule: str, walk_steps: float, kern_s: float, clk
                     "the gap is init/epilogue, SIMT divergence, latency stalls and the tail"}
 
 
+def l1_pipe_roof(key: str, kern_s: float, clk_mhz, sms: int):
+    """The L1 data pipe as a roof (the incoherent walk's binding unit, ncu
+    r02): the walk's LSU wavefronts per launch, counted once by ncu for this
+    workload (profiles/pipe_util.json, tools/evidence_from_ncu.py), over the
+    live kernel time, against SMs x wavefronts per SM cycle x the live SM
+    clock.  None when no capture counted them."""
+    p = pipes_of(key) or {}
+    wf, per_cycle = p.get("l1tex_lsu_wavefronts_per_launch"), p.get("l1tex_lsu_wavefronts_peak_per_sm_cycle")
+    if not (wf and per_cycle and clk_mhz):
+        return None
+    peak = sms * per_cycle * clk_mhz * 1e6
+    return {"bound": "l1_data_pipe", "achieved": wf / kern_s / 1e9, "peak": peak / 1e9, "unit": "G wavefronts/s",
+            "frac": wf / kern_s / peak, "wavefronts_per_launch": wf, "sms": sms, "sm_mhz": clk_mhz,
+            "note": "L1TEX data-pipe (LSU) wavefronts of the walk per launch from one ncu capture of this workload, "
+                    "over the live kernel time; peak = SMs x wavefronts per SM cycle (ncu) x live SM clock"}
+
+
+def binding_roof(alu, l1):
+    """The roof that binds: the larger utilisation of the ALU-pipe issue roof
+    and the L1 data-pipe roof; the other rides along."""
+    if l1 is None:
+        return alu
+    if alu is None or l1["frac"] > alu["frac"]:
+        return dict(l1, roofline_alu_pipe=alu)
+    return dict(alu, roofline_l1_data_pipe=l1)
+
+
 def pipes_of(key: str):
     """ncu pipe / L1 utilisation of the walk (profiles/pipe_util.json)."""
     pp = os.path.join(ROOT, "profiles", "pipe_util.json")
@@ -862,6 +889,8 @@ def run_ours(args, cfg):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     walk_steps = (vis_sum - total_rays) / world  # one rank's launch
     roof = issue_roof(cfg["layout"], schedule, walk_steps, kern_s, clk.get("sm_mhz"), sms) if not sctp else None
+    if not sctp:
+        roof = binding_roof(roof, l1_pipe_roof(f"cfg{args.config}/{cfg['layout']}", kern_s, clk.get("sm_mhz"), sms))
     traffic = traffic_of(f"cfg{args.config}/{cfg['layout']}")
     kname = (f"sctp_kernel<{cfg['layout'][3:]}>" if sctp else
              f"{'cast_compact_kernel' if schedule in ('compact', 'compact512') else 'cast_kernel'}"
@@ -1034,7 +1063,8 @@ def config4_secondaries(args, mesh20, stream, flush, threads, clocks):
     kb = float(ms["binned"].mean())
     clk = clocks.summary(clocks.t_ramp, clocks.t_end).get("sm_mhz")
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    roof = issue_roof("tet16", "binned", float(v2.astype(np.int64).sum() - ns), kb / 1e3, clk, sms)
+    roof = binding_roof(issue_roof("tet16", "binned", float(v2.astype(np.int64).sum() - ns), kb / 1e3, clk, sms),
+                        l1_pipe_roof("cfg4/tet16", kb / 1e3, clk, sms))
     out = {"value": ns / kb / 1e3, "unit": "Mrays/s", "rays": ns, "kernel_ms": kb, "schedule": "binned",
            "one_ray_per_lane": {"value": ns / float(ms["lane"].mean()) / 1e3, "kernel_ms": float(ms["lane"].mean())},
            "tets_visited_per_ray": {"mean": float(v2.mean()), "max": int(v2.max())},

@@ -75,6 +75,25 @@ def test_roofline_is_the_binding_pipe_of_the_committed_sass():
     assert bench.issue_roof("tet20", "lane", 1e9, 1e-3, None, 148) is None  # no clock sample: no roof
 
 
+def test_incoherent_walk_reports_the_l1_data_pipe_when_it_binds():
+    """Config 4's binned walk: the L1 data-pipe roof (ncu wavefronts per
+    launch over the live time, peak = SMs x 1 wavefront per SM cycle x clock)
+    binds over the ALU-pipe roof, which rides along; walks without a wavefront
+    count keep the ALU-pipe roof."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    wf = bench.pipes_of("cfg4/tet16")["l1tex_lsu_wavefronts_per_launch"]
+    l1 = bench.l1_pipe_roof("cfg4/tet16", kern_s=4.62e-3, clk_mhz=1965.0, sms=148)
+    assert l1["frac"] == pytest.approx(wf / 4.62e-3 / (148 * 1.0 * 1965e6), rel=1e-3)
+    alu = bench.issue_roof("tet16", "binned", walk_steps=16_777_216 * 64.0, kern_s=4.62e-3, clk_mhz=1965.0, sms=148)
+    r = bench.binding_roof(alu, l1)
+    assert r["bound"] == "l1_data_pipe" and r["roofline_alu_pipe"]["bound"] == "alu_pipe"
+    assert 0.5 < r["frac"] < 1.0 and r["frac"] > alu["frac"]
+    assert bench.l1_pipe_roof("cfg2/tet20", 1.7e-4, 1965.0, 148) is None
+    assert bench.binding_roof(alu, None) is alu
+
+
 def test_profiles_carry_traffic_and_pipes_for_every_bench_config():
     sys.path.insert(0, str(ROOT))
     import bench

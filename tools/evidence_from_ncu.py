@@ -62,6 +62,17 @@ def main(argv):
         }
         if len(ms) > 1:
             pipes[key]["launches"] = len(ms)
+        wf_key = "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg"
+        if all(wf_key in x for x in ms):
+            sms = num(m, "device__attribute_multiprocessor_count") if "device__attribute_multiprocessor_count" in m \
+                else 148
+            # L1 data-pipe wavefronts of the whole walk (launches summed) and
+            # the pipe's peak per SM cycle (per-SM average over its utilisation
+            # over the SM's elapsed cycles: 1.0 on sm_100)
+            pipes[key]["l1tex_lsu_wavefronts_per_launch"] = int(sum(num(x, wf_key) for x in ms) * sms)
+            pipes[key]["l1tex_lsu_wavefronts_peak_per_sm_cycle"] = round(
+                num(m, wf_key) / (num(m, "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed") / 100)
+                / num(m, "sm__cycles_elapsed.avg"), 3)
         traffic[key] = int(round(sum(num(x, "dram__bytes_read.sum") + num(x, "dram__bytes_write.sum")
                                      for x in ms), -5))
         print(key, pipes[key], traffic[key])
