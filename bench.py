@@ -1102,8 +1102,8 @@ def render_e2e(args, cfg, dm, stream, sctp):
     r_s = time.perf_counter() - t0
     return {"value": W * H * args.steps / r_s / 1e6, "unit": "Mrays/s", "h2d_bytes_per_step": 14 * 8,
             "d2h_bytes_per_step": int(W * H * 29), "ms_per_step": r_s / args.steps * 1e3,
-            "path": "trace_camera: rays generated in HBM, trace writes all 7 hit arrays straight to pinned host "
-                    "memory (camera tet located once)"}
+            "path": "trace_camera (tb_trace_camera): one launch forms each pixel's ray in registers, walks it and "
+                    "writes all 7 hit arrays straight to pinned host memory (camera tet located once)"}
 
 
 def small_batch(args, mesh, o, d, st, threads):

@@ -276,6 +276,18 @@ int tb_locate_points_host(tb_mesh* mesh, int64_t n, const double* q, const int32
 int tb_camera_rays(int64_t width, int64_t height, const double* frame, const int64_t* pixels, int64_t n,
                    float* o, float* d, void* stream);
 
+/* A frame's primary pass in one launch: render.camera_rays (render.py:169-185)
+ * fused with the cast from the camera tet (batch.cast_rays, batch.py:39-71)
+ * -- each lane forms its pixel's ray exactly as tb_camera_rays does and
+ * walks it; no rays are stored.  frame: 14 float64 HOST values (as for
+ * tb_camera_rays, passed by value to the kernel); cam_tet: the located
+ * camera tet (render.py:478-482); outputs (width * height,) as for
+ * tb_cast_rays, device or mapped pinned host memory.  Results are
+ * bit-identical to tb_camera_rays + tb_cast_rays. */
+int tb_trace_camera(tb_mesh* mesh, int64_t width, int64_t height, const double* frame, int32_t cam_tet,
+                    uint8_t* status, int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t,
+                    int32_t* tet_back, void* stream);
+
 /* Hull clipping for ray origins outside the mesh.
  * Replaces: the brute-force boundary-face search of traversal.cast_ray_auto
  *   (traversal.py:545-589, hull_faces traversal.py:530-542).

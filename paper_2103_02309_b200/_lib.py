@@ -65,6 +65,7 @@ _SIGS = {
     "tb_locate_points": (c_int, [c_void_p, c_int64, P, P, P, P, c_void_p]),
     "tb_hull_clip": (c_int, [c_void_p, c_int64, P, P, P, c_int64, P, P, P, c_void_p]),
     "tb_camera_rays": (c_int, [c_int64, c_int64, P, P, c_int64, P, P, c_void_p]),
+    "tb_trace_camera": (c_int, [c_void_p, c_int64, c_int64, P, c_int, P, P, P, P, P, P, P, c_void_p]),
     "tb_locate_points_host": (c_int, [c_void_p, c_int64, P, P, P, P]),
     "tb_shadow_rays": (c_int, [c_void_p, c_int64, P, P, c_int, P, P, c_int, c_double, P, P, c_void_p]),
     "tb_shadow_rays_host": (c_int, [c_void_p, c_int64, P, P, c_int, P, P, c_int, c_double, P, P]),

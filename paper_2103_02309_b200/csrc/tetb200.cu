@@ -1042,6 +1042,55 @@ __global__ void camera_rays_kernel(int64_t width, int64_t height, const double* 
   }
 }
 
+// A frame's primary pass in one launch (tb_trace_camera): each lane forms
+// its pixel's ray with camera_rays_kernel's fp64 arithmetic (so the ray is
+// bit-identical to tb_camera_rays' output), walks it from the camera tet and
+// writes the seven hit arrays -- no rays in HBM, no second launch.  The frame
+// comes by value (112 B of kernel parameters: nothing to upload).  Outputs
+// may be mapped pinned host memory (render-style: the hits cross PCIe as the
+// warps' stores); a full block's 1-byte statuses are staged in shared memory
+// and stored as one 128 B write, as cast_kernel does for host rays.
+struct CamFrame {
+  double f[14];
+};
+template <int L, bool kClamp>
+__global__ void __launch_bounds__(kCastBlock, (cast_min_blocks<L, false>()))
+    camera_cast_kernel(MeshView m, int64_t width, int64_t height, CamFrame fr, uint32_t cam_tet,
+                       uint8_t* __restrict__ status, int32_t* __restrict__ cf, int32_t* __restrict__ tet,
+                       int32_t* __restrict__ visited, int32_t* __restrict__ triangle, double* __restrict__ t,
+                       int32_t* __restrict__ tet_back) {
+  const int64_t n = width * height;
+  const int64_t r = (int64_t)blockIdx.x * kCastBlock + threadIdx.x;
+  const bool full = (int64_t)(blockIdx.x + 1) * kCastBlock <= n && (reinterpret_cast<uintptr_t>(status) & 3u) == 0;
+  if (!full && r >= n) return;
+  const double xs = (double)(r % width), ys = (double)(r / width);
+  const double W = (double)width, H = (double)height;
+  const double sx = __dmul_rn(__dsub_rn(__dmul_rn(__ddiv_rn(__dadd_rn(xs, 0.5), W), 2.0), 1.0), fr.f[12]);
+  const double sy = __dmul_rn(__dsub_rn(1.0, __dmul_rn(__ddiv_rn(__dadd_rn(ys, 0.5), H), 2.0)), fr.f[13]);
+  float dv[3], ov[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    dv[k] = __double2float_rn(__dadd_rn(__dadd_rn(fr.f[k], __dmul_rn(sx, fr.f[3 + k])), __dmul_rn(sy, fr.f[6 + k])));
+    ov[k] = __double2float_rn(fr.f[9 + k]);
+  }
+  uint32_t cur = cam_tet, ref;
+  int vis;
+  uint8_t st;
+  walk_ray<L, kClamp>(m, ov[0], ov[1], ov[2], dv[0], dv[1], dv[2], cur, ref, vis, st);
+  if (full) {  // no lane of a full block returned early: the barrier is safe
+    __shared__ uint32_t s_status[kCastBlock / 4];
+    reinterpret_cast<uint8_t*>(s_status)[threadIdx.x] = st;
+    write_result(m, r, st, ref, cur, vis, ov[0], ov[1], ov[2], dv[0], dv[1], dv[2], nullptr, cf, tet, visited,
+                 triangle, t, tet_back);
+    __syncthreads();
+    if (threadIdx.x < kCastBlock / 4)
+      reinterpret_cast<uint32_t*>(status + (int64_t)blockIdx.x * kCastBlock)[threadIdx.x] = s_status[threadIdx.x];
+    return;
+  }
+  write_result(m, r, st, ref, cur, vis, ov[0], ov[1], ov[2], dv[0], dv[1], dv[2], status, cf, tet, visited, triangle,
+               t, tet_back);
+}
+
 // Hull clipping for origins outside the mesh (traversal.cast_ray_auto,
 // traversal.py:545-589): the nearest boundary face hit by the ray, tested
 // brute force in fp64 (Moller-Trumbore with u, v, t bounds, det == 0
@@ -1475,6 +1524,16 @@ struct ShadowL {
       shadow_kernel<L, false><<<g, kBlock, 0, s>>>(a...);
     else
       shadow_kernel<L, true><<<g, kBlock, 0, s>>>(a...);
+  }
+};
+template <int L>
+struct CameraCastL {
+  template <typename... A>
+  static void launch(unsigned g, cudaStream_t s, bool safe, A... a) {
+    if (safe && L != 80)
+      camera_cast_kernel<L, false><<<g, kCastBlock, 0, s>>>(a...);
+    else
+      camera_cast_kernel<L, true><<<g, kCastBlock, 0, s>>>(a...);
   }
 };
 template <int L>
@@ -2569,6 +2628,25 @@ int tb_camera_rays(int64_t width, int64_t height, const double* frame, const int
   if (n == 0) return TB_OK;
   if (!frame || !o || !d) return set_error(TB_E_ARG, "NULL buffer");
   camera_rays_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(width, height, frame, pixels, n, o, d);
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_trace_camera(tb_mesh* m, int64_t width, int64_t height, const double* frame, int32_t cam_tet, uint8_t* status,
+                    int32_t* cf, int32_t* tet, int32_t* visited, int32_t* triangle, double* t, int32_t* tet_back,
+                    void* stream) {
+  if (int e = check_mesh(m)) return e;
+  if (width <= 0 || height <= 0) return set_error(TB_E_ARG, "bad camera size");
+  if (!frame || !status || !cf || !tet || !visited) return set_error(TB_E_ARG, "NULL buffer");
+  if (cam_tet < 0 || cam_tet >= m->n_tets) return set_error(TB_E_ARG, "camera tet %d out of range", cam_tet);
+  CamFrame fr;
+  for (int k = 0; k < 14; ++k) fr.f[k] = frame[k];
+  DeviceGuard g(m->device);
+  const int64_t n = width * height;
+  if (int e = launch_layout<CameraCastL>(m->layout, grid_for(n, kCastBlock), (cudaStream_t)stream, m->safe, m->view(),
+                                         width, height, fr, (uint32_t)cam_tet, status, cf, tet, visited, triangle, t,
+                                         tet_back))
+    return e;
   TB_CUDA(cudaGetLastError());
   return TB_OK;
 }

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from ._lib import SCHEDULES, addr, check, lib
@@ -150,7 +151,7 @@ def camera_rays_device(camera: dict, width: int, height: int, device, pixels: to
 
 def trace_camera(mesh, camera: dict, width: int, height: int, *, device=None, out: TraceResult | None = None,
                  stream=None, sctp: bool = False, layout: str | None = None, cam_tet: int | None = None,
-                 block_order: torch.Tensor | None = None):
+                 block_order: torch.Tensor | None = None, fused: bool = True):
     """Render-style primary pass entirely on the device: locate the camera
     (render.py:478-482; skipped when ``cam_tet`` is given), generate the
     frame's rays in HBM, trace.  ``out`` may hold pinned host tensors: the
@@ -158,6 +159,9 @@ def trace_camera(mesh, camera: dict, width: int, height: int, *, device=None, ou
     pinned memory under UVA), overlapping the copy with the walk.
     ``block_order``: see ``trace`` (for an animation, ``longest_first`` of
     the previous frame's ``visited``; the pixel order is row-major here).
+    ``fused`` (2-D walk without a block order): one launch that forms each
+    pixel's ray in registers and walks it (tb_trace_camera) -- no rays in
+    HBM; bit-identical to the two-launch path (fused=False).
     Returns (TraceResult, cam_tet)."""
     dm = device_mesh(mesh, device=None if device is None else torch.device(device).index, layout=layout)
     dev = torch.device("cuda", dm.device)
@@ -167,6 +171,21 @@ def trace_camera(mesh, camera: dict, width: int, height: int, *, device=None, ou
         cam_tet = int(cam.item())
         if cam_tet < 0:
             raise ValueError("camera is outside the tetrahedralized volume")
+    if fused and not sctp and block_order is None:
+        from .scenes import camera_frame
+
+        frame = np.ascontiguousarray(camera_frame(camera["position"], camera["look_at"],
+                                                  camera.get("up", (0.0, 1.0, 0.0)), camera.get("fov", 68.0), width,
+                                                  height), dtype=np.float64)
+        res = out if out is not None else empty_result(width * height, dev)
+        if len(res) != width * height:
+            raise ValueError(f"out holds {len(res)} rays, the frame {width * height}")
+        s = (stream or torch.cuda.current_stream(dev)).cuda_stream
+        with torch.cuda.device(dev):
+            check(lib.tb_trace_camera(dm.handle, width, height, frame.ctypes.data, int(cam_tet), addr(res.status),
+                                      addr(res.cf), addr(res.tet), addr(res.visited), addr(res.triangle),
+                                      addr(res.t), addr(res.tet_back), s), "tb_trace_camera")
+        return res, cam_tet
     o, d = camera_rays_device(camera, width, height, dev, stream=stream)
     start = torch.full((o.shape[0],), cam_tet, dtype=torch.int32, device=dev)
     return trace(dm, o, d, start, out=out, stream=stream, sctp=sctp, block_order=block_order), cam_tet

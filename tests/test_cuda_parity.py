@@ -280,6 +280,44 @@ def test_device_camera_rays_and_trace_camera(digests):
     assert digest(*h[:4]) == digests["blob12/hilbert/cast"] and digest(*h[4:]) == digests["blob12/hilbert/epilogue"]
 
 
+@pytest.mark.parametrize("layout", ("tet16", "tet20", "tet32", "tet80"))
+def test_fused_camera_pass_equals_two_launch_path(layout):
+    """tb_trace_camera (the pixel's ray formed in registers, one launch) is
+    bit-identical to tb_camera_rays + the cast, for every layout, a ragged
+    frame (partial last block), device and pinned-host outputs; bad
+    arguments fail loudly."""
+    import torch
+
+    from paper_2103_02309_b200._lib import lib
+    from paper_2103_02309_b200.device import device_mesh
+    from paper_2103_02309_b200.scenes import BLOB_CAMERA, blob_scene
+    from paper_2103_02309_b200.trace import TraceResult, trace_camera
+
+    sc = blob_scene(12, scheme="hilbert")
+    for W, H in ((256, 256), (333, 217)):
+        a, cam = trace_camera(sc.mesh, BLOB_CAMERA, W, H, layout=layout, fused=False)
+        b, cam_b = trace_camera(sc.mesh, BLOB_CAMERA, W, H, layout=layout, cam_tet=cam)
+        host = TraceResult(*[torch.empty(W * H, dtype=x.dtype).pin_memory() for x in
+                             (a.status, a.cf, a.triangle, a.t, a.tet, a.tet_back, a.visited)])
+        trace_camera(sc.mesh, BLOB_CAMERA, W, H, layout=layout, cam_tet=cam, out=host)
+        torch.cuda.synchronize()
+        assert cam_b == cam
+        for k in NAMES7:
+            assert torch.equal(getattr(a, k), getattr(b, k)), (layout, W, H, k)
+            assert torch.equal(getattr(a, k).cpu(), getattr(host, k)), (layout, W, H, k)
+    dm = device_mesh(sc.mesh, device=0, layout=layout)
+    fr = np.zeros(14)
+    r = a
+    args = (fr.ctypes.data, 0, r.status.data_ptr(), r.cf.data_ptr(), r.tet.data_ptr(), r.visited.data_ptr(), None,
+            None, None, None)
+    assert lib.tb_trace_camera(dm.handle, 0, 4, *args) != 0
+    assert lib.tb_trace_camera(dm.handle, 4, 4, fr.ctypes.data, -1, *args[2:]) != 0
+    assert lib.tb_trace_camera(dm.handle, 4, 4, fr.ctypes.data, 1 << 30, *args[2:]) != 0
+    assert lib.tb_trace_camera(dm.handle, 4, 4, None, 0, *args[2:]) != 0
+    with pytest.raises(ValueError):
+        trace_camera(sc.mesh, BLOB_CAMERA, 8, 8, layout=layout, cam_tet=cam, out=a)  # wrong-size out
+
+
 def test_batch_layer_mirror(golden, K):
     """The mirrored batch API (batch.py:39-80 semantics) over the CUDA module."""
     from paper_2103_02309_b200 import batch
